@@ -86,7 +86,10 @@ def test_known_answers():
     assert math.exp(-O.SQRT_2PI) == pytest.approx(0.081543, abs=1e-6)
     # tomography centre ray of a unit Gaussian is sqrt(2 pi) (test_tomo.py:35-45)
     scene, cam, d = load_case("tomo_unit")
-    assert O.tomo_forward(scene, cam)[16, 16] == pytest.approx(O.SQRT_2PI, rel=1e-12)
+    # (theta is stored as float32, so kappa is 1 only to ~1e-7)
+    centre = O.tomo_forward(scene, cam)[16, 16]
+    assert centre == pytest.approx(O.SQRT_2PI, rel=1e-6)
+    assert centre == pytest.approx(d["tomo_image"][16, 16], rel=1e-13)
 
 
 def test_parallel_beam_matches_quadrature():
