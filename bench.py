@@ -1,0 +1,470 @@
+"""Benchmark: Mpixels/s of the analytic rasterizer's forward+backward step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config large]
+                    [--impl ours|reference] [--views V] [--no-e2e] [--no-cpu]
+
+Workload (default `--config large`, BASELINE.json configs[2], the config the
+north-star 1000x target is quoted on): N=1M Gaussians with SH-3 colour,
+64 cameras at 1920x1080.  One step = every view of the config rendered
+forward, L2 loss against a seeded target (fused into the backward blend),
+backward, per-Gaussian finalize with gradient accumulation over the views,
+and -- on N>1 GPUs -- one NCCL all-reduce of the flat gradient buffer.
+Views are sharded round-robin over ranks, so total work is fixed ("strong").
+
+`value` is device-timed with CUDA events (inputs resident in HBM), max over
+ranks.  `e2e` runs the same step through the public engine API with the
+scene and targets copied from pinned host memory and the gradients + loss
+copied back inside the timed region.  `roofline` is for the dominant kernel
+(measured live with CUDA events on the launch stream); its denominator is
+the FP32 / MUFU throughput probed on this GPU at its live clock.
+`cpu_baseline` is the float64 numpy oracle (a port of the reference path,
+oracle/) on a bounded, seeded sample of tiles of view 0, all host cores.
+`--impl reference` prints that CPU arm as the line itself.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixels/sec fwd+bwd (render+grad)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="large",
+                    choices=["tiny", "medium", "large", "opaque", "tomography"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--views", type=int, default=0, help="limit the number of views (0 = all)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tiles", type=int, default=0, help="tiles in the CPU sample (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_config(name, views):
+    from paper_2412_03378_b200 import configs
+    cfg = configs.BY_NAME[name]()
+    if views:
+        cfg.cameras = cfg.cameras[:views]
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def roofline_counts(n_act, n_con):
+    """Active / live pair-pixels of one view."""
+    return float(n_act.sum()), float(n_con.sum())
+
+
+# canonical per-unit costs (BASELINE.md section 4 / SURVEY 8(d))
+COST = {"render_fwd": (21.0, 3.0, 5.0), "render_bwd": (24.0, 4.0, 46.0)}
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_03378_b200 import _lib
+    from paper_2412_03378_b200.engine import Engine
+    from paper_2412_03378_b200.raster import DeviceScene
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = load_config(args.config, args.views)
+    tomo = cfg.tomography
+    my_views = list(range(rank, len(cfg.cameras), ws))
+    eng = Engine(local)
+    ds = eng.upload(cfg.scene)
+    grads = eng.new_grads(ds)
+    cams = cfg.cameras
+    H, W = int(cams[0].height), int(cams[0].width)
+    tshape = (H, W) if tomo else (H, W, 3)
+    targets = {v: torch.from_numpy(cfg.target(v, tshape)).to(dev) for v in my_views}
+    loss = torch.zeros((), dtype=torch.float64, device=dev)
+
+    def step(scene_dev, tgts, gbuf):
+        loss.zero_()
+        for j, v in enumerate(my_views):
+            cam = cams[v]
+            if tomo:
+                eng.prepare(scene_dev, cam, tomo=True, parallel=cfg.parallel, extent=cfg.extent)
+                img = eng.tomo_forward()
+                eng.tomo_backward_l2(img, tgts[v], gbuf, accumulate=j > 0, loss=loss)
+            else:
+                eng.prepare(scene_dev, cam)
+                color, tfin, _ = eng.forward()
+                eng.backward_l2(color, tfin, tgts[v], gbuf, accumulate=j > 0, loss=loss)
+        if ws > 1:
+            dist.all_reduce(gbuf.flat)
+            dist.all_reduce(loss)
+        return loss
+
+    for _ in range(args.warmup):
+        step(ds, targets, grads)
+    torch.cuda.synchronize()
+
+    fp32_peak = mufu_peak = None
+    import ctypes
+    fp, mu = ctypes.c_double(), ctypes.c_double()
+    if _lib.load().vg_probe_peaks(local, ctypes.byref(fp), ctypes.byref(mu)) == 0:
+        fp32_peak, mufu_peak = fp.value, mu.value
+
+    # --- timed region (device time, CUDA events on the launch stream)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng.ctx.profile(True)
+    l0 = eng.launches()
+    st = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        step(ds, targets, grads)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    launches = eng.launches() - l0
+    prof = eng.ctx.profile_read()
+    eng.ctx.profile(False)
+    clk = clocks.stop()
+    loss_val = float(loss) / (len(cams) * math.prod(tshape))
+    if ws > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t)
+        if ws > 1:
+            dist.barrier()
+    ms_step = ms_total / args.steps
+    px_step = len(cams) * H * W
+    value = px_step / (ms_step * 1e-3) / 1e6
+
+    # --- end to end: host buffers in, host buffers out
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step)
+
+    result = None
+    if rank == 0:
+        kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                   for k, v in prof.items() if v[1]}
+        roof = build_roofline(prof, args.steps, eng, ds, cams, my_views, tomo, cfg,
+                              fp32_peak, mufu_peak)
+        result = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpixels/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
+            "config": {"workload": f"config {'3' if args.config == 'large' else args.config}: "
+                                   + cfg.description,
+                       "views_per_step": len(cams), "pixels_per_step": px_step,
+                       "gaussians": len(cfg.scene), "parallelism": f"views sharded over {ws} GPU(s)",
+                       "l2_flush": "inputs larger than L2 (scene + SH coefficients > 126 MB)"},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "kernels": kernels,
+            "roofline": roof, "loss": loss_val,
+        }
+    return result
+
+
+def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step):
+    import torch
+    from paper_2412_03378_b200.raster import DeviceScene
+    s = cfg.scene
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(s, k))).pin_memory()
+            for k in ("means", "scales", "rotations", "thetas", "colors")}
+    if s.sh is not None:
+        host["sh"] = torch.from_numpy(np.ascontiguousarray(s.sh)).pin_memory()
+    htgt = {v: torch.from_numpy(cfg.target(v, tshape)).pin_memory() for v in my_views}
+    dev_scene = DeviceScene(cfg.scene, dev.index)
+    dtg = {v: torch.empty(tshape, dtype=torch.float32, device=dev) for v in my_views}
+    grads = eng.new_grads(dev_scene)
+    hgrad = torch.empty(grads.flat.shape, dtype=torch.float32).pin_memory()
+    hloss = torch.empty((), dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host.values()) + \
+        sum(t.numel() * t.element_size() for t in htgt.values())
+    d2h = hgrad.numel() * 4 + 8
+
+    def one():
+        for k, t in host.items():
+            getattr(dev_scene, k).copy_(t.view(getattr(dev_scene, k).shape), non_blocking=True)
+        for v in my_views:
+            dtg[v].copy_(htgt[v], non_blocking=True)
+        loss = step(dev_scene, dtg, grads)
+        hgrad.copy_(grads.flat, non_blocking=True)
+        hloss.copy_(loss, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        one()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    px = len(cfg.cameras) * int(cfg.cameras[0].height) * int(cfg.cameras[0].width)
+    return {"value": round(px / (ms * 1e-3) / 1e6, 3), "unit": "Mpixels/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms, 3)}
+
+
+def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak):
+    """Roofline of the dominant blend kernel from this run's CUDA-event times.
+    Algorithmic units: A = active pair-pixels, L = live pair-pixels of the
+    views of one step; counted in an untimed pass."""
+    import torch
+    if tomo:
+        return None
+    dom = max(("render_fwd", "render_bwd"), key=lambda k: prof.get(k, (0, 0))[0])
+    ms, cnt = prof[dom]
+    if not cnt:
+        return None
+    A = L = 0.0
+    for v in my_views:
+        eng.prepare(ds, cams[v])
+        _, _, nc = eng.forward()
+        na = eng.n_active()
+        A += float(na.double().sum())
+        L += float(nc.double().sum())
+    torch.cuda.synchronize()
+    fp_u, mu_u, live_u = COST[dom]
+    t = ms * 1e-3 / steps                       # seconds per step in this kernel
+    fp_ops = fp_u * A + live_u * L
+    mu_ops = mu_u * A
+    out = {"kernel": dom, "active_pair_pixels_per_step": A, "live_pair_pixels_per_step": L,
+           "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
+           "traffic": load_traffic(dom)}
+    if fp32_peak and mufu_peak:
+        f_fp = fp_ops / t / fp32_peak
+        f_mu = mu_ops / t / mufu_peak
+        if f_mu >= f_fp:
+            out.update(bound="sfu", achieved=mu_ops / t / 1e9, peak=mufu_peak / 1e9, unit="Gop/s (MUFU)",
+                       frac=f_mu)
+        else:
+            out.update(bound="fp32", achieved=fp_ops / t / 1e9, peak=fp32_peak / 1e9,
+                       unit="Ginstr/s (FP32 lane-ops)", frac=f_fp)
+        out["frac_fp32"] = f_fp
+        out["frac_mufu"] = f_mu
+        out["peak_source"] = "vg_probe_peaks on this GPU at the live clock (FFMA and MUFU.EX2 loops)"
+    return out
+
+
+def load_traffic(kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: float64 numpy oracle (port of the reference path) on sampled tiles
+
+
+def cpu_sample(cfg, n_tiles_target, seed=0, budget_s=25.0):
+    """Fwd+bwd Mpx/s of the oracle on a seeded sample of tiles of view 0,
+    using every host core; the per-view preprocessing cost is prorated."""
+    from oracle import volgauss_oracle as O
+    threads = os.cpu_count() or 1
+    s = cfg.scene
+    cam = cfg.cameras[0]
+    from types import SimpleNamespace
+    scene = SimpleNamespace(means=s.means.astype(np.float64), scales=s.scales.astype(np.float64),
+                            rotations=s.rotations.astype(np.float64), thetas=s.thetas.astype(np.float64),
+                            colors=s.colors.astype(np.float64), background=np.zeros(3))
+    t0 = time.perf_counter()
+    if cfg.tomography:
+        prep = O.tomo_prepare(scene, cam, cfg.parallel, cfg.extent)
+    else:
+        prep = O.prepare(scene, cam)
+    t_prep = time.perf_counter() - t0
+    n_all = prep.tiles_x * prep.tiles_y
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(n_all)
+    H, W = cam.height, cam.width
+    tshape = (H, W) if cfg.tomography else (H, W, 3)
+    target = cfg.target(0, tshape).astype(np.float64)
+    done_px = 0
+    t_work = 0.0
+    used = []
+    for start in range(0, n_all, max(threads, 8)):
+        chunk = [int(t) for t in order[start:start + max(threads, 8)]]
+        t1 = time.perf_counter()
+        if cfg.tomography:
+            img = O.tomo_forward(scene, cam, prep=prep, threads=threads, tiles=chunk)
+            mask = _tile_mask(prep, chunk, H, W)
+            O.tomo_backward(scene, cam, 2 * (img - target) * mask / (H * W), prep=prep,
+                            threads=threads, tiles=chunk)
+        else:
+            img = O.render(scene, cam, prep=prep, threads=threads, tiles=chunk)
+            mask = _tile_mask(prep, chunk, H, W)[..., None]
+            O.backward(scene, cam, 2 * (img.color - target) * mask / (H * W * 3), prep=prep,
+                       tiles=chunk, threads=threads)
+        t_work += time.perf_counter() - t1
+        used += chunk
+        done_px += sum(_tile_px(prep, t, H, W) for t in chunk)
+        if (n_tiles_target and len(used) >= n_tiles_target) or t_work > budget_s:
+            break
+    frac = done_px / (H * W)
+    t_eff = t_work + t_prep * frac
+    return {"value": done_px / t_eff / 1e6, "unit": "Mpixels/s", "cores": threads, "kind": "port",
+            "sample": (f"{len(used)} seeded-random 16x16 tiles ({done_px} px) of view 0 of "
+                       f"{cfg.name}, fwd+bwd, float64 numpy oracle/ (port of raster/grad"
+                       f"{'/tomo' if cfg.tomography else ''}.py); per-view prepare "
+                       f"{t_prep:.1f}s prorated by pixel fraction"),
+            "seconds": round(t_eff, 2)}
+
+
+def _tile_px(prep, t, H, W):
+    ty, tx = divmod(t, prep.tiles_x)
+    return min(16, H - ty * 16) * min(16, W - tx * 16)
+
+
+def _tile_mask(prep, tiles, H, W):
+    m = np.zeros((H, W))
+    for t in tiles:
+        ty, tx = divmod(t, prep.tiles_x)
+        m[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = 1.0
+    return m
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    cfg = load_config(args.config, args.views)
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(cfg, args.cpu_tiles or 16, seed=i, budget_s=20.0)
+        if i >= args.warmup:
+            samples.append(r)
+    val = statistics.mean(r["value"] for r in samples)
+    ms_step = len(cfg.cameras) * cfg.cameras[0].height * cfg.cameras[0].width / (val * 1e6) * 1e3
+    return {"metric": METRIC, "value": round(val, 6), "unit": "Mpixels/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
+            "impl": "reference",
+            "config": {"workload": f"config {'3' if args.config == 'large' else args.config}: "
+                                   + cfg.description, "views_per_step": len(cfg.cameras)},
+            "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(val, 6)},
+            "e2e": {"value": round(val, 6), "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res))
+        return
+    res = run_gpu(args)
+    ws, rank, _ = dist_env()
+    if rank == 0:
+        if not args.no_cpu and ws == 1:
+            cfg = load_config(args.config, args.views)
+            res["cpu_baseline"] = cpu_sample(cfg, args.cpu_tiles or 0, budget_s=15.0)
+        print(json.dumps(res))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

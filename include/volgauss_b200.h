@@ -1,0 +1,200 @@
+/*
+ * volgauss_b200 -- C ABI of the B200-native (sm_100a) analytic-transmittance
+ * Gaussian rasterizer (arXiv 2412.03378).
+ *
+ * This is the drop-in boundary for the reference package `volgauss` 0.1.0,
+ * whose hot path is the Python API in pkg/src/volgauss/{raster,grad,tomo}.py.
+ * The reference has no FFI of its own (it is pure numpy); each entry point
+ * below replaces one reference call, cited as file:line relative to
+ * /root/reference/pkg/src/volgauss/.  The Python facade
+ * (paper_2412_03378_b200/{raster,grad,tomo}.py) binds these symbols through
+ * ctypes and keeps the reference signatures; INTEGRATION.md shows the
+ * binding.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *    storage), float32 struct-of-arrays in the reference field order:
+ *    means N*3, scales N*3, rotations N*4 (w,x,y,z; need not be unit),
+ *    thetas N, colors N*3.  Images are row-major (H, W[, 3]).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *    Every call is stream-ordered; nothing synchronises the host except
+ *    vg_pair_count (which reads the pair count back).
+ *  - Return codes: VG_OK, VG_EINVAL (bad argument -> the facade raises
+ *    ValueError like raster.py:268-269, 293-294), VG_ECUDA (CUDA error ->
+ *    RuntimeError), VG_ENOMEM.  vg_last_error() returns a thread-local
+ *    message for the last failing call on this thread.
+ *  - A context is not thread-safe; use one per (device, stream).  It owns
+ *    the preprocessed records, the sorted tile lists and the per-pixel
+ *    forward state that backward reuses (the reference's `prep`,
+ *    raster.py:123-145, reused by optim.py:379-386).
+ */
+#ifndef VOLGAUSS_B200_H
+#define VOLGAUSS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VG_ABI_VERSION 1
+
+#define VG_OK 0
+#define VG_EINVAL 1
+#define VG_ECUDA 2
+#define VG_ENOMEM 3
+
+/* ray models */
+#define VG_PINHOLE 0  /* camera.Camera pinhole rays from the centre (camera.py:57-64) */
+#define VG_PARALLEL 1 /* orthographic detector of half-width `extent` (tomo.py:272-282) */
+
+typedef struct vg_context vg_context;
+
+/* camera.Camera (camera.py:14-48): x_view = R x_world + t */
+typedef struct {
+  int32_t width, height;
+  int32_t projection; /* VG_PINHOLE or VG_PARALLEL */
+  int32_t _pad;
+  double fx, fy, cx, cy;
+  double rotation[9]; /* row-major */
+  double translation[3];
+  double z_near;
+  double extent; /* parallel detector half-width (world units) */
+} vg_camera;
+
+/* render()/backward() keyword flags (raster.py:26-35, 410-413) */
+typedef struct {
+  int32_t tile_size;   /* only 16 is supported (raster.TILE_SIZE) */
+  int32_t _pad;
+  double early_stop;   /* <= 0 disables early termination (early_stop=None) */
+  double alpha_cut;    /* <= 0 disables the alpha skip (alpha_cut=0) */
+  double alpha_clamp;  /* raster.ALPHA_CLAMP */
+  double bin_cut;      /* alpha_cut used for bin radii: raster.prepare's
+                          alpha_cut, or tomo.TOMO_BIN_CUT (tomo.py:28) */
+} vg_options;
+
+/* raster.Scene (raster.py:38-97) as device float32 SoA */
+typedef struct {
+  const float* means;
+  const float* scales;
+  const float* rotations;
+  const float* thetas;
+  const float* colors;  /* may be NULL for tomography */
+  const float* sh;      /* optional N*16*3 SH-3 coefficients; when set, colors
+                           are evaluated per view from sh (DC band = RGB) */
+  int64_t n;
+  double background[3];
+} vg_scene;
+
+/* grad.SceneGrads (grad.py:41-69) as device pointers.  Any pointer may be
+ * NULL to skip that output.  With accumulate != 0 the results are ADDED to
+ * the existing contents (multi-view gradient accumulation); otherwise they
+ * overwrite. */
+typedef struct {
+  float* d_means;      /* N*3 */
+  float* d_scales;     /* N*3 */
+  float* d_rotations;  /* N*4 */
+  float* d_thetas;     /* N   */
+  float* d_colors;     /* N*3 */
+  float* d_kappas;     /* N   */
+  float* d_sh;         /* N*48, only with vg_scene.sh */
+  float* d_background; /* 3   */
+  uint8_t* visible;    /* N   (OR-accumulated) */
+  int32_t accumulate;
+  int32_t _pad;
+} vg_grads;
+
+/* lifecycle */
+int vg_abi_version(void);
+const char* vg_last_error(void);
+int vg_create(vg_context** out, int32_t device);
+void vg_destroy(vg_context* ctx);
+
+/* raster.prepare (raster.py:263-296) / bin_tiles (raster.py:315-319):
+ * per-Gaussian projection, bounding radius and tile rectangle
+ * (_project_all/_bounding_radii, raster.py:154-209), blend records,
+ * tile-pair duplication, 64-bit (tile, depth) radix sort and per-tile ranges
+ * (_build_grid, raster.py:222-260).  The scene pointers must stay valid
+ * until the matching backward has run. */
+int vg_prepare(vg_context* ctx, const vg_scene* scene, const vg_camera* cam,
+               const vg_options* opt, void* stream);
+
+/* Update the blend flags (early_stop, alpha_cut, alpha_clamp) of a prepared
+ * context without re-binning -- render(prep=...) may pass flags that differ
+ * from prepare's (raster.py:410-418).  bin_cut and tile_size are ignored. */
+int vg_set_options(vg_context* ctx, const vg_options* opt);
+
+/* Number of (tile, primitive) pairs of the last vg_prepare (synchronises). */
+int vg_pair_count(vg_context* ctx, int64_t* out_pairs);
+
+/* TileGrid.tiles (raster.py:100-112): the sorted per-tile primitive lists,
+ * flattened.  prims: device int32[pairs]; offsets: device int32[n_tiles+1]. */
+int vg_tile_lists(vg_context* ctx, int32_t* prims, int32_t* offsets, void* stream);
+
+/* raster.render (raster.py:410-439), analytic mode: color (H,W,3),
+ * final_transmittance (H,W), n_contrib (H,W). */
+int vg_render_forward(vg_context* ctx, float* color, float* final_t, int32_t* n_contrib,
+                      void* stream);
+
+/* grad.backward (grad.py:107-213), analytic mode.  color/final_t are the
+ * outputs of the matching vg_render_forward; d_color (H,W,3) and optional
+ * d_transmittance (H,W) are dL/d(outputs). */
+int vg_render_backward(vg_context* ctx, const float* color, const float* final_t,
+                       const float* d_color, const float* d_transmittance, vg_grads* grads,
+                       void* stream);
+
+/* Fused L2 training step: grad.loss_and_grad(l2) (grad.py:346-348) folded
+ * into the backward blend.  dL/dcolor = 2 (color - target) / (H*W*3) is
+ * formed per pixel in the kernel and sum((color-target)^2) is ADDED to
+ * *loss_sum (device float64). */
+int vg_render_backward_l2(vg_context* ctx, const float* color, const float* final_t,
+                          const float* target, double* loss_sum, vg_grads* grads,
+                          void* stream);
+
+/* Per-pixel count of composited (active) entries of the last forward,
+ * int32 (H,W) -- the backward replay bound, also the roofline's A count. */
+int vg_n_active(vg_context* ctx, int32_t* out, void* stream);
+
+/* tomo.tomo_forward (tomo.py:34-57): line-integral image (H,W).  Pass
+ * intensity != NULL to also write exp(-image). */
+int vg_tomo_forward(vg_context* ctx, float* image, float* intensity, void* stream);
+
+/* tomo.tomo_backward (tomo.py:60-103): gradients of sum(d_image * image). */
+int vg_tomo_backward(vg_context* ctx, const float* d_image, vg_grads* grads, void* stream);
+
+/* Fused tomography L2 step: d_image = 2 (image - target) / (H*W) in-kernel,
+ * sum((image-target)^2) added to *loss_sum. */
+int vg_tomo_backward_l2(vg_context* ctx, const float* image, const float* target,
+                        double* loss_sum, vg_grads* grads, void* stream);
+
+/* Number of kernels this context launched since creation (bench accounting). */
+int64_t vg_launch_count(vg_context* ctx);
+
+/* Per-kernel device timing with CUDA events recorded on the launch stream.
+ * vg_profile(ctx, 1) clears and enables, (ctx, 0) disables.  vg_profile_read
+ * waits for the recorded events and returns, per kernel kind (VG_K_*),
+ * the summed milliseconds and launch counts (arrays of VG_K_COUNT). */
+#define VG_K_PREPROCESS 0
+#define VG_K_SCAN 1
+#define VG_K_DUPLICATE 2
+#define VG_K_SORT 3
+#define VG_K_RANGES 4
+#define VG_K_RENDER_FWD 5
+#define VG_K_RENDER_BWD 6
+#define VG_K_FINALIZE 7
+#define VG_K_TOMO_FWD 8
+#define VG_K_TOMO_BWD 9
+#define VG_K_COUNT 10
+int vg_profile(vg_context* ctx, int32_t enable);
+int vg_profile_read(vg_context* ctx, double* ms, int64_t* counts);
+
+/* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and
+ * MUFU ex2 ops/s over all SMs of `device`. */
+int vg_probe_peaks(int32_t device, double* fp32_per_s, double* mufu_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VOLGAUSS_B200_H */

@@ -1,0 +1,521 @@
+// The C ABI (include/volgauss_b200.h): context management and orchestration
+// of the kernel pipeline  K1 preprocess -> scan -> K2 duplicate -> K3 radix
+// sort -> K4 ranges -> K5/K6/K8 tile kernels -> K7 finalize.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vg_kernels.cuh"
+
+using namespace vg;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define VG_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(VG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+#define VG_LAUNCHED(ctx, k)                                                                \
+  do {                                                                                     \
+    (ctx)->launches += (k);                                                                \
+    cudaError_t _e = cudaGetLastError();                                                   \
+    if (_e != cudaSuccess) return fail(VG_ECUDA, std::string("launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct vg_context {
+  int device = 0;
+  int64_t launches = 0;
+  // per-Gaussian
+  Buf rec, depth, rect, count, offset, acc;
+  // per-pair (double-buffered for the radix sort)
+  Buf keys0, keys1, vals0, vals1;
+  Buf ranges, n_act, scan_tmp, sort_tmp, total;
+  uint64_t* total_host = nullptr;
+  // state of the last prepare
+  vg_scene scene{};
+  CamK cam{};
+  vg_options opt{};
+  int64_t pairs = 0;
+  int n_tiles = 0;
+  uint64_t* keys = nullptr;  // sorted buffers
+  uint32_t* vals = nullptr;
+  bool prepared = false;
+  bool have_fwd = false;
+  // event profiling (vg_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  struct Mark { int kind; cudaEvent_t a, b; };
+  std::vector<Mark> marks;
+};
+
+static cudaEvent_t pool_event(vg_context* c) {
+  if (c->pool_used == c->pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_used++];
+}
+
+// Bracket a launch with events when profiling is on.
+struct ProfScope {
+  vg_context* c;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(vg_context* c_, int k, cudaStream_t s) : c(c_), kind(k), st(s) {
+    if (c->prof && (a = pool_event(c))) cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = pool_event(c);
+    if (!b) return;
+    cudaEventRecord(b, st);
+    c->marks.push_back({kind, a, b});
+  }
+};
+
+static int ensure(Buf& b, size_t bytes, cudaStream_t st, bool zero = false) {
+  if (b.bytes >= bytes && b.p) return VG_OK;
+  if (b.p) VG_CUDA(cudaFreeAsync(b.p, st));
+  size_t want = bytes + bytes / 4 + 256;
+  VG_CUDA(cudaMallocAsync(&b.p, want, st));
+  b.bytes = want;
+  if (zero) VG_CUDA(cudaMemsetAsync(b.p, 0, want, st));
+  return VG_OK;
+}
+
+#define VG_TRY(x)                 \
+  do {                            \
+    int _r = (x);                 \
+    if (_r != VG_OK) return _r;   \
+  } while (0)
+
+extern "C" {
+
+int vg_abi_version(void) { return VG_ABI_VERSION; }
+
+const char* vg_last_error(void) { return g_err.c_str(); }
+
+int vg_create(vg_context** out, int32_t device) {
+  if (!out) return fail(VG_EINVAL, "vg_create: out is NULL");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(VG_ECUDA, "vg_create: no CUDA device");
+  if (device < 0 || device >= count) return fail(VG_EINVAL, "vg_create: bad device index");
+  VG_CUDA(cudaSetDevice(device));
+  vg_context* c = new vg_context();
+  c->device = device;
+  // keep freed stream-ordered allocations cached in the device pool
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  if (cudaMallocHost(&c->total_host, sizeof(uint64_t)) != cudaSuccess) {
+    delete c;
+    return fail(VG_ENOMEM, "vg_create: pinned alloc failed");
+  }
+  *out = c;
+  return VG_OK;
+}
+
+void vg_destroy(vg_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
+                &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
+                &c->sort_tmp, &c->total};
+  for (Buf* b : all)
+    if (b->p) cudaFree(b->p);
+  if (c->total_host) cudaFreeHost(c->total_host);
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  delete c;
+}
+
+int64_t vg_launch_count(vg_context* c) { return c ? c->launches : 0; }
+
+int vg_profile(vg_context* c, int32_t enable) {
+  if (!c) return fail(VG_EINVAL, "vg_profile: NULL context");
+  c->prof = enable != 0;
+  if (enable) {
+    c->marks.clear();
+    c->pool_used = 0;
+  }
+  return VG_OK;
+}
+
+int vg_profile_read(vg_context* c, double* ms, int64_t* counts) {
+  if (!c || !ms || !counts) return fail(VG_EINVAL, "vg_profile_read: NULL argument");
+  for (int k = 0; k < VG_K_COUNT; ++k) { ms[k] = 0.0; counts[k] = 0; }
+  for (const auto& m : c->marks) {
+    VG_CUDA(cudaEventSynchronize(m.b));
+    float t = 0.f;
+    VG_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    ms[m.kind] += t;
+    counts[m.kind] += 1;
+  }
+  return VG_OK;
+}
+
+static int make_cam(const vg_camera* cam, CamK& k) {
+  if (!cam) return fail(VG_EINVAL, "camera is NULL");
+  if (cam->width <= 0 || cam->height <= 0) return fail(VG_EINVAL, "camera size must be positive");
+  if (cam->projection != VG_PINHOLE && cam->projection != VG_PARALLEL)
+    return fail(VG_EINVAL, "unknown projection");
+  if (cam->projection == VG_PINHOLE && (!(cam->fx > 0) || !(cam->fy > 0)))
+    return fail(VG_EINVAL, "focal lengths must be positive");
+  if (cam->projection == VG_PARALLEL && !(cam->extent > 0))
+    return fail(VG_EINVAL, "parallel detector extent must be positive");
+  k.width = cam->width;
+  k.height = cam->height;
+  k.ntx = (cam->width + TILE - 1) / TILE;
+  k.nty = (cam->height + TILE - 1) / TILE;
+  k.projection = cam->projection;
+  k.fx = cam->fx; k.fy = cam->fy; k.cx = cam->cx; k.cy = cam->cy;
+  k.z_near = cam->z_near;
+  k.extent = cam->extent;
+  for (int i = 0; i < 9; ++i) k.R[i] = cam->rotation[i];
+  for (int i = 0; i < 3; ++i) k.t[i] = cam->translation[i];
+  for (int j = 0; j < 3; ++j)  // centre = -R^T t
+    k.center[j] = -(k.R[0 * 3 + j] * k.t[0] + k.R[1 * 3 + j] * k.t[1] + k.R[2 * 3 + j] * k.t[2]);
+  return VG_OK;
+}
+
+int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_options* opt,
+               void* stream) {
+  if (!c || !s || !opt) return fail(VG_EINVAL, "vg_prepare: NULL argument");
+  if (opt->tile_size != TILE) return fail(VG_EINVAL, "only tile_size=16 is supported");
+  if (s->n < 0) return fail(VG_EINVAL, "negative primitive count");
+  if (s->n > 0x7fffffff) return fail(VG_EINVAL, "too many primitives (> 2^31-1)");
+  if (s->n > 0 && (!s->means || !s->scales || !s->rotations || !s->thetas))
+    return fail(VG_EINVAL, "scene arrays must be non-NULL");
+  CamK k;
+  VG_TRY(make_cam(cam, k));
+  cudaStream_t st = (cudaStream_t)stream;
+  VG_CUDA(cudaSetDevice(c->device));
+  const int64_t n = s->n;
+  c->scene = *s;
+  c->cam = k;
+  c->opt = *opt;
+  c->n_tiles = k.ntx * k.nty;
+  c->prepared = false;
+  c->have_fwd = false;
+  const int64_t npix = (int64_t)k.width * k.height;
+  VG_TRY(ensure(c->ranges, sizeof(uint2) * (size_t)c->n_tiles, st));
+  VG_TRY(ensure(c->n_act, sizeof(int) * (size_t)npix, st));
+  VG_TRY(ensure(c->total, sizeof(uint64_t), st));
+  VG_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->n_tiles, st));
+  c->pairs = 0;
+  if (n > 0) {
+    size_t accb = sizeof(float) * 16 * (size_t)n;
+    bool grow_acc = c->acc.bytes < accb;
+    VG_TRY(ensure(c->rec, sizeof(GRec) * (size_t)n, st));
+    VG_TRY(ensure(c->depth, sizeof(float) * (size_t)n, st));
+    VG_TRY(ensure(c->rect, sizeof(int4) * (size_t)n, st));
+    VG_TRY(ensure(c->count, sizeof(uint32_t) * (size_t)n, st));
+    VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)n, st));
+    if (grow_acc) VG_TRY(ensure(c->acc, accb, st, true));
+    {
+      ProfScope ps(c, VG_K_PREPROCESS, st);
+      launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
+                        (int4*)c->rect.p, (uint32_t*)c->count.p, st);
+    }
+    VG_LAUNCHED(c, 1);
+    size_t tmp = 0;
+    VG_CUDA(scan_temp_bytes(n, &tmp));
+    VG_TRY(ensure(c->scan_tmp, tmp, st));
+    {
+      ProfScope ps(c, VG_K_SCAN, st);
+      VG_CUDA(exclusive_scan(c->scan_tmp.p, c->scan_tmp.bytes, (const uint32_t*)c->count.p,
+                             (uint32_t*)c->offset.p, n, st));
+    }
+    VG_LAUNCHED(c, 1);
+    launch_total(n, (const uint32_t*)c->count.p, (const uint32_t*)c->offset.p,
+                 (uint64_t*)c->total.p, st);
+    VG_LAUNCHED(c, 1);
+    VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    VG_CUDA(cudaStreamSynchronize(st));
+    uint64_t P = *c->total_host;
+    if (P > 0xffffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^32");
+    c->pairs = (int64_t)P;
+  }
+  const int64_t P = c->pairs;
+  if (P > 0) {
+    VG_TRY(ensure(c->keys0, sizeof(uint64_t) * (size_t)P, st));
+    VG_TRY(ensure(c->keys1, sizeof(uint64_t) * (size_t)P, st));
+    VG_TRY(ensure(c->vals0, sizeof(uint32_t) * (size_t)P, st));
+    VG_TRY(ensure(c->vals1, sizeof(uint32_t) * (size_t)P, st));
+    {
+      ProfScope ps(c, VG_K_DUPLICATE, st);
+      launch_duplicate(n, (const uint32_t*)c->count.p, (const uint32_t*)c->offset.p,
+                       (const int4*)c->rect.p, (const float*)c->depth.p, k.ntx,
+                       (uint64_t*)c->keys0.p, (uint32_t*)c->vals0.p, st);
+    }
+    VG_LAUNCHED(c, 1);
+    int tile_bits = 0;
+    while ((1 << tile_bits) < c->n_tiles) ++tile_bits;
+    int end_bit = 32 + tile_bits;
+    size_t tmp = 0;
+    VG_CUDA(sort_temp_bytes(P, end_bit, &tmp));
+    VG_TRY(ensure(c->sort_tmp, tmp, st));
+    int which = 0;
+    {
+      ProfScope ps(c, VG_K_SORT, st);
+      VG_CUDA(radix_sort_pairs(c->sort_tmp.p, c->sort_tmp.bytes, (uint64_t*)c->keys0.p,
+                               (uint64_t*)c->keys1.p, (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p,
+                               P, end_bit, &which, st));
+    }
+    c->launches += sort_launches(end_bit);
+    c->keys = which ? (uint64_t*)c->keys1.p : (uint64_t*)c->keys0.p;
+    c->vals = which ? (uint32_t*)c->vals1.p : (uint32_t*)c->vals0.p;
+    {
+      ProfScope ps(c, VG_K_RANGES, st);
+      launch_ranges(P, c->keys, (uint2*)c->ranges.p, st);
+    }
+    VG_LAUNCHED(c, 1);
+  } else {
+    c->keys = nullptr;
+    c->vals = nullptr;
+  }
+  c->prepared = true;
+  return VG_OK;
+}
+
+int vg_set_options(vg_context* c, const vg_options* opt) {
+  if (!c || !opt) return fail(VG_EINVAL, "vg_set_options: NULL argument");
+  c->opt.early_stop = opt->early_stop;
+  c->opt.alpha_cut = opt->alpha_cut;
+  c->opt.alpha_clamp = opt->alpha_clamp;
+  return VG_OK;
+}
+
+int vg_pair_count(vg_context* c, int64_t* out) {
+  if (!c || !out) return fail(VG_EINVAL, "vg_pair_count: NULL argument");
+  if (!c->prepared) return fail(VG_EINVAL, "vg_pair_count: call vg_prepare first");
+  *out = c->pairs;
+  return VG_OK;
+}
+
+__global__ void k_tile_lists(int64_t P, const uint64_t* keys, const uint32_t* vals,
+                             const uint2* ranges, int n_tiles, int32_t* prims, int32_t* offsets) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) prims[i] = (int32_t)vals[i];
+  if (i <= n_tiles) {
+    // offsets[t] = start of tile t; empty tiles take the next non-empty start
+    if (i == n_tiles) {
+      offsets[i] = (int32_t)P;
+    } else {
+      uint2 r = ranges[i];
+      if (r.y > r.x) {
+        offsets[i] = (int32_t)r.x;
+      } else {
+        int64_t t = i + 1;
+        uint32_t nxt = (uint32_t)P;
+        while (t < n_tiles) {
+          uint2 q = ranges[t];
+          if (q.y > q.x) { nxt = q.x; break; }
+          ++t;
+        }
+        offsets[i] = (int32_t)nxt;
+      }
+    }
+  }
+}
+
+int vg_tile_lists(vg_context* c, int32_t* prims, int32_t* offsets, void* stream) {
+  if (!c || !offsets) return fail(VG_EINVAL, "vg_tile_lists: NULL argument");
+  if (!c->prepared) return fail(VG_EINVAL, "vg_tile_lists: call vg_prepare first");
+  if (c->pairs > 0 && !prims) return fail(VG_EINVAL, "vg_tile_lists: prims is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t work = c->pairs > c->n_tiles + 1 ? c->pairs : c->n_tiles + 1;
+  k_tile_lists<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
+      c->pairs, c->keys, c->vals, (const uint2*)c->ranges.p, c->n_tiles, prims, offsets);
+  VG_LAUNCHED(c, 1);
+  return VG_OK;
+}
+
+static BlendParams blend_params(const vg_context* c) {
+  BlendParams p;
+  p.width = c->cam.width;
+  p.height = c->cam.height;
+  p.ntx = c->cam.ntx;
+  p.cx = (float)c->cam.cx;
+  p.cy = (float)c->cam.cy;
+  p.fx = (float)(c->cam.fx > 0 ? c->cam.fx : 1.0);
+  p.fy = (float)(c->cam.fy > 0 ? c->cam.fy : 1.0);
+  p.stop = (float)c->opt.early_stop;
+  p.cut = (float)c->opt.alpha_cut;
+  p.clamp = (float)c->opt.alpha_clamp;
+  for (int i = 0; i < 3; ++i) p.bg[i] = (float)c->scene.background[i];
+  return p;
+}
+
+int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_contrib,
+                      void* stream) {
+  if (!c || !color || !final_t || !n_contrib) return fail(VG_EINVAL, "vg_render_forward: NULL argument");
+  if (!c->prepared) return fail(VG_EINVAL, "vg_render_forward: call vg_prepare first");
+  if (c->cam.projection != VG_PINHOLE) return fail(VG_EINVAL, "render needs a pinhole camera");
+  cudaStream_t st = (cudaStream_t)stream;
+  BlendParams p = blend_params(c);
+  {
+    ProfScope ps(c, VG_K_RENDER_FWD, st);
+    launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p, p,
+                      c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
+                      (int*)c->n_act.p, st);
+  }
+  VG_LAUNCHED(c, 1);
+  c->have_fwd = true;
+  return VG_OK;
+}
+
+int vg_n_active(vg_context* c, int32_t* out, void* stream) {
+  if (!c || !out) return fail(VG_EINVAL, "vg_n_active: NULL argument");
+  if (!c->have_fwd) return fail(VG_EINVAL, "vg_n_active: no forward on this context");
+  size_t bytes = sizeof(int32_t) * (size_t)c->cam.width * (size_t)c->cam.height;
+  VG_CUDA(cudaMemcpyAsync(out, c->n_act.p, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return VG_OK;
+}
+
+static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
+  if (!g) return fail(VG_EINVAL, "grads is NULL");
+  if (!g->accumulate) {
+    if (g->d_background) VG_CUDA(cudaMemsetAsync(g->d_background, 0, 3 * sizeof(float), st));
+    if (g->visible && c->scene.n) VG_CUDA(cudaMemsetAsync(g->visible, 0, (size_t)c->scene.n, st));
+  }
+  return VG_OK;
+}
+
+static int render_bwd_common(vg_context* c, const float* color, const float* final_t,
+                             const float* d_color, const float* d_t, const float* target,
+                             double* loss_sum, vg_grads* g, void* stream) {
+  if (!c || !color || !final_t) return fail(VG_EINVAL, "vg_render_backward: NULL argument");
+  if (!c->prepared || !c->have_fwd)
+    return fail(VG_EINVAL, "vg_render_backward: run vg_render_forward on this context first");
+  cudaStream_t st = (cudaStream_t)stream;
+  VG_TRY(prep_grads(c, g, st));
+  BlendParams p = blend_params(c);
+  BwdIO io;
+  io.color = color;
+  io.final_t = final_t;
+  io.n_act = (const int*)c->n_act.p;
+  io.d_color = d_color;
+  io.d_t = d_t;
+  io.target = target;
+  io.loss_scale = (float)(2.0 / (3.0 * (double)c->cam.width * (double)c->cam.height));
+  io.loss_sum = loss_sum;
+  io.acc = (float*)c->acc.p;
+  io.visible = g->visible;
+  io.d_background = g->d_background;
+  if (!io.visible) {
+    // visibility is always tracked; route it to scratch when not requested
+    VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)(c->scene.n > 0 ? c->scene.n : 1), st));
+    io.visible = (uint8_t*)c->offset.p;
+  }
+  if (c->scene.n > 0) {
+    {
+      ProfScope ps(c, VG_K_RENDER_BWD, st);
+      launch_render_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p, p,
+                        c->opt.alpha_cut > 0, target ? 1 : 0, io, st);
+    }
+    VG_LAUNCHED(c, 1);
+    {
+      ProfScope ps(c, VG_K_FINALIZE, st);
+      launch_finalize(c->scene.n, c->scene, c->cam, (float*)c->acc.p, *g, st);
+    }
+    VG_LAUNCHED(c, 1);
+  } else {
+    // empty scene: d_background = sum of d_color (grad.py:126-128) -- the
+    // blend kernel still runs over the (empty) tiles to form it.
+    launch_render_bwd(c->n_tiles, nullptr, nullptr, (const uint2*)c->ranges.p, p, false,
+                      target ? 1 : 0, io, st);
+    VG_LAUNCHED(c, 1);
+  }
+  return VG_OK;
+}
+
+int vg_render_backward(vg_context* c, const float* color, const float* final_t,
+                       const float* d_color, const float* d_t, vg_grads* g, void* stream) {
+  if (!d_color) return fail(VG_EINVAL, "vg_render_backward: d_color is NULL");
+  return render_bwd_common(c, color, final_t, d_color, d_t, nullptr, nullptr, g, stream);
+}
+
+int vg_render_backward_l2(vg_context* c, const float* color, const float* final_t,
+                          const float* target, double* loss_sum, vg_grads* g, void* stream) {
+  if (!target || !loss_sum) return fail(VG_EINVAL, "vg_render_backward_l2: NULL argument");
+  return render_bwd_common(c, color, final_t, nullptr, nullptr, target, loss_sum, g, stream);
+}
+
+int vg_tomo_forward(vg_context* c, float* image, float* intensity, void* stream) {
+  if (!c || !image) return fail(VG_EINVAL, "vg_tomo_forward: NULL argument");
+  if (!c->prepared) return fail(VG_EINVAL, "vg_tomo_forward: call vg_prepare first");
+  cudaStream_t st = (cudaStream_t)stream;
+  BlendParams p = blend_params(c);
+  {
+    ProfScope ps(c, VG_K_TOMO_FWD, st);
+    launch_tomo_fwd(c->n_tiles, c->cam.projection, (const GRec*)c->rec.p, c->vals,
+                    (const uint2*)c->ranges.p, p, image, intensity, st);
+  }
+  VG_LAUNCHED(c, 1);
+  return VG_OK;
+}
+
+static int tomo_bwd_common(vg_context* c, const float* d_image, const float* image,
+                           const float* target, double* loss_sum, vg_grads* g, void* stream) {
+  if (!c->prepared) return fail(VG_EINVAL, "vg_tomo_backward: call vg_prepare first");
+  cudaStream_t st = (cudaStream_t)stream;
+  VG_TRY(prep_grads(c, g, st));
+  BlendParams p = blend_params(c);
+  uint8_t* vis = g->visible;
+  if (!vis) {
+    VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)(c->scene.n > 0 ? c->scene.n : 1), st));
+    vis = (uint8_t*)c->offset.p;
+  }
+  float scale = (float)(2.0 / ((double)c->cam.width * (double)c->cam.height));
+  {
+    ProfScope ps(c, VG_K_TOMO_BWD, st);
+    launch_tomo_bwd(c->n_tiles, c->cam.projection, target ? 1 : 0, (const GRec*)c->rec.p, c->vals,
+                    (const uint2*)c->ranges.p, p, d_image, image, target, scale, loss_sum,
+                    (float*)c->acc.p, vis, st);
+  }
+  VG_LAUNCHED(c, 1);
+  if (c->scene.n > 0) {
+    {
+      ProfScope ps(c, VG_K_FINALIZE, st);
+      launch_finalize(c->scene.n, c->scene, c->cam, (float*)c->acc.p, *g, st);
+    }
+    VG_LAUNCHED(c, 1);
+  }
+  return VG_OK;
+}
+
+int vg_tomo_backward(vg_context* c, const float* d_image, vg_grads* g, void* stream) {
+  if (!c || !d_image) return fail(VG_EINVAL, "vg_tomo_backward: NULL argument");
+  return tomo_bwd_common(c, d_image, nullptr, nullptr, nullptr, g, stream);
+}
+
+int vg_tomo_backward_l2(vg_context* c, const float* image, const float* target, double* loss_sum,
+                        vg_grads* g, void* stream) {
+  if (!c || !image || !target || !loss_sum) return fail(VG_EINVAL, "vg_tomo_backward_l2: NULL argument");
+  return tomo_bwd_common(c, nullptr, image, target, loss_sum, g, stream);
+}
+
+}  // extern "C"

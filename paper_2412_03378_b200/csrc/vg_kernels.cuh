@@ -1,0 +1,60 @@
+// Launcher declarations shared by the kernel translation units and the C ABI.
+#pragma once
+
+#include "vg_common.cuh"
+
+namespace vg {
+
+struct BlendParams {
+  int width, height, ntx;
+  float cx, cy, fx, fy;
+  float stop, cut, clamp;
+  float bg[3];
+};
+
+struct BwdIO {
+  const float* color;
+  const float* final_t;
+  const int* n_act;
+  const float* d_color;     // explicit upstream gradient (LOSS == 0)
+  const float* d_t;         // optional dL/dT_final (LOSS == 0)
+  const float* target;      // fused L2 (LOSS == 1)
+  float loss_scale;         // 2 / (H W 3)
+  double* loss_sum;         // fused L2: sum of squared residuals
+  float* acc;               // per-Gaussian accumulators, 16 floats each
+  uint8_t* visible;
+  float* d_background;
+};
+
+void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
+                       float* depth, int4* rect, uint32_t* count, cudaStream_t st);
+void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,
+                      const float* depth, int ntx, uint64_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t st);
+void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
+                  cudaStream_t st);
+void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                       const BlendParams& p, bool stop, bool cut, float* color, float* final_t,
+                       int* n_contrib, int* n_act, cudaStream_t st);
+void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                       const BlendParams& p, bool cut, int loss, const BwdIO& io, cudaStream_t st);
+void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
+                     const uint2* ranges, const BlendParams& p, float* image, float* intensity,
+                     cudaStream_t st);
+void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint32_t* vals,
+                     const uint2* ranges, const BlendParams& p, const float* d_image,
+                     const float* image, const float* target, float loss_scale, double* loss_sum,
+                     float* acc, uint8_t* visible, cudaStream_t st);
+void launch_finalize(int64_t n, const vg_scene& s, const CamK& c, float* acc, const vg_grads& g,
+                     cudaStream_t st);
+
+// radix sort / scan (vg_sort.cu)
+cudaError_t scan_temp_bytes(int64_t n, size_t* bytes);
+cudaError_t exclusive_scan(void* tmp, size_t tmp_bytes, const uint32_t* in, uint32_t* out,
+                           int64_t n, cudaStream_t st);
+cudaError_t sort_temp_bytes(int64_t n, int end_bit, size_t* bytes);
+cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t* k1, uint32_t* v0,
+                             uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st);
+int sort_launches(int end_bit);
+
+}  // namespace vg

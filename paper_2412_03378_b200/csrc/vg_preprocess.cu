@@ -1,0 +1,137 @@
+// K1: per-Gaussian preprocessing (float64), one thread per Gaussian.
+//
+// Replaces raster.prepare's per-primitive half (raster.py:154-209, 263-288;
+// core.py:81-153): view transform, validity z > z_near, EWA screen
+// covariance with 0.3 px^2 dilation, lambda_max, the amplitude-aware bin
+// radius, the tile rectangle and its tile count, kappa, and the 64-byte blend
+// record the tile kernels gather.  Compiled with -fmad=false so the binning
+// arithmetic rounds like the reference's numpy float64 (tile lists must match
+// bit for bit).
+#include "vg_kernels.cuh"
+
+namespace vg {
+
+struct PrepOut {
+  GRec* rec;
+  float* depth;        // sort key (float32 view depth)
+  int4* rect;          // tile rectangle x0, y0, x1, y1 (inclusive)
+  uint32_t* count;     // tiles overlapped (0 = not binned)
+};
+
+__global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __restrict__ means,
+                                                    const float* __restrict__ scales,
+                                                    const float* __restrict__ rots,
+                                                    const float* __restrict__ thetas,
+                                                    const float* __restrict__ colors,
+                                                    const float* __restrict__ sh, CamK c,
+                                                    double bin_cut, PrepOut o) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Frame f;
+  bool ok = make_frame(c, means + 3 * i, scales + 3 * i, rots + 4 * i, f);
+  uint32_t cnt = 0;
+  int4 rect = make_int4(0, 0, -1, -1);
+  double kappa = kappa_of((double)thetas[i], f.s, nullptr, nullptr);
+  if (ok) {
+    // --- EWA screen covariance (raster.py:175-209) or orthographic projection
+    double Sig[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += f.R[a * 3 + k] * (f.s[k] * f.s[k]) * f.R[b * 3 + k];
+        Sig[a * 3 + b] = acc;
+      }
+    double U[6];
+    if (c.projection == VG_PINHOLE) {
+      double z = f.v[2];
+      double limx = 1.3 * (0.5 * c.width / c.fx), limy = 1.3 * (0.5 * c.height / c.fy);
+      double rx = fmin(fmax(f.v[0] / z, -limx), limx);
+      double ry = fmin(fmax(f.v[1] / z, -limy), limy);
+      double J[6] = {c.fx / z, 0.0, -c.fx * rx / z, 0.0, c.fy / z, -c.fy * ry / z};
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+          U[a * 3 + b] = J[a * 3 + 0] * c.R[0 * 3 + b] + J[a * 3 + 1] * c.R[1 * 3 + b] +
+                         J[a * 3 + 2] * c.R[2 * 3 + b];
+    } else {
+      double sx = c.width / (2.0 * c.extent), sy = c.height / (2.0 * c.extent);
+      for (int b = 0; b < 3; ++b) { U[b] = sx * c.R[b]; U[3 + b] = sy * c.R[3 + b]; }
+    }
+    double cov[4];
+    for (int a = 0; a < 2; ++a)
+      for (int l = 0; l < 2; ++l) {
+        double acc = 0.0;
+        for (int j = 0; j < 3; ++j)
+          for (int k = 0; k < 3; ++k) acc += U[a * 3 + j] * Sig[j * 3 + k] * U[l * 3 + k];
+        cov[a * 2 + l] = acc;
+      }
+    cov[0] += DILATION;
+    cov[3] += DILATION;
+    // --- bounding radius (raster.py:154-172)
+    double half_tr = 0.5 * (cov[0] + cov[3]);
+    double det = cov[0] * cov[3] - cov[1] * cov[2];
+    double lam = half_tr + sqrt(fmax(half_tr * half_tr - det, 0.0));
+    double smax = fmax(fmax(f.s[0], f.s[1]), f.s[2]);
+    double amp = SQRT_2PI * kappa * smax;
+    double cut = fmax(bin_cut, 1e-12);
+    double need = sqrt(2.0 * log(fmax(1.05 * amp / cut, 1.0)));
+    double mult = fmax(BASE_SIGMA, need + 0.5);
+    double r = mult * sqrt(lam);
+    // --- tile rectangle (raster.py:233-244)
+    double u = f.pu, v = f.pv;
+    bool outside = (u + r < 0.0) || (u - r >= c.width) || (v + r < 0.0) || (v - r >= c.height);
+    if (!outside) {
+      double fx0 = fmin(fmax(floor((u - r) / TILE), 0.0), (double)(c.ntx - 1));
+      double fx1 = fmin(fmax(floor((u + r) / TILE), 0.0), (double)(c.ntx - 1));
+      double fy0 = fmin(fmax(floor((v - r) / TILE), 0.0), (double)(c.nty - 1));
+      double fy1 = fmin(fmax(floor((v + r) / TILE), 0.0), (double)(c.nty - 1));
+      rect = make_int4((int)fx0, (int)fy0, (int)fx1, (int)fy1);
+      cnt = (uint32_t)((rect.z - rect.x + 1) * (rect.w - rect.y + 1));
+    }
+  }
+  o.count[i] = cnt;
+  o.rect[i] = rect;
+  o.depth[i] = (float)f.v[2];
+  if (!cnt) return;
+  // --- blend record
+  GRec g;
+  g.u = f.pu;
+  g.v = f.pv;
+  g.P11 = (float)f.P11;
+  g.P21 = (float)f.P21;
+  g.P22 = (float)f.P22;
+  g.n1 = (float)f.n1;
+  g.n2 = (float)f.n2;
+  g.wm = (float)f.wm;
+  g.cD2 = (float)(0.5 * LOG2E * f.D * f.D);
+  g.D = (float)(c.projection == VG_PINHOLE ? f.D : f.beta);
+  g.kap2 = (float)(kappa * SQRT_2PI * LOG2E);
+  double rgb[3] = {0.0, 0.0, 0.0};
+  if (sh) {
+    double d[3] = {means[3 * i] - c.center[0], means[3 * i + 1] - c.center[1],
+                   means[3 * i + 2] - c.center[2]};
+    double dn = sqrt(dot3(d, d));
+    d[0] /= dn; d[1] /= dn; d[2] /= dn;
+    double b[16];
+    sh_basis(d, b);
+    const float* q = sh + 48 * i;
+    for (int l = 0; l < 16; ++l)
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += b[l] * q[l * 3 + ch];
+  } else if (colors) {
+    rgb[0] = colors[3 * i]; rgb[1] = colors[3 * i + 1]; rgb[2] = colors[3 * i + 2];
+  }
+  g.cr = (float)rgb[0];
+  g.cg = (float)rgb[1];
+  g.cb = (float)rgb[2];
+  o.rec[i] = g;
+}
+
+void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
+                       float* depth, int4* rect, uint32_t* count, cudaStream_t st) {
+  if (n <= 0) return;
+  PrepOut o{rec, depth, rect, count};
+  int blocks = (int)((n + 255) / 256);
+  k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
+                                       s.sh, c, bin_cut, o);
+}
+
+}  // namespace vg

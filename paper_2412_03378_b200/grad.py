@@ -1,0 +1,205 @@
+"""Drop-in mirror of the reference `volgauss.grad` hot path (grad.py):
+`SceneGrads`, `ParamGrad`, `backward`, `loss_and_grad` (L2 / L1).
+
+`backward` runs the sm_100a backward blend (front-to-back replay, warp-reduced
+per-Gaussian accumulators) and the float64 parameter chain through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .raster import (ALPHA_CLAMP, ALPHA_CUT, EARLY_STOP_T, TILE_SIZE, DeviceScene, _check_mode,
+                     _forward, _out, _stream, prepare)
+
+
+@dataclass
+class ParamGrad:
+    index: int
+    d_mean: object
+    d_scale: object
+    d_rotation: object
+    d_theta: float
+    d_color: object
+    d_splat_opacity: float
+
+
+class SceneGrads:
+    """Struct-of-arrays gradients (grad.py:41-69)."""
+
+    FIELDS = ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_kappas")
+
+    def __init__(self, n, mode):
+        self.mode = mode
+        self.d_means = np.zeros((n, 3))
+        self.d_scales = np.zeros((n, 3))
+        self.d_rotations = np.zeros((n, 4))
+        self.d_thetas = np.zeros(n)
+        self.d_colors = np.zeros((n, 3))
+        self.d_splat_opacities = np.zeros(n)
+        self.d_background = np.zeros(3)
+        self.d_kappas = np.zeros(n)
+        self.visible = np.zeros(n, dtype=bool)
+        self.d_sh = None
+
+    def __len__(self):
+        return len(self.d_thetas)
+
+    def __getitem__(self, i) -> ParamGrad:
+        return ParamGrad(index=i, d_mean=self.d_means[i], d_scale=self.d_scales[i],
+                         d_rotation=self.d_rotations[i], d_theta=float(self.d_thetas[i]),
+                         d_color=self.d_colors[i], d_splat_opacity=float(self.d_splat_opacities[i]))
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def position_norms(self):
+        if _lib_is_torch(self.d_means):
+            return self.d_means.norm(dim=1)
+        return np.linalg.norm(self.d_means, axis=1)
+
+
+def _lib_is_torch(x):
+    try:
+        import torch
+        return isinstance(x, torch.Tensor)
+    except ImportError:
+        return False
+
+
+class GradBuffers:
+    """One flat float32 device buffer holding every per-Gaussian gradient
+    (so a multi-GPU step all-reduces it with a single collective), plus
+    d_background and the visibility mask."""
+
+    LAYOUT = (("d_means", 3), ("d_scales", 3), ("d_rotations", 4), ("d_thetas", 1),
+              ("d_colors", 3), ("d_kappas", 1))
+
+    def __init__(self, n, device, with_sh=False):
+        import torch
+        self.n = n
+        width = sum(w for _, w in self.LAYOUT) + (48 if with_sh else 0)
+        self.flat = torch.zeros(max(n, 1) * width + 3, dtype=torch.float32, device=device)
+        self.views = {}
+        off = 0
+        for name, w in self.LAYOUT:
+            self.views[name] = self.flat[off:off + n * w].view(n, w) if w > 1 else self.flat[off:off + n]
+            off += n * w
+        self.views["d_sh"] = self.flat[off:off + n * 48].view(n, 16, 3) if with_sh else None
+        off += n * 48 if with_sh else 0
+        self.views["d_background"] = self.flat[off:off + 3]
+        self.visible = torch.zeros(max(n, 1), dtype=torch.uint8, device=device)
+
+    def struct(self, accumulate=False):
+        g = _lib.VgGrads()
+        for name in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_kappas",
+                     "d_background"):
+            setattr(g, name, _lib.ptr(self.views[name]).value)
+        g.d_sh = _lib.ptr(self.views["d_sh"]).value if self.views["d_sh"] is not None else None
+        g.visible = _lib.ptr(self.visible).value
+        g.accumulate = 1 if accumulate else 0
+        return g
+
+    def zero_(self):
+        self.flat.zero_()
+        self.visible.zero_()
+
+    def to_scene_grads(self, mode, torch_out):
+        n = self.n
+        sg = SceneGrads(0, mode)
+        for name, _ in self.LAYOUT:
+            setattr(sg, name, _out(self.views[name], torch_out))
+        sg.d_background = _out(self.views["d_background"], torch_out)
+        vis = self.visible[:n]
+        sg.visible = vis.bool() if torch_out else vis.cpu().numpy().astype(bool)
+        if torch_out:
+            import torch
+            sg.d_splat_opacities = torch.zeros(n, dtype=torch.float32, device=self.flat.device)
+        else:
+            sg.d_splat_opacities = np.zeros(n)
+        if self.views["d_sh"] is not None:
+            sg.d_sh = _out(self.views["d_sh"], torch_out)
+        return sg
+
+
+def _finite_or_raise(*arrays):
+    import torch
+    for a in arrays:
+        if a is None:
+            continue
+        ok = bool(torch.isfinite(a).all()) if isinstance(a, torch.Tensor) else bool(np.all(np.isfinite(a)))
+        if not ok:
+            raise ValueError("non-finite upstream pixel gradient")
+
+
+def _dev_image(a, shape, dev):
+    import torch
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=torch.float32).reshape(shape).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(dev).reshape(shape)
+
+
+def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
+             tile_size=TILE_SIZE, sort_by="depth", early_stop=EARLY_STOP_T, alpha_cut=ALPHA_CUT,
+             alpha_clamp=ALPHA_CLAMP, threads=None, prep=None) -> SceneGrads:
+    """grad.backward (grad.py:107-213), analytic mode.  Flags must match the
+    forward render they differentiate.  Raises ValueError on a non-finite
+    upstream gradient (grad.py:121-125)."""
+    _check_mode(mode, sort_by, tile_size)
+    _finite_or_raise(d_color, d_transmittance)
+    if prep is None:
+        dscene = DeviceScene(scene)
+        prep = prepare(dscene, camera, mode, tile_size, sort_by, alpha_cut,
+                       _ctx=_lib.scratch_context(dscene.device.index))
+    dscene = prep.dscene
+    _, color, tfin, _ = _forward(prep, early_stop, alpha_cut, alpha_clamp)
+    H, W = int(camera.height), int(camera.width)
+    dev = dscene.device
+    dc = _dev_image(d_color, (H, W, 3), dev)
+    dt = _dev_image(d_transmittance, (H, W), dev) if d_transmittance is not None else None
+    bufs = GradBuffers(dscene.n, dev, with_sh=dscene.sh is not None)
+    g = bufs.struct(accumulate=False)
+    _lib.check(_lib.load().vg_render_backward(prep.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),
+                                              _lib.ptr(dc), _lib.ptr(dt), ctypes.byref(g),
+                                              _stream(dev)), "vg_render_backward")
+    return bufs.to_scene_grads(mode, dscene.torch_in)
+
+
+@dataclass
+class LossSpec:
+    """Photometric loss (grad.py:308-320).  This build implements 'l2' and
+    'l1' on the device; 'dssim'/'mixed' are outside the hot path."""
+    kind: str = "l2"
+    lam: float = 0.2
+
+    @classmethod
+    def parse(cls, text):
+        if ":" in text:
+            kind, lam = text.split(":", 1)
+            return cls(kind=kind.strip(), lam=float(lam))
+        return cls(kind=text.strip())
+
+
+def loss_and_grad(image, target, spec: LossSpec = None):
+    """Loss value and dL/d(image) (grad.py:338-358) for 'l2' and 'l1'."""
+    spec = spec or LossSpec("l2")
+    if spec.kind not in ("l1", "l2"):
+        if spec.kind in ("dssim", "mixed"):
+            raise NotImplementedError(f"loss {spec.kind!r} is outside this build's hot path")
+        raise ValueError(f"unknown loss kind {spec.kind!r}")
+    if _lib_is_torch(image):
+        import torch
+        r = image - target.to(image)
+        n = r.numel()
+        if spec.kind == "l2":
+            return float((r * r).mean()), 2.0 * r / n
+        return float(r.abs().mean()), torch.sign(r) / n
+    r = np.asarray(image, dtype=float) - np.asarray(target, dtype=float)
+    n = r.size
+    if spec.kind == "l2":
+        return float(np.mean(r * r)), 2.0 * r / n
+    return float(np.mean(np.abs(r))), np.sign(r) / n

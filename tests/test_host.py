@@ -1,0 +1,81 @@
+"""Host-side logic of the facade, checked on CPU: reference-compatible
+argument validation, loud failure without a GPU (no CPU fallback), the
+synthetic configs, and the loss helper."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2412_03378_b200 as vg
+from conftest import cuda_available, load_case
+from paper_2412_03378_b200 import configs
+
+
+def test_mode_and_sort_validation():
+    scene, cam, _ = load_case("golden_scene")
+    with pytest.raises(ValueError):
+        vg.render(scene, cam, mode="hybrid")
+    with pytest.raises(ValueError):
+        vg.render(scene, cam, sort_by="nonsense")
+    with pytest.raises(NotImplementedError):
+        vg.render(scene, cam, mode="splat")
+    with pytest.raises(NotImplementedError):
+        vg.render(scene, cam, tile_size=8)
+
+
+@pytest.mark.skipif(cuda_available(), reason="checks the no-GPU path")
+def test_no_cpu_fallback():
+    scene, cam, _ = load_case("golden_scene")
+    with pytest.raises(RuntimeError):
+        vg.render(scene, cam)
+    with pytest.raises(RuntimeError):
+        vg.tomo_forward(scene, cam)
+
+
+def test_scene_container_mirrors_reference():
+    s = vg.Scene(means=[[0, 0, 1]], scales=[[0.1] * 3], rotations=[[1, 0, 0, 0]], thetas=[0.5],
+                 colors=[[1, 0, 0]], background=(0.1, 0.2, 0.3))
+    assert len(s) == 1 and s.splat_opacities.shape == (1,)
+    assert s.kappas()[0] == pytest.approx(-np.log1p(-0.99 * 0.5) * 10.0)
+    c = s.copy()
+    c.means[0, 0] = 5
+    assert s.means[0, 0] == 0
+    assert len(vg.Scene.empty()) == 0
+
+
+def test_composite_pixel_semantics():
+    # raster.py:442-454: two layers, early stop before an entry
+    color, t = vg.composite_pixel([(0.5, (1, 0, 0)), (0.5, (0, 1, 0))], (0, 0, 0))
+    assert np.allclose(color, [0.5, 0.25, 0.0]) and t == 0.25
+    layers = [(0.9, (1, 0, 0))] * 6 + [(1 - 1e-12, (0, 1, 0))]
+    color, t = vg.composite_pixel(layers, (0, 0, 0))
+    assert color[1] == 0.0 and t == pytest.approx(1e-4, rel=1e-9)
+
+
+def test_loss_helper():
+    rng = np.random.default_rng(0)
+    a, b = rng.uniform(size=(4, 4, 3)), rng.uniform(size=(4, 4, 3))
+    v, g = vg.loss_and_grad(a, b, vg.LossSpec("l2"))
+    assert v == pytest.approx(np.mean((a - b) ** 2))
+    assert np.allclose(g, 2 * (a - b) / a.size)
+    with pytest.raises(ValueError):
+        vg.loss_and_grad(a, b, vg.LossSpec("huber"))
+
+
+def test_configs_deterministic_and_shaped():
+    a, b = configs.tiny(), configs.tiny()
+    assert np.array_equal(a.scene.means, b.scene.means)
+    s = a.scene
+    assert s.means.dtype == np.float32 and s.means.shape == (1024, 3)
+    assert np.all((s.thetas > 0) & (s.thetas < 1))
+    cam = a.cameras[0]
+    assert (cam.width, cam.height) == (64, 64)
+    assert np.allclose(cam.center, [0, 0, -3])
+    m = configs.medium(n=2000, size=32)
+    assert len(m.cameras) == 8
+    assert all(np.linalg.norm(c.center) == pytest.approx(5.0) for c in m.cameras)
+    t = configs.tomography(n=500, size=32, n_views=6)
+    assert t.parallel and len(t.cameras) == 6
+    o = configs.opaque(n=1000, size=32, n_views=2)
+    assert np.allclose(o.scene.scales[:, 2], 1e-3)

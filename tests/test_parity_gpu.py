@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the golden vectors
+the reference produced and against the pinned CPU oracle.
+
+Contract (tests/parity.py): tile lists and their order bit-exact (order
+defined with float32 depth keys); images and gradients within
+1e-4 absolute (scaled by the field magnitude for gradients) + 1e-3 relative,
+with any out-of-tolerance pixel attributed to a float32/float64 threshold
+flip.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import RASTER_CASES, TOMO_CASES, case_flags, cuda_available, golden_lists, load_case
+from oracle import volgauss_oracle as O
+from parity import check_field, check_image
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+GRAD_FIELDS = ["d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_kappas"]
+
+
+def vg():
+    import paper_2412_03378_b200 as m
+    return m
+
+
+def test_library_is_native():
+    """The product path is the in-tree .so, not a fallback."""
+    import paper_2412_03378_b200._lib as L
+    lib = L.load()
+    assert lib._name.endswith("libvolgauss_b200.so")
+    ctx = L.Context()
+    assert ctx.launches() == 0
+
+
+@pytest.mark.parametrize("name", RASTER_CASES)
+def test_tile_lists_bit_exact(name):
+    scene, cam, d = load_case(name)
+    flags = case_flags(d)
+    prep = vg().prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    got = prep.grid.tiles
+    ref64 = golden_lists(d)
+    ref32 = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"], key_dtype=np.float32).lists()
+    assert len(got) == len(ref32)
+    ties = 0
+    for t, (g, r32, r64) in enumerate(zip(got, ref32, ref64)):
+        assert np.array_equal(g, r32), f"tile {t}: order differs from lexsort(prim, f32 depth, tile)"
+        assert np.array_equal(np.sort(g), np.sort(r64)), f"tile {t}: set differs from reference"
+        ties += int(np.sum(g != r64))
+    # any difference from the float64 order is a float32 depth tie
+    assert ties <= 2 * max(1, len(scene.means) // 500)
+
+
+@pytest.mark.parametrize("name", RASTER_CASES)
+def test_render_matches_reference(name):
+    scene, cam, d = load_case(name)
+    flags = case_flags(d)
+    out = vg().render(scene, cam, **flags)
+    prep = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    check_image(out.color, d["color"], prep, scene, flags, f"{name} color")
+    check_image(out.final_transmittance, d["final_transmittance"], prep, scene, flags, f"{name} T")
+    if flags["alpha_cut"] > 0:
+        diff = np.argwhere(out.n_contrib != d["n_contrib"])
+        from parity import pixel_is_flip
+        bad = [tuple(x) for x in diff if not pixel_is_flip(prep, scene, x[0], x[1], flags)]
+        assert not bad, f"n_contrib differs at {bad[:5]}"
+
+
+@pytest.mark.parametrize("name", [c for c in RASTER_CASES])
+def test_backward_matches_reference(name):
+    scene, cam, d = load_case(name)
+    if "d_color" not in d:
+        pytest.skip("no backward in this case")
+    flags = case_flags(d)
+    g = vg().backward(scene, cam, d["d_color"], d_transmittance=d.get("d_transmittance"), **flags)
+    for f in GRAD_FIELDS:
+        check_field(getattr(g, f), d[f"bwd_{f}"], f"{name} {f}")
+    check_field(g.d_background, d["bwd_d_background"], f"{name} d_background")
+    assert np.array_equal(g.visible, d["bwd_visible"])
+
+
+@pytest.mark.parametrize("name", TOMO_CASES)
+def test_tomo_matches_reference(name):
+    scene, cam, d = load_case(name)
+    img = vg().tomo_forward(scene, cam)
+    check_field(img, d["tomo_image"], f"{name} tomo image", atol=1e-4, rtol=1e-3)
+    g = vg().tomo_backward(scene, cam, d["tomo_weights"])
+    for f in GRAD_FIELDS:
+        check_field(getattr(g, f), d[f"tomo_{f}"], f"{name} tomo {f}")
+    assert np.array_equal(g.visible, d["tomo_visible"])
+
+
+def test_empty_scene_and_background():
+    scene, cam, d = load_case("empty")
+    out = vg().render(scene, cam)
+    assert np.allclose(out.color, d["background"])
+    assert np.all(out.final_transmittance == 1.0) and np.all(out.n_contrib == 0)
+    dc = np.random.default_rng(0).uniform(-1, 1, (cam.height, cam.width, 3))
+    g = vg().backward(scene, cam, dc)
+    np.testing.assert_allclose(g.d_background, dc.reshape(-1, 3).sum(axis=0), rtol=1e-5, atol=1e-5)
+
+
+def test_nan_upstream_raises():
+    scene, cam, d = load_case("tiny")
+    dc = np.zeros((cam.height, cam.width, 3))
+    dc[4, 4, 0] = np.nan
+    with pytest.raises(ValueError):
+        vg().backward(scene, cam, dc)
+
+
+def test_fused_l2_equals_explicit():
+    """vg_render_backward_l2 == loss_and_grad(l2) + vg_render_backward."""
+    import torch
+    from paper_2412_03378_b200 import engine
+    scene, cam, d = load_case("tiny")
+    eng = engine.Engine()
+    ds = eng.upload(scene)
+    tgt = torch.tensor(d["target"], dtype=torch.float32, device="cuda")
+    eng.prepare(ds, cam)
+    color, tfin, _ = eng.forward()
+    b1 = eng.new_grads(ds)
+    loss = eng.backward_l2(color, tfin, tgt, b1)
+    ref_loss, dimg = vg().loss_and_grad(color.double().cpu().numpy(), d["target"])
+    assert float(loss) == pytest.approx(ref_loss, rel=1e-5)
+    g2 = vg().backward(scene, cam, dimg)
+    for f in GRAD_FIELDS:
+        check_field(b1.views[f].cpu().numpy(), getattr(g2, f), f"fused {f}", rtol=1e-4, atol=1e-6)
+
+
+def test_parallel_beam_matches_oracle():
+    rng = np.random.default_rng(11)
+    n = 300
+    from types import SimpleNamespace
+    scene = SimpleNamespace(means=rng.uniform(-1, 1, (n, 3)).astype(np.float32).astype(np.float64),
+                            scales=np.repeat(np.exp(rng.uniform(np.log(0.02), np.log(0.1), (n, 1))), 3, 1).astype(np.float32).astype(np.float64),
+                            rotations=np.tile([1.0, 0, 0, 0], (n, 1)),
+                            thetas=rng.uniform(0.05, 0.9, n).astype(np.float32).astype(np.float64),
+                            colors=np.zeros((n, 3)), background=np.zeros(3))
+    cam = vg().look_at([4.0 * np.sin(0.3), 0.0, 4.0 * np.cos(0.3)], [0, 0, 0], width=40, height=36,
+                       fov_x_deg=30.0)
+    img = vg().tomo_forward(scene, cam, parallel=True, extent=1.6)
+    ref = O.tomo_forward(scene, cam, parallel=True, extent=1.6)
+    check_field(img, ref, "parallel image")
+    w = rng.uniform(0.1, 1.0, (36, 40))
+    g = vg().tomo_backward(scene, cam, w, parallel=True, extent=1.6)
+    rg = O.tomo_backward(scene, cam, w, parallel=True, extent=1.6)
+    for f in ["d_means", "d_scales", "d_rotations", "d_thetas", "d_kappas"]:
+        check_field(getattr(g, f), getattr(rg, f), f"parallel {f}")
+
+
+def test_multiview_accumulation_and_order_independence():
+    """Summing per-view grads with accumulate=True equals the sum of
+    separate backward calls (the view-sharded step relies on it)."""
+    import torch
+    from paper_2412_03378_b200 import configs, engine
+    cfg = configs.medium(n=3000, size=64, n_views=3)
+    eng = engine.Engine()
+    ds = eng.upload(cfg.scene)
+    acc = eng.new_grads(ds)
+    parts = []
+    for v, cam in enumerate(cfg.cameras):
+        tgt = torch.tensor(cfg.target(v, (64, 64, 3)), device="cuda")
+        eng.prepare(ds, cam)
+        color, tfin, _ = eng.forward()
+        eng.backward_l2(color, tfin, tgt, acc, accumulate=v > 0)
+        one = eng.new_grads(ds)
+        eng.prepare(ds, cam)
+        color, tfin, _ = eng.forward()
+        eng.backward_l2(color, tfin, tgt, one)
+        parts.append(one.flat.clone())
+    total = sum(parts)
+    check_field(acc.flat.cpu().numpy(), total.cpu().numpy(), "accumulated grads", rtol=1e-4, atol=1e-6)
+
+
+def test_full_size_large_view_tiles_and_sampled_pixels():
+    """Config 3 (N=1M, 1920x1080) first view: every tile list bit-exact
+    against the oracle's float32-key order, and a sample of tiles rendered
+    and back-propagated against the float64 oracle."""
+    import torch
+    from paper_2412_03378_b200 import configs
+    cfg = configs.large()
+    s = cfg.scene
+    cam = cfg.cameras[0]
+    from types import SimpleNamespace
+    colors = s.colors  # per-view SH colour is checked separately; use DC RGB here
+    scene = SimpleNamespace(means=s.means.astype(np.float64), scales=s.scales.astype(np.float64),
+                            rotations=s.rotations.astype(np.float64), thetas=s.thetas.astype(np.float64),
+                            colors=colors.astype(np.float64), background=np.zeros(3))
+    prep = vg().prepare(scene, cam)
+    oprep = O.prepare(scene, cam, key_dtype=np.float32)
+    assert prep.pair_count() == len(oprep.pair_prim)
+    prims, offs = prep.tile_lists_device()
+    assert np.array_equal(offs.cpu().numpy(), oprep.tile_start)
+    assert np.array_equal(prims.cpu().numpy(), oprep.pair_prim)
+    out = vg().render(scene, cam, prep=prep)
+    rng = np.random.default_rng(5)
+    busy = np.argsort(np.diff(oprep.tile_start))[-3:]
+    tiles = sorted(set(busy.tolist()) | set(rng.integers(0, oprep.tiles_x * oprep.tiles_y, 5).tolist()))
+    ref = O.render(scene, cam, prep=oprep, tiles=tiles)
+    mask = np.zeros((cam.height, cam.width), dtype=bool)
+    for t in tiles:
+        ty, tx = divmod(t, oprep.tiles_x)
+        mask[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+    col = np.where(mask[..., None], out.color, ref.color)
+    tf = np.where(mask, out.final_transmittance, ref.final_transmittance)
+    check_image(np.where(mask[..., None], col, 0), np.where(mask[..., None], ref.color, 0), oprep, scene, {}, "large color")
+    check_image(np.where(mask, tf, 0), np.where(mask, ref.final_transmittance, 0), oprep, scene, {}, "large T")
+    # backward restricted to the sampled tiles (d_color vanishes elsewhere)
+    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)) * mask[..., None]
+    g = vg().backward(scene, cam, dc, prep=prep)
+    rg = O.backward(scene, cam, dc, prep=oprep, tiles=tiles)
+    for f in GRAD_FIELDS:
+        check_field(getattr(g, f), getattr(rg, f), f"large {f}")
