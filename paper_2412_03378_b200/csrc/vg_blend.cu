@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) k_render_bwd(const GRec* __restrict__ rec
       float v[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) v[q] = 0.f;
-      bool nz = false;
+      bool nz = false, vis = false;
       if (j < na) {
         Pair e = eval_pinhole(s, lx, ly, Lp);
         float araw = 1.f - ex2f(-e.E2);
@@ -303,12 +303,15 @@ __global__ void __launch_bounds__(256) k_render_bwd(const GRec* __restrict__ rec
         v[6] = hr1; v[7] = hr2; v[8] = hr3;
         v[9] = h;
         v[10] = contrib * dc0; v[11] = contrib * dc1; v[12] = contrib * dc2;
-        nz = a > 0.f;
+        vis = a > 0.f;
+        nz = vis || h != 0.f;
         T = Tn;
       }
-      if (__any_sync(FULL, nz)) {
+      const unsigned any_nz = __ballot_sync(FULL, nz);
+      if (any_nz) {
         uint32_t gid = __float_as_uint(s.c.w);
-        if (lane == 0) io.visible[gid] = 1;
+        const bool any_vis = __any_sync(FULL, vis);
+        if (lane == 0 && any_vis) io.visible[gid] = 1;
         flush_acc(v, lane, gid, io.acc);
       }
     }

@@ -362,7 +362,12 @@ static BlendParams blend_params(const vg_context* c) {
   p.cy = (float)c->cam.cy;
   p.fx = (float)(c->cam.fx > 0 ? c->cam.fx : 1.0);
   p.fy = (float)(c->cam.fy > 0 ? c->cam.fy : 1.0);
-  p.stop = (float)c->opt.early_stop;
+  // An entry is active iff T_before >= early_stop (raster.py:384-385).  The
+  // comparison carries a 2^-20 relative slack: products of exactly clamped
+  // alphas, e.g. (1 - 0.99)^2 = 1.0000000000000018e-4 in float64, land just
+  // above 1e-4 in the reference but just below it in float32 (0.99 is not
+  // representable), which would systematically drop the next layer.
+  p.stop = (float)(c->opt.early_stop * (1.0 - 9.5367431640625e-07));
   p.cut = (float)c->opt.alpha_cut;
   p.clamp = (float)c->opt.alpha_clamp;
   for (int i = 0; i < 3; ++i) p.bg[i] = (float)c->scene.background[i];

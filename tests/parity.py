@@ -20,7 +20,7 @@ from oracle import volgauss_oracle as O
 
 ATOL = 1e-4
 RTOL = 1e-3
-FLIP_BAND = 3e-5
+FLIP_BAND = 1e-6
 
 
 def image_mismatch(gpu, ref):
@@ -53,8 +53,17 @@ def pixel_is_flip(prep, scene, row, col, flags):
     if cut > 0:
         near |= np.abs(raw - cut) < FLIP_BAND
     if stop is not None and stop > 0:
-        near |= np.abs(before - stop) < FLIP_BAND * stop
+        near |= stop_knife(before, stop)
     return bool(near.any())
+
+
+def stop_knife(before, stop):
+    """Transmittance within float32 reach of the early-stop threshold.  The
+    device compares against stop * (1 - 2^-20) so that exact products of
+    clamped alphas (e.g. (1-0.99)^2, a hair above 1e-4 in float64) decide like
+    the reference; those exact cases are therefore not knife-edges."""
+    return ((before >= stop * (1 - 3e-6)) & (before < stop)) | \
+        ((before > stop * (1 + 1e-12)) & (before <= stop * (1 + 2e-6)))
 
 
 def check_image(gpu, ref, prep, scene, flags, what, max_flips=None):
@@ -82,3 +91,31 @@ def check_field(gpu, ref, what, rtol=RTOL, atol=ATOL):
     assert not bad.any(), (f"{what}: {int(bad.sum())}/{bad.size} entries out of tolerance; "
                            f"worst err {float(err.max()):.3e} (scale {scale:.3e}) at "
                            f"{np.unravel_index(int(np.argmax(err - lim)), err.shape)}")
+
+
+def knife_edge_mask(prep, scene, flags, tiles=None):
+    """(H, W) bool: pixels whose oracle ray has a threshold knife-edge within
+    its active prefix (plus the first inactive entry)."""
+    cut = flags.get("alpha_cut", O.ALPHA_CUT)
+    stop = flags.get("early_stop", O.EARLY_STOP_T)
+    clamp = flags.get("alpha_clamp", O.ALPHA_CLAMP)
+    O._attach(prep, scene)
+    H, W = prep.height, prep.width
+    mask = np.zeros((H, W), dtype=bool)
+    for t in (range(prep.tiles_x * prep.tiles_y) if tiles is None else tiles):
+        ids = prep.tile_ids(t)
+        if ids.size == 0:
+            continue
+        r0, c0, h, w, rows, cols = O._tile_box(prep, t)
+        terms = O.ray_terms(prep, ids, rows, cols)
+        raw, alpha, _ = O.clamp_cut(terms["e"], cut, clamp)
+        before, active, _, _, n_act = O.front_to_back(alpha, stop)
+        k = np.arange(len(ids))[:, None]
+        relevant = k <= n_act[None, :]
+        near = np.abs(raw - clamp) < FLIP_BAND
+        if cut > 0:
+            near |= np.abs(raw - cut) < FLIP_BAND
+        if stop is not None and stop > 0:
+            near |= stop_knife(before, stop)
+        mask[r0:r0 + h, c0:c0 + w] = (near & relevant).any(axis=0).reshape(h, w)
+    return mask

@@ -15,7 +15,7 @@ import pytest
 
 from conftest import RASTER_CASES, TOMO_CASES, case_flags, cuda_available, golden_lists, load_case
 from oracle import volgauss_oracle as O
-from parity import check_field, check_image
+from parity import check_field, check_image, knife_edge_mask
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
@@ -76,11 +76,23 @@ def test_backward_matches_reference(name):
     if "d_color" not in d:
         pytest.skip("no backward in this case")
     flags = case_flags(d)
-    g = vg().backward(scene, cam, d["d_color"], d_transmittance=d.get("d_transmittance"), **flags)
+    dc, dt = d["d_color"], d.get("d_transmittance")
+    ref = {f: d[f"bwd_{f}"] for f in GRAD_FIELDS + ["d_background", "visible"]}
+    prep = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    knife = knife_edge_mask(prep, scene, flags)
+    if knife.any():
+        # float32/float64 threshold flips: take those pixels out of the
+        # upstream gradient on both sides (oracle is pinned to the reference)
+        assert knife.mean() < 0.02, f"{knife.sum()} knife-edge pixels"
+        dc = dc * ~knife[..., None]
+        dt = None if dt is None else dt * ~knife
+        g64 = O.backward(scene, cam, dc, d_transmittance=dt, prep=prep, **flags)
+        ref = {f: getattr(g64, f) for f in ref}
+    g = vg().backward(scene, cam, dc, d_transmittance=dt, **flags)
     for f in GRAD_FIELDS:
-        check_field(getattr(g, f), d[f"bwd_{f}"], f"{name} {f}")
-    check_field(g.d_background, d["bwd_d_background"], f"{name} d_background")
-    assert np.array_equal(g.visible, d["bwd_visible"])
+        check_field(getattr(g, f), ref[f], f"{name} {f}")
+    check_field(g.d_background, ref["d_background"], f"{name} d_background")
+    assert np.array_equal(g.visible, ref["visible"])
 
 
 @pytest.mark.parametrize("name", TOMO_CASES)
@@ -209,8 +221,10 @@ def test_full_size_large_view_tiles_and_sampled_pixels():
     tf = np.where(mask, out.final_transmittance, ref.final_transmittance)
     check_image(np.where(mask[..., None], col, 0), np.where(mask[..., None], ref.color, 0), oprep, scene, {}, "large color")
     check_image(np.where(mask, tf, 0), np.where(mask, ref.final_transmittance, 0), oprep, scene, {}, "large T")
-    # backward restricted to the sampled tiles (d_color vanishes elsewhere)
-    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)) * mask[..., None]
+    # backward restricted to the sampled tiles (d_color vanishes elsewhere),
+    # knife-edge pixels excluded on both sides
+    knife = knife_edge_mask(oprep, scene, {}, tiles=tiles)
+    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)) * (mask & ~knife)[..., None]
     g = vg().backward(scene, cam, dc, prep=prep)
     rg = O.backward(scene, cam, dc, prep=oprep, tiles=tiles)
     for f in GRAD_FIELDS:
