@@ -1,24 +1,36 @@
 // K5 forward blend, K6 backward blend, K8 tomography projector + adjoint.
 //
-// One 256-thread CTA per 16x16 tile (raster.py:322-329), one pixel per
-// thread.  The tile's sorted Gaussian list is staged through shared memory
-// in batches of 256: each thread gathers one 64-byte record and derives the
-// tile-relative coefficients (c1, c2, c3) once, so the per-pair cost is the
-// float32 evaluation in vg_common.cuh plus 4 broadcast LDS.128.
+// Layout: one 128-thread CTA per 16x16 tile (raster.py:322-329), launched in
+// heavy-tiles-first order.  Each warp owns an 8x8 pixel block; each lane owns
+// two pixels of one column (rows r and r+4) and evaluates both with packed
+// FP32x2 instructions (FFMA2/FMUL2/FADD2); exp2 / rsqrt run on the SFU.
+// The tile's depth-sorted list is staged through shared memory in batches of
+// 256 records; the staging thread derives the tile-relative coefficients once
+// and a 4-bit mask of the warp blocks the Gaussian can reach.
+//
+// Culling (result-preserving): e = kappa sqrt(2pi) beta peak with
+// beta <= s_max and expo = D^2 X / (w_par^2 + X), so alpha >= alpha_cut at
+// some pixel of a block needs X (D^2 - R^2) <= R^2 w_par^2 there, with
+// R^2 = 2 ln(kappa sqrt(2pi) s_max / e_cut).  A block is skipped only when the
+// interval lower bound of X and upper bound of w_par^2 over the block violate
+// it (with a 1e-3 margin on e_cut); every skipped pair would have been cut to
+// alpha = 0, so images, n_contrib and gradients are unchanged.
 //
 // Semantics reproduced exactly (raster.py:332-395, grad.py:135-178):
 //   alpha_raw = 1 - exp(-e), alpha = min(alpha_raw, clamp), alpha < cut -> 0;
 //   an entry is composited iff the transmittance IN FRONT of it is >= stop;
 //   T_final is the transmittance after the last active entry; n_contrib
 //   counts active entries with alpha > 0.
+// The transmittance factor is carried directly: om = max(exp(-e), 1-clamp)
+// (1 if cut), T <- T * om, alpha = 1 - om.
 // The backward runs front to back and needs no division: with
 //   total = dc . color + dT * T_final  (= sum over active of dot*contrib
 //                                         + (dc . bg + dT) T_final),
 //   suffix_i = total - sum_{j<=i} dot_j contrib_j, and for live entries
 //   dL/de_i = dL/dalpha_i (1 - alpha_i) = dot_i T_after_i - suffix_i.
 // Per-Gaussian accumulators (13 floats, whitened e-frame, see vg_finalize.cu)
-// are warp-reduced with a transpose-reduce (16 shuffles) and one vector of
-// 13 red.global.add per warp.
+// are summed over the lane's two pixels, warp-reduced with a transpose-reduce
+// (16 shuffles) and added with one 13-lane red.global.add per warp.
 #include "vg_kernels.cuh"
 
 namespace vg {
@@ -26,6 +38,8 @@ namespace vg {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float C_HALF_LOG2E = 0.72134752044448170f;  // 0.5 * log2(e)
 constexpr int ACC_STRIDE = 16;                         // floats per Gaussian accumulator
+constexpr int NT = 128;                                // threads per tile CTA
+constexpr int BATCH = 256;                             // staged records per batch
 
 struct __align__(16) SRec {
   float4 a;  // c1, c2, c3, cD2
@@ -34,53 +48,143 @@ struct __align__(16) SRec {
   float4 d;  // r, g, b, 0
 };
 
+// ---------------------------------------------------------------------------
+// packed FP32x2 helpers (sm_100a FFMA2 / FMUL2 / FADD2)
 
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 f2(float a, float b) {
+  F2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ F2 f2s(float a) { return f2(a, a); }
+__device__ __forceinline__ float lo(F2 x) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+  return a;
+}
+__device__ __forceinline__ float hi(F2 x) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+  return b;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return d;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+  F2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+  F2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+  F2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 ex2_2(F2 x) { return f2(ex2f(lo(x)), ex2f(hi(x))); }
+__device__ __forceinline__ F2 rsq_2(F2 x) { return f2(rsqf(lo(x)), rsqf(hi(x))); }
+__device__ __forceinline__ F2 neg2(F2 x) { return f2(-lo(x), -hi(x)); }
+__device__ __forceinline__ F2 sel2(bool p0, bool p1, F2 a, F2 b) {
+  return f2(p0 ? lo(a) : lo(b), p1 ? hi(a) : hi(b));
+}
 
-__device__ __forceinline__ void stage(SRec* sm, int slot, const GRec* __restrict__ rec, uint32_t gid,
-                                      int x0, int y0) {
+// ---------------------------------------------------------------------------
+// staging + culling
+
+__device__ __forceinline__ float d0(float lo_, float hi_) {
+  // distance of the interval [lo_, hi_] from 0
+  return fmaxf(fmaxf(lo_, -hi_), 0.f);
+}
+
+// Stage one record for the tile at pixel origin (x0, y0); return the 4-bit
+// mask of 8x8 warp blocks the Gaussian may reach with alpha >= cut.
+__device__ __forceinline__ uint32_t stage(SRec* sm, int slot, const GRec* __restrict__ rec,
+                                          uint32_t gid, int x0, int y0, bool cull, float ecut) {
   const GRec g = rec[gid];
   float bu = (float)((double)x0 + 0.5 - g.u);
   float bv = (float)((double)y0 + 0.5 - g.v);
+  float c1 = g.P11 * bu;
+  float c2 = fmaf(g.P22, bv, g.P21 * bu);
+  float c3 = fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm));
   SRec s;
-  s.a = make_float4(g.P11 * bu, fmaf(g.P22, bv, g.P21 * bu), fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm)),
-                    g.cD2);
+  s.a = make_float4(c1, c2, c3, g.cD2);
   s.b = make_float4(g.P11, g.P21, g.P22, g.kap2);
   s.c = make_float4(g.n1, g.n2, g.D, __uint_as_float(gid));
   s.d = make_float4(g.cr, g.cg, g.cb, 0.f);
   sm[slot] = s;
+  if (!cull) return 0xFu;
+  if (!(g.amp > ecut)) return 0u;  // alpha < cut at every pixel
+  float R2 = 2.f * __logf(g.amp / ecut);
+  float D2 = g.D * g.D;
+  if (D2 <= R2 * 1.001f) return 0xFu;
+  float k2 = R2 / (D2 - R2) * 1.001f + 1e-30f;
+  uint32_t m = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const float xa = (float)(8 * (b & 1)), xb = xa + 7.f;
+    const float ya = (float)(8 * (b >> 1)), yb = ya + 7.f;
+    float q1a = fmaf(g.P11, xa, c1), q1b = fmaf(g.P11, xb, c1);
+    float pxa = g.P21 * xa, pxb = g.P21 * xb, pya = g.P22 * ya, pyb = g.P22 * yb;
+    float q2lo = c2 + fminf(pxa, pxb) + fminf(pya, pyb);
+    float q2hi = c2 + fmaxf(pxa, pxb) + fmaxf(pya, pyb);
+    float nxa = g.n1 * xa, nxb = g.n1 * xb, nya = g.n2 * ya, nyb = g.n2 * yb;
+    float wlo = c3 + fminf(nxa, nxb) + fminf(nya, nyb);
+    float whi = c3 + fmaxf(nxa, nxb) + fmaxf(nya, nyb);
+    float t1 = d0(fminf(q1a, q1b), fmaxf(q1a, q1b));
+    float t2 = d0(q2lo, q2hi);
+    float Xmin = (t1 * t1 + t2 * t2) * 0.999f;
+    float wmax2 = fmaxf(wlo * wlo, whi * whi);
+    if (Xmin <= k2 * wmax2) m |= 1u << b;
+  }
+  return m;
 }
 
-struct Pair {
-  float q1, q2, wp, X, rs, G, E2;
+struct Pair2 {
+  float q1;
+  F2 q2, wp, X, rs, G, E2, ex;
 };
 
-// Pinhole ray: the shared (forward == backward) float32 evaluation.  Explicit
-// fmaf / __fmul_rn keep the rounding identical in every kernel.
-__device__ __forceinline__ Pair eval_pinhole(const SRec& s, float lx, float ly, float Lp) {
-  Pair o;
+// Pinhole rays, two pixels (same column lx, rows ly.x / ly.y).  The single
+// shared evaluation for forward and backward (identical rounding).
+__device__ __forceinline__ Pair2 eval_pinhole2(const SRec& s, float lx, F2 ly, F2 Lp) {
+  Pair2 o;
   o.q1 = fmaf(s.b.x, lx, s.a.x);
-  o.q2 = fmaf(s.b.y, lx, fmaf(s.b.z, ly, s.a.y));
-  o.wp = fmaf(s.c.x, lx, fmaf(s.c.y, ly, s.a.z));
-  o.X = fmaf(o.q1, o.q1, __fmul_rn(o.q2, o.q2));
-  float W2 = fmaf(o.wp, o.wp, o.X);
-  o.rs = rsqf(W2);
-  float ri = __fmul_rn(o.rs, o.rs);
-  float arg = fmaf(-s.a.w, __fmul_rn(o.X, ri), Lp);
-  o.G = __fmul_rn(o.rs, ex2f(arg));
-  o.E2 = __fmul_rn(s.b.w, o.G);
+  const float t2 = fmaf(s.b.y, lx, s.a.y);
+  o.q2 = fma2(f2s(s.b.z), ly, f2s(t2));
+  const float tw = fmaf(s.c.x, lx, s.a.z);
+  o.wp = fma2(f2s(s.c.y), ly, f2s(tw));
+  o.X = fma2(o.q2, o.q2, f2s(__fmul_rn(o.q1, o.q1)));
+  const F2 W2 = fma2(o.wp, o.wp, o.X);
+  o.rs = rsq_2(W2);
+  const F2 ri = mul2(o.rs, o.rs);
+  const F2 arg = fma2(f2s(-s.a.w), mul2(o.X, ri), Lp);
+  o.G = mul2(o.rs, ex2_2(arg));
+  o.E2 = mul2(f2s(s.b.w), o.G);
+  o.ex = ex2_2(neg2(o.E2));
   return o;
 }
 
-// Parallel ray: beta is per Gaussian (slot c.z), expo = X.
-__device__ __forceinline__ Pair eval_parallel(const SRec& s, float lx, float ly) {
-  Pair o;
+// Parallel rays: beta is per Gaussian (slot c.z), expo = X.
+__device__ __forceinline__ Pair2 eval_parallel2(const SRec& s, float lx, F2 ly) {
+  Pair2 o;
   o.q1 = fmaf(s.b.x, lx, s.a.x);
-  o.q2 = fmaf(s.b.y, lx, fmaf(s.b.z, ly, s.a.y));
-  o.wp = 0.f;
-  o.X = fmaf(o.q1, o.q1, __fmul_rn(o.q2, o.q2));
-  o.rs = 0.f;
-  o.G = __fmul_rn(s.c.z, ex2f(__fmul_rn(-C_HALF_LOG2E, o.X)));
-  o.E2 = __fmul_rn(s.b.w, o.G);
+  const float t2 = fmaf(s.b.y, lx, s.a.y);
+  o.q2 = fma2(f2s(s.b.z), ly, f2s(t2));
+  o.wp = f2s(0.f);
+  o.X = fma2(o.q2, o.q2, f2s(__fmul_rn(o.q1, o.q1)));
+  o.rs = f2s(0.f);
+  o.G = mul2(f2s(s.c.z), ex2_2(mul2(f2s(-C_HALF_LOG2E), o.X)));
+  o.E2 = mul2(f2s(s.b.w), o.G);
+  o.ex = f2s(1.f);
   return o;
 }
 
@@ -90,34 +194,53 @@ __device__ __forceinline__ float pixel_lp(const BlendParams& p, int col, int row
   return 0.5f * lg2f(fmaf(X, X, fmaf(Y, Y, 1.f)));
 }
 
-// Reduce 16 per-lane values over the warp; returns, in every lane, the
-// warp total of value index ((l>>4&1)*8 + (l>>3&1)*4 + (l>>2&1)*2 + (l>>1&1)).
+// Lane geometry: warp w owns the 8x8 block (8(w&1), 8(w>>1)); lane l owns
+// column 8(w&1) + (l&7) and rows 8(w>>1) + (l>>3) and +4.
+struct LaneGeo {
+  int lxi, ly0, col, row0, row1;
+  bool in0, in1;
+};
+__device__ __forceinline__ LaneGeo lane_geo(const BlendParams& p, int tx, int ty) {
+  LaneGeo g;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  g.lxi = 8 * (w & 1) + (l & 7);
+  g.ly0 = 8 * (w >> 1) + (l >> 3);
+  g.col = tx * TILE + g.lxi;
+  g.row0 = ty * TILE + g.ly0;
+  g.row1 = g.row0 + 4;
+  g.in0 = g.col < p.width && g.row0 < p.height;
+  g.in1 = g.col < p.width && g.row1 < p.height;
+  return g;
+}
+
+// Reduce 16 per-lane values over the warp; lane l ends with the warp total of
+// value index ((l>>4&1)*8 + (l>>3&1)*4 + (l>>2&1)*2 + (l>>1&1)).
 __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    bool hi = lane & 16;
-    float send = hi ? v[i] : v[i + 8];
-    float keep = hi ? v[i + 8] : v[i];
+    bool h = lane & 16;
+    float send = h ? v[i] : v[i + 8];
+    float keep = h ? v[i + 8] : v[i];
     v[i] = keep + __shfl_xor_sync(FULL, send, 16);
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    bool hi = lane & 8;
-    float send = hi ? v[i] : v[i + 4];
-    float keep = hi ? v[i + 4] : v[i];
+    bool h = lane & 8;
+    float send = h ? v[i] : v[i + 4];
+    float keep = h ? v[i + 4] : v[i];
     v[i] = keep + __shfl_xor_sync(FULL, send, 8);
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    bool hi = lane & 4;
-    float send = hi ? v[i] : v[i + 2];
-    float keep = hi ? v[i + 2] : v[i];
+    bool h = lane & 4;
+    float send = h ? v[i] : v[i + 2];
+    float keep = h ? v[i + 2] : v[i];
     v[i] = keep + __shfl_xor_sync(FULL, send, 4);
   }
   {
-    bool hi = lane & 2;
-    float send = hi ? v[0] : v[1];
-    float keep = hi ? v[1] : v[0];
+    bool h = lane & 2;
+    float send = h ? v[0] : v[1];
+    float keep = h ? v[1] : v[0];
     v[0] = keep + __shfl_xor_sync(FULL, send, 2);
   }
   return v[0] + __shfl_xor_sync(FULL, v[0], 1);
@@ -132,8 +255,8 @@ __device__ __forceinline__ void flush_acc(float (&v)[16], int lane, uint32_t gid
 // Block sum of 3 floats + 1 double into global (d_background, loss).
 __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double l, float* out3,
                                             double* outl) {
-  __shared__ float r3[8][3];
-  __shared__ double rl[8];
+  __shared__ float r3[NT / 32][3];
+  __shared__ double rl[NT / 32];
   for (int o = 16; o; o >>= 1) {
     a0 += __shfl_xor_sync(FULL, a0, o);
     a1 += __shfl_xor_sync(FULL, a1, o);
@@ -146,7 +269,7 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
   if (threadIdx.x == 0) {
     float s0 = 0, s1 = 0, s2 = 0;
     double sl = 0;
-    for (int i = 0; i < 8; ++i) { s0 += r3[i][0]; s1 += r3[i][1]; s2 += r3[i][2]; sl += rl[i]; }
+    for (int i = 0; i < NT / 32; ++i) { s0 += r3[i][0]; s1 += r3[i][1]; s2 += r3[i][2]; sl += rl[i]; }
     if (out3) {
       if (s0 != 0.f) atomicAdd(out3 + 0, s0);
       if (s1 != 0.f) atomicAdd(out3 + 1, s1);
@@ -160,159 +283,239 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
 // K5 forward blend (raster.render)
 
 template <bool STOP, bool CUT>
-__global__ void __launch_bounds__(256) k_render_fwd(const GRec* __restrict__ rec,
-                                                    const uint32_t* __restrict__ vals,
-                                                    const uint2* __restrict__ ranges,
-                                                    BlendParams p, float* __restrict__ color,
-                                                    float* __restrict__ final_t,
-                                                    int* __restrict__ n_contrib,
-                                                    int* __restrict__ n_act) {
-  __shared__ SRec sm[TILE_PIX];
-  const int tile = blockIdx.x;
+__global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const uint2* __restrict__ ranges,
+                                                   const uint32_t* __restrict__ order,
+                                                   BlendParams p, float* __restrict__ color,
+                                                   float* __restrict__ final_t,
+                                                   int* __restrict__ n_contrib,
+                                                   int* __restrict__ n_act) {
+  __shared__ SRec sm[BATCH];
+  __shared__ uint8_t smask[BATCH];
+  const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int lxi = threadIdx.x & 15, lyi = threadIdx.x >> 4;
-  const int col = tx * TILE + lxi, row = ty * TILE + lyi;
-  const bool inside = col < p.width && row < p.height;
-  const float lx = (float)lxi, ly = (float)lyi;
-  const float Lp = pixel_lp(p, col, row);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
-  float T = 1.f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-  int nc = 0, na = 0;
-  bool done = !inside;
-  for (uint32_t base = r.x; base < r.y; base += TILE_PIX) {
-    if (__syncthreads_count(done) == TILE_PIX) break;
-    uint32_t i = base + threadIdx.x;
-    if (i < r.y) stage(sm, threadIdx.x, rec, vals[i], tx * TILE, ty * TILE);
+  const int len = (int)(r.y - r.x);
+  F2 T = f2s(1.f), Cr = f2s(0.f), Cg = f2s(0.f), Cb = f2s(0.f);
+  // per-pixel floor of the transmittance factor: 1 - clamp while active,
+  // 1 once the pixel stopped (or lies outside the image) so alpha = 0 after.
+  float fl0 = G.in0 ? p.cc : 1.f, fl1 = G.in1 ? p.cc : 1.f;
+  int nc0 = 0, nc1 = 0, na0 = len, na1 = len;
+  bool done = !(G.in0 || G.in1);
+  for (uint32_t base = r.x; base < r.y; base += BATCH) {
+    if (__syncthreads_count(done) == NT) break;
+    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
+      uint32_t i = base + sidx;
+      if (i < r.y) smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut);
+    }
     __syncthreads();
-    const int nb = min((uint32_t)TILE_PIX, r.y - base);
-    if (!done) {
-      for (int k = 0; k < nb; ++k) {
-        if (STOP && T < p.stop) { done = true; break; }
+    const int nb = min((uint32_t)BATCH, r.y - base);
+    const int jb = (int)(base - r.x);
+    for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
+      const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
+      unsigned bits = __ballot_sync(FULL, vb);
+      while (bits) {
+        const int k = c + __ffs(bits) - 1;
+        bits &= bits - 1;
         const SRec s = sm[k];
-        Pair e = eval_pinhole(s, lx, ly, Lp);
-        float a = fminf(1.f - ex2f(-e.E2), p.clamp);
-        if (CUT && a < p.cut) a = 0.f;
-        float w = __fmul_rn(a, T);
-        c0 = fmaf(w, s.d.x, c0);
-        c1 = fmaf(w, s.d.y, c1);
-        c2 = fmaf(w, s.d.z, c2);
-        nc += (a > 0.f);
-        T = fmaf(-a, T, T);
-        ++na;
+        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
+        if (CUT) {
+          if (om0 > p.omcut) om0 = 1.f;
+          if (om1 > p.omcut) om1 = 1.f;
+        }
+        nc0 += om0 < 1.f;
+        nc1 += om1 < 1.f;
+        const F2 om = f2(om0, om1);
+        const F2 a = sub2(f2s(1.f), om);
+        const F2 w = mul2(a, T);
+        Cr = fma2(w, f2s(s.d.x), Cr);
+        Cg = fma2(w, f2s(s.d.y), Cg);
+        Cb = fma2(w, f2s(s.d.z), Cb);
+        T = mul2(T, om);
+        if (STOP) {
+          const int j1 = jb + k + 1;
+          if (fl0 < 1.f && lo(T) < p.stop) { fl0 = 1.f; na0 = j1; }
+          if (fl1 < 1.f && hi(T) < p.stop) { fl1 = 1.f; na1 = j1; }
+        }
       }
+      if (STOP) done = fl0 == 1.f && fl1 == 1.f;
     }
   }
-  if (inside) {
-    int pix = row * p.width + col;
-    color[3 * pix + 0] = fmaf(T, p.bg[0], c0);
-    color[3 * pix + 1] = fmaf(T, p.bg[1], c1);
-    color[3 * pix + 2] = fmaf(T, p.bg[2], c2);
-    final_t[pix] = T;
-    n_contrib[pix] = nc;
-    n_act[pix] = na;
+  const float t0 = lo(T), t1 = hi(T);
+  if (G.in0) {
+    const int pix = G.row0 * p.width + G.col;
+    color[3 * pix + 0] = fmaf(t0, p.bg[0], lo(Cr));
+    color[3 * pix + 1] = fmaf(t0, p.bg[1], lo(Cg));
+    color[3 * pix + 2] = fmaf(t0, p.bg[2], lo(Cb));
+    final_t[pix] = t0;
+    n_contrib[pix] = nc0;
+    n_act[pix] = na0;
   }
+  if (G.in1) {
+    const int pix = G.row1 * p.width + G.col;
+    color[3 * pix + 0] = fmaf(t1, p.bg[0], hi(Cr));
+    color[3 * pix + 1] = fmaf(t1, p.bg[1], hi(Cg));
+    color[3 * pix + 2] = fmaf(t1, p.bg[2], hi(Cb));
+    final_t[pix] = t1;
+    n_contrib[pix] = nc1;
+    n_act[pix] = na1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-pair gradient terms (shared by the render and cone-beam backward):
+// fills v[0..9] with h (rho rho^T + w^ w^T), h rho, h summed over 2 pixels.
+__device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s, F2 h,
+                                                   float (&v)[16]) {
+  const F2 ri = mul2(e.rs, e.rs);
+  const F2 dr = mul2(f2s(s.c.z), ri);
+  const F2 t = mul2(dr, e.wp);
+  const F2 r1 = mul2(t, f2s(-e.q1));
+  const F2 r2 = neg2(mul2(t, e.q2));
+  const F2 r3 = mul2(dr, e.X);
+  const F2 w1 = mul2(e.rs, f2s(e.q1));
+  const F2 w2 = mul2(e.rs, e.q2);
+  const F2 w3 = mul2(e.rs, e.wp);
+  const F2 hr1 = mul2(h, r1), hr2 = mul2(h, r2), hr3 = mul2(h, r3);
+  const F2 hw1 = mul2(h, w1), hw2 = mul2(h, w2), hw3 = mul2(h, w3);
+  F2 A;
+  A = fma2(hr1, r1, mul2(hw1, w1)); v[0] = lo(A) + hi(A);
+  A = fma2(hr1, r2, mul2(hw1, w2)); v[1] = lo(A) + hi(A);
+  A = fma2(hr1, r3, mul2(hw1, w3)); v[2] = lo(A) + hi(A);
+  A = fma2(hr2, r2, mul2(hw2, w2)); v[3] = lo(A) + hi(A);
+  A = fma2(hr2, r3, mul2(hw2, w3)); v[4] = lo(A) + hi(A);
+  A = fma2(hr3, r3, mul2(hw3, w3)); v[5] = lo(A) + hi(A);
+  v[6] = lo(hr1) + hi(hr1);
+  v[7] = lo(hr2) + hi(hr2);
+  v[8] = lo(hr3) + hi(hr3);
+  v[9] = lo(h) + hi(h);
 }
 
 // ---------------------------------------------------------------------------
 // K6 backward blend (grad.backward tile_job + e_chain)
 
-
-
 template <bool CUT, int LOSS>
-__global__ void __launch_bounds__(256) k_render_bwd(const GRec* __restrict__ rec,
-                                                    const uint32_t* __restrict__ vals,
-                                                    const uint2* __restrict__ ranges,
-                                                    BlendParams p, BwdIO io) {
-  __shared__ SRec sm[TILE_PIX];
+__global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const uint2* __restrict__ ranges,
+                                                   const uint32_t* __restrict__ order,
+                                                   BlendParams p, BwdIO io) {
+  __shared__ SRec sm[BATCH];
+  __shared__ uint8_t smask[BATCH];
   __shared__ int s_maxna;
-  const int tile = blockIdx.x;
+  const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int lxi = threadIdx.x & 15, lyi = threadIdx.x >> 4;
-  const int lane = threadIdx.x & 31;
-  const int col = tx * TILE + lxi, row = ty * TILE + lyi;
-  const bool inside = col < p.width && row < p.height;
-  const float lx = (float)lxi, ly = (float)lyi;
-  const float Lp = pixel_lp(p, col, row);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
-  float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, tot = 0.f, Tf = 1.f;
+  float dcv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+  float totv[2] = {0.f, 0.f}, Tfv[2] = {1.f, 1.f};
+  int nav[2] = {0, 0};
   double lossv = 0.0;
-  int na = 0;
   if (threadIdx.x == 0) s_maxna = 0;
-  if (inside) {
-    int pix = row * p.width + col;
-    float cc0 = io.color[3 * pix], cc1 = io.color[3 * pix + 1], cc2 = io.color[3 * pix + 2];
-    Tf = io.final_t[pix];
-    na = io.n_act[pix];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool in = q ? G.in1 : G.in0;
+    if (!in) continue;
+    const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
+    const float cc0 = io.color[3 * pix], cc1 = io.color[3 * pix + 1], cc2 = io.color[3 * pix + 2];
+    Tfv[q] = io.final_t[pix];
+    nav[q] = io.n_act[pix];
     float dT = 0.f;
     if (LOSS == 0) {
-      dc0 = io.d_color[3 * pix]; dc1 = io.d_color[3 * pix + 1]; dc2 = io.d_color[3 * pix + 2];
+      dcv[q][0] = io.d_color[3 * pix];
+      dcv[q][1] = io.d_color[3 * pix + 1];
+      dcv[q][2] = io.d_color[3 * pix + 2];
       if (io.d_t) dT = io.d_t[pix];
     } else {
-      float r0 = cc0 - io.target[3 * pix], r1 = cc1 - io.target[3 * pix + 1],
-            r2 = cc2 - io.target[3 * pix + 2];
-      lossv = (double)r0 * r0 + (double)r1 * r1 + (double)r2 * r2;
-      dc0 = io.loss_scale * r0; dc1 = io.loss_scale * r1; dc2 = io.loss_scale * r2;
+      const float r0 = cc0 - io.target[3 * pix], r1 = cc1 - io.target[3 * pix + 1],
+                  r2 = cc2 - io.target[3 * pix + 2];
+      lossv += (double)r0 * r0 + (double)r1 * r1 + (double)r2 * r2;
+      dcv[q][0] = io.loss_scale * r0;
+      dcv[q][1] = io.loss_scale * r1;
+      dcv[q][2] = io.loss_scale * r2;
     }
-    tot = fmaf(dc0, cc0, fmaf(dc1, cc1, fmaf(dc2, cc2, dT * Tf)));
+    totv[q] = fmaf(dcv[q][0], cc0, fmaf(dcv[q][1], cc1, fmaf(dcv[q][2], cc2, dT * Tfv[q])));
   }
   __syncthreads();
-  if (na) atomicMax(&s_maxna, na);
-  block_flush(dc0 * Tf, dc1 * Tf, dc2 * Tf, lossv, io.d_background, LOSS ? io.loss_sum : nullptr);
+  const int my_na = max(nav[0], nav[1]);
+  if (my_na) atomicMax(&s_maxna, my_na);
+  int warp_na = my_na;
+  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
+  block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
+              dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
+              LOSS ? io.loss_sum : nullptr);
   __syncthreads();
   const uint32_t end = r.x + (uint32_t)s_maxna;
-  float T = 1.f, P = 0.f;
-  for (uint32_t base = r.x; base < end; base += TILE_PIX) {
+  const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
+           dcb = f2(dcv[0][2], dcv[1][2]);
+  const F2 tot = f2(totv[0], totv[1]);
+  F2 T = f2s(1.f), P = f2s(0.f);
+  for (uint32_t base = r.x; base < end; base += BATCH) {
     __syncthreads();
-    uint32_t i = base + threadIdx.x;
-    if (i < end) stage(sm, threadIdx.x, rec, vals[i], tx * TILE, ty * TILE);
+    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
+      uint32_t i = base + sidx;
+      if (i < end) smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut);
+    }
     __syncthreads();
-    const int nb = min((uint32_t)TILE_PIX, end - base);
-    for (int k = 0; k < nb; ++k) {
-      const int j = (int)(base - r.x) + k;
-      const SRec s = sm[k];
-      float v[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = 0.f;
-      bool nz = false, vis = false;
-      if (j < na) {
-        Pair e = eval_pinhole(s, lx, ly, Lp);
-        float araw = 1.f - ex2f(-e.E2);
-        float a = fminf(araw, p.clamp);
-        bool cut = CUT && a < p.cut;
-        if (cut) a = 0.f;
-        float contrib = __fmul_rn(a, T);
-        float Tn = fmaf(-a, T, T);
-        float dot = fmaf(dc0, s.d.x, fmaf(dc1, s.d.y, dc2 * s.d.z));
-        P = fmaf(dot, contrib, P);
-        bool live = !cut && araw < p.clamp;
-        float de = live ? fmaf(dot, Tn, P - tot) : 0.f;
-        float h = de * e.G;
-        float ri = e.rs * e.rs;
-        float dr = s.c.z * ri;
-        float t = dr * e.wp;
-        float r1 = -t * e.q1, r2 = -t * e.q2, r3 = dr * e.X;
-        float w1 = e.rs * e.q1, w2 = e.rs * e.q2, w3 = e.rs * e.wp;
-        float hr1 = h * r1, hr2 = h * r2, hr3 = h * r3;
-        float hw1 = h * w1, hw2 = h * w2, hw3 = h * w3;
-        v[0] = fmaf(hr1, r1, hw1 * w1);
-        v[1] = fmaf(hr1, r2, hw1 * w2);
-        v[2] = fmaf(hr1, r3, hw1 * w3);
-        v[3] = fmaf(hr2, r2, hw2 * w2);
-        v[4] = fmaf(hr2, r3, hw2 * w3);
-        v[5] = fmaf(hr3, r3, hw3 * w3);
-        v[6] = hr1; v[7] = hr2; v[8] = hr3;
-        v[9] = h;
-        v[10] = contrib * dc0; v[11] = contrib * dc1; v[12] = contrib * dc2;
-        vis = a > 0.f;
-        nz = vis || h != 0.f;
+    const int jb = (int)(base - r.x);
+    const int nb = min(min((int)BATCH, (int)(end - base)), warp_na - jb);
+    for (int c = 0; c < nb; c += 32) {
+      const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
+      unsigned bits = __ballot_sync(FULL, vb);
+      while (bits) {
+        const int k = c + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int j = jb + k;
+        const SRec s = sm[k];
+        const bool act0 = j < nav[0], act1 = j < nav[1];
+        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
+        float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
+        bool cut0 = false, cut1 = false;
+        if (CUT) {
+          cut0 = om0 > p.omcut;
+          cut1 = om1 > p.omcut;
+          if (cut0) om0 = 1.f;
+          if (cut1) om1 = 1.f;
+        }
+        const F2 om = f2(om0, om1);
+        const F2 a = sub2(f2s(1.f), om);
+        const F2 contrib = mul2(a, T);
+        const F2 Tn = mul2(T, om);
+        const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
+        P = fma2(dot, contrib, P);
+        // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
+        const bool live0 = act0 && !cut0 && lo(e.ex) > p.cc;
+        const bool live1 = act1 && !cut1 && hi(e.ex) > p.cc;
+        const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
+        const F2 h = mul2(de, e.G);
+        float v[16];
+        pinhole_grad_terms(e, s, h, v);
+        const F2 dr_ = mul2(contrib, dcr), dg_ = mul2(contrib, dcg), db_ = mul2(contrib, dcb);
+        v[10] = lo(dr_) + hi(dr_);
+        v[11] = lo(dg_) + hi(dg_);
+        v[12] = lo(db_) + hi(db_);
+        v[13] = v[14] = v[15] = 0.f;
         T = Tn;
-      }
-      const unsigned any_nz = __ballot_sync(FULL, nz);
-      if (any_nz) {
-        uint32_t gid = __float_as_uint(s.c.w);
-        const bool any_vis = __any_sync(FULL, vis);
-        if (lane == 0 && any_vis) io.visible[gid] = 1;
-        flush_acc(v, lane, gid, io.acc);
+        const bool vis = om0 < 1.f || om1 < 1.f;
+        const bool nz = vis || live0 || live1;
+        if (__any_sync(FULL, nz)) {
+          const uint32_t gid = __float_as_uint(s.c.w);
+          const bool any_vis = __any_sync(FULL, vis);
+          if (lane == 0 && any_vis) io.visible[gid] = 1;
+          flush_acc(v, lane, gid, io.acc);
+        }
       }
     }
   }
@@ -323,118 +526,119 @@ __global__ void __launch_bounds__(256) k_render_bwd(const GRec* __restrict__ rec
 // of e over every binned pair; no cut, clamp or early stop (tomo.py:43-47).
 
 template <int RAY>
-__global__ void __launch_bounds__(256) k_tomo_fwd(const GRec* __restrict__ rec,
-                                                  const uint32_t* __restrict__ vals,
-                                                  const uint2* __restrict__ ranges, BlendParams p,
-                                                  float* __restrict__ image,
-                                                  float* __restrict__ intensity) {
-  __shared__ SRec sm[TILE_PIX];
-  const int tile = blockIdx.x;
+__global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
+                                                 const uint32_t* __restrict__ vals,
+                                                 const uint2* __restrict__ ranges,
+                                                 const uint32_t* __restrict__ order,
+                                                 BlendParams p, float* __restrict__ image,
+                                                 float* __restrict__ intensity) {
+  __shared__ SRec sm[BATCH];
+  const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int lxi = threadIdx.x & 15, lyi = threadIdx.x >> 4;
-  const int col = tx * TILE + lxi, row = ty * TILE + lyi;
-  const bool inside = col < p.width && row < p.height;
-  const float lx = (float)lxi, ly = (float)lyi;
-  const float Lp = RAY == VG_PINHOLE ? pixel_lp(p, col, row) : 0.f;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = RAY == VG_PINHOLE ? f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1))
+                                  : f2s(0.f);
   const uint2 r = ranges[tile];
-  float sum = 0.f;
-  for (uint32_t base = r.x; base < r.y; base += TILE_PIX) {
+  F2 sum = f2s(0.f);
+  for (uint32_t base = r.x; base < r.y; base += BATCH) {
     __syncthreads();
-    uint32_t i = base + threadIdx.x;
-    if (i < r.y) stage(sm, threadIdx.x, rec, vals[i], tx * TILE, ty * TILE);
+    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
+      uint32_t i = base + sidx;
+      if (i < r.y) stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, false, 0.f);
+    }
     __syncthreads();
-    const int nb = min((uint32_t)TILE_PIX, r.y - base);
+    const int nb = min((uint32_t)BATCH, r.y - base);
     for (int k = 0; k < nb; ++k) {
       const SRec s = sm[k];
-      Pair e = RAY == VG_PINHOLE ? eval_pinhole(s, lx, ly, Lp) : eval_parallel(s, lx, ly);
-      sum += e.E2;
+      const Pair2 e = RAY == VG_PINHOLE ? eval_pinhole2(s, lx, ly, Lp) : eval_parallel2(s, lx, ly);
+      sum = add2(sum, e.E2);
     }
   }
-  if (inside) {
-    int pix = row * p.width + col;
-    float I = sum * (float)LN2;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool in = q ? G.in1 : G.in0;
+    if (!in) continue;
+    const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
+    const float I = (q ? hi(sum) : lo(sum)) * (float)LN2;
     image[pix] = I;
     if (intensity) intensity[pix] = __expf(-I);
   }
 }
 
 template <int RAY, int LOSS>
-__global__ void __launch_bounds__(256) k_tomo_bwd(const GRec* __restrict__ rec,
-                                                  const uint32_t* __restrict__ vals,
-                                                  const uint2* __restrict__ ranges, BlendParams p,
-                                                  const float* __restrict__ d_image,
-                                                  const float* __restrict__ image,
-                                                  const float* __restrict__ target,
-                                                  float loss_scale, double* loss_sum,
-                                                  float* __restrict__ acc,
-                                                  uint8_t* __restrict__ visible) {
-  __shared__ SRec sm[TILE_PIX];
-  const int tile = blockIdx.x;
+__global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
+                                                 const uint32_t* __restrict__ vals,
+                                                 const uint2* __restrict__ ranges,
+                                                 const uint32_t* __restrict__ order,
+                                                 BlendParams p, const float* __restrict__ d_image,
+                                                 const float* __restrict__ image,
+                                                 const float* __restrict__ target,
+                                                 float loss_scale, double* loss_sum,
+                                                 float* __restrict__ acc,
+                                                 uint8_t* __restrict__ visible) {
+  __shared__ SRec sm[BATCH];
+  const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int lxi = threadIdx.x & 15, lyi = threadIdx.x >> 4;
   const int lane = threadIdx.x & 31;
-  const int col = tx * TILE + lxi, row = ty * TILE + lyi;
-  const bool inside = col < p.width && row < p.height;
-  const float lx = (float)lxi, ly = (float)lyi;
-  const float Lp = RAY == VG_PINHOLE ? pixel_lp(p, col, row) : 0.f;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = RAY == VG_PINHOLE ? f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1))
+                                  : f2s(0.f);
   const uint2 r = ranges[tile];
-  float de = 0.f;
+  float dev[2] = {0.f, 0.f};
   double lossv = 0.0;
-  if (inside) {
-    int pix = row * p.width + col;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const bool in = q ? G.in1 : G.in0;
+    if (!in) continue;
+    const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
     if (LOSS == 0) {
-      de = d_image[pix];
+      dev[q] = d_image[pix];
     } else {
-      float rr = image[pix] - target[pix];
-      lossv = (double)rr * rr;
-      de = loss_scale * rr;
+      const float rr = image[pix] - target[pix];
+      lossv += (double)rr * rr;
+      dev[q] = loss_scale * rr;
     }
   }
   if (LOSS) block_flush(0.f, 0.f, 0.f, lossv, nullptr, loss_sum);
-  for (uint32_t base = r.x; base < r.y; base += TILE_PIX) {
+  const F2 de = f2(dev[0], dev[1]);
+  for (uint32_t base = r.x; base < r.y; base += BATCH) {
     __syncthreads();
-    uint32_t i = base + threadIdx.x;
-    if (i < r.y) stage(sm, threadIdx.x, rec, vals[i], tx * TILE, ty * TILE);
+    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
+      uint32_t i = base + sidx;
+      if (i < r.y) stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, false, 0.f);
+    }
     __syncthreads();
-    const int nb = min((uint32_t)TILE_PIX, r.y - base);
+    const int nb = min((uint32_t)BATCH, r.y - base);
     for (int k = 0; k < nb; ++k) {
       const SRec s = sm[k];
+      const Pair2 e = RAY == VG_PINHOLE ? eval_pinhole2(s, lx, ly, Lp) : eval_parallel2(s, lx, ly);
+      const F2 h = mul2(de, e.G);
       float v[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = 0.f;
-      bool nz = false;
-      if (inside) {
-        Pair e = RAY == VG_PINHOLE ? eval_pinhole(s, lx, ly, Lp) : eval_parallel(s, lx, ly);
-        float h = de * e.G;
-        if (RAY == VG_PINHOLE) {
-          float ri = e.rs * e.rs;
-          float dr = s.c.z * ri;
-          float t = dr * e.wp;
-          float r1 = -t * e.q1, r2 = -t * e.q2, r3 = dr * e.X;
-          float w1 = e.rs * e.q1, w2 = e.rs * e.q2, w3 = e.rs * e.wp;
-          float hr1 = h * r1, hr2 = h * r2, hr3 = h * r3;
-          float hw1 = h * w1, hw2 = h * w2, hw3 = h * w3;
-          v[0] = fmaf(hr1, r1, hw1 * w1);
-          v[1] = fmaf(hr1, r2, hw1 * w2);
-          v[2] = fmaf(hr1, r3, hw1 * w3);
-          v[3] = fmaf(hr2, r2, hw2 * w2);
-          v[4] = fmaf(hr2, r3, hw2 * w3);
-          v[5] = fmaf(hr3, r3, hw3 * w3);
-          v[6] = hr1; v[7] = hr2; v[8] = hr3;
-        } else {
-          // rho = -(q1, q2, 0), w_hat = (0, 0, 1)
-          float hq1 = h * e.q1, hq2 = h * e.q2;
-          v[0] = hq1 * e.q1;
-          v[1] = hq1 * e.q2;
-          v[3] = hq2 * e.q2;
-          v[5] = h;
-          v[6] = -hq1; v[7] = -hq2;
-        }
-        v[9] = h;
-        nz = e.E2 > 0.f;
+      if (RAY == VG_PINHOLE) {
+        pinhole_grad_terms(e, s, h, v);
+      } else {
+        // rho = -(q1, q2, 0), w_hat = (0, 0, 1)
+        const F2 hq1 = mul2(h, f2s(e.q1)), hq2 = mul2(h, e.q2);
+        F2 t;
+        t = mul2(hq1, f2s(e.q1)); v[0] = lo(t) + hi(t);
+        t = mul2(hq1, e.q2); v[1] = lo(t) + hi(t);
+        v[2] = 0.f;
+        t = mul2(hq2, e.q2); v[3] = lo(t) + hi(t);
+        v[4] = 0.f;
+        v[5] = lo(h) + hi(h);
+        v[6] = -(lo(hq1) + hi(hq1));
+        v[7] = -(lo(hq2) + hi(hq2));
+        v[8] = 0.f;
+        v[9] = v[5];
       }
-      if (__any_sync(FULL, nz)) {
-        uint32_t gid = __float_as_uint(s.c.w);
+      v[10] = v[11] = v[12] = v[13] = v[14] = v[15] = 0.f;
+      const bool vis = (G.in0 && lo(e.E2) > 0.f) || (G.in1 && hi(e.E2) > 0.f);
+      if (__any_sync(FULL, vis)) {
+        const uint32_t gid = __float_as_uint(s.c.w);
         if (lane == 0) visible[gid] = 1;
         flush_acc(v, lane, gid, acc);
       }
@@ -446,45 +650,47 @@ __global__ void __launch_bounds__(256) k_tomo_bwd(const GRec* __restrict__ rec,
 // launchers
 
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
-                       const BlendParams& p, bool stop, bool cut, float* color, float* final_t,
-                       int* n_contrib, int* n_act, cudaStream_t st) {
-  if (stop && cut)
-    k_render_fwd<true, true><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, color, final_t, n_contrib, n_act);
-  else if (stop)
-    k_render_fwd<true, false><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, color, final_t, n_contrib, n_act);
-  else if (cut)
-    k_render_fwd<false, true><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, color, final_t, n_contrib, n_act);
-  else
-    k_render_fwd<false, false><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, color, final_t, n_contrib, n_act);
+                       const uint32_t* order, const BlendParams& p, bool stop, bool cut,
+                       float* color, float* final_t, int* n_contrib, int* n_act, cudaStream_t st) {
+#define VG_RF(S, C)                                                                             \
+  k_render_fwd<S, C><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color, final_t,       \
+                                             n_contrib, n_act)
+  if (stop && cut) VG_RF(true, true);
+  else if (stop) VG_RF(true, false);
+  else if (cut) VG_RF(false, true);
+  else VG_RF(false, false);
+#undef VG_RF
 }
 
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
-                       const BlendParams& p, bool cut, int loss, const BwdIO& io, cudaStream_t st) {
+                       const uint32_t* order, const BlendParams& p, bool cut, int loss,
+                       const BwdIO& io, cudaStream_t st) {
+#define VG_RB(C, L) k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io)
   if (cut) {
-    if (loss) k_render_bwd<true, 1><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, io);
-    else k_render_bwd<true, 0><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, io);
+    if (loss) VG_RB(true, 1); else VG_RB(true, 0);
   } else {
-    if (loss) k_render_bwd<false, 1><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, io);
-    else k_render_bwd<false, 0><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, io);
+    if (loss) VG_RB(false, 1); else VG_RB(false, 0);
   }
+#undef VG_RB
 }
 
 void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
-                     const uint2* ranges, const BlendParams& p, float* image, float* intensity,
-                     cudaStream_t st) {
+                     const uint2* ranges, const uint32_t* order, const BlendParams& p,
+                     float* image, float* intensity, cudaStream_t st) {
   if (ray == VG_PINHOLE)
-    k_tomo_fwd<VG_PINHOLE><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, image, intensity);
+    k_tomo_fwd<VG_PINHOLE><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity);
   else
-    k_tomo_fwd<VG_PARALLEL><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, image, intensity);
+    k_tomo_fwd<VG_PARALLEL><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity);
 }
 
 void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint32_t* vals,
-                     const uint2* ranges, const BlendParams& p, const float* d_image,
-                     const float* image, const float* target, float loss_scale, double* loss_sum,
-                     float* acc, uint8_t* visible, cudaStream_t st) {
-#define VG_TB(R, L)                                                                           \
-  k_tomo_bwd<R, L><<<n_tiles, 256, 0, st>>>(rec, vals, ranges, p, d_image, image, target,     \
-                                            loss_scale, loss_sum, acc, visible)
+                     const uint2* ranges, const uint32_t* order, const BlendParams& p,
+                     const float* d_image, const float* image, const float* target,
+                     float loss_scale, double* loss_sum, float* acc, uint8_t* visible,
+                     cudaStream_t st) {
+#define VG_TB(R, L)                                                                            \
+  k_tomo_bwd<R, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, d_image, image, target, \
+                                           loss_scale, loss_sum, acc, visible)
   if (ray == VG_PINHOLE) {
     if (loss) VG_TB(VG_PINHOLE, 1); else VG_TB(VG_PINHOLE, 0);
   } else {

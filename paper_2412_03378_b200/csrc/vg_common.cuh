@@ -34,7 +34,7 @@ constexpr double THETA_CEILING = 0.99;  // core.py:22
 constexpr double DILATION = 0.3;        // raster.py:30
 constexpr double BASE_SIGMA = 3.0;      // raster.py:35
 
-// Per-Gaussian blend record (64 B), written by preprocess, gathered per tile.
+// Per-Gaussian blend record (80 B), written by preprocess, gathered per tile.
 struct __align__(16) GRec {
   double u, v;            // projected mean in pixel coordinates (continuous)
   float P11, P21, P22;    // q = P (du, dv)
@@ -43,8 +43,10 @@ struct __align__(16) GRec {
   float D;                // D (pinhole) | beta (parallel)
   float kap2;             // kappa sqrt(2 pi) log2(e)
   float cr, cg, cb;       // RGB (evaluated from SH when present)
+  float amp;              // kappa sqrt(2 pi) s_max >= e at any pixel (culling bound)
+  float pad0, pad1, pad2;
 };
-static_assert(sizeof(GRec) == 64, "GRec must be 64 bytes");
+static_assert(sizeof(GRec) == 80, "GRec must be 80 bytes");
 
 // Camera in the form kernels take by value.
 struct CamK {

@@ -8,7 +8,12 @@ namespace vg {
 struct BlendParams {
   int width, height, ntx;
   float cx, cy, fx, fy;
-  float stop, cut, clamp;
+  float stop;      // early_stop * (1 - 2^-20)  (see blend_params)
+  float cut;       // alpha_cut
+  float clamp;     // alpha_clamp
+  float cc;        // 1 - alpha_clamp (rounded once from float64): clamped transmittance factor
+  float omcut;     // 1 - alpha_cut: factor above which an entry is cut
+  float ecut;      // culling threshold on e: -log1p(-alpha_cut) * (1 - 1e-3)
   float bg[3];
 };
 
@@ -34,15 +39,17 @@ void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t 
 void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
                   cudaStream_t st);
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
-                       const BlendParams& p, bool stop, bool cut, float* color, float* final_t,
-                       int* n_contrib, int* n_act, cudaStream_t st);
+                       const uint32_t* order, const BlendParams& p, bool stop, bool cut,
+                       float* color, float* final_t, int* n_contrib, int* n_act, cudaStream_t st);
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
-                       const BlendParams& p, bool cut, int loss, const BwdIO& io, cudaStream_t st);
+                       const uint32_t* order, const BlendParams& p, bool cut, int loss,
+                       const BwdIO& io, cudaStream_t st);
 void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
-                     const uint2* ranges, const BlendParams& p, float* image, float* intensity,
-                     cudaStream_t st);
+                     const uint2* ranges, const uint32_t* order, const BlendParams& p,
+                     float* image, float* intensity, cudaStream_t st);
 void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint32_t* vals,
-                     const uint2* ranges, const BlendParams& p, const float* d_image,
+                     const uint2* ranges, const uint32_t* order, const BlendParams& p,
+                     const float* d_image,
                      const float* image, const float* target, float loss_scale, double* loss_sum,
                      float* acc, uint8_t* visible, cudaStream_t st);
 void launch_finalize(int64_t n, const vg_scene& s, const CamK& c, float* acc, const vg_grads& g,
@@ -56,5 +63,10 @@ cudaError_t sort_temp_bytes(int64_t n, int end_bit, size_t* bytes);
 cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t* k1, uint32_t* v0,
                              uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st);
 int sort_launches(int end_bit);
+// heavy-tiles-first order: tile ids sorted by descending list length
+cudaError_t tile_order_temp_bytes(int n_tiles, size_t* bytes);
+cudaError_t tile_order(void* tmp, size_t tmp_bytes, const uint2* ranges, uint32_t* len_in,
+                       uint32_t* len_out, uint32_t* ids_in, uint32_t* ids_out, int n_tiles,
+                       cudaStream_t st);
 
 }  // namespace vg

@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   g.cD2 = (float)(0.5 * LOG2E * f.D * f.D);
   g.D = (float)(c.projection == VG_PINHOLE ? f.D : f.beta);
   g.kap2 = (float)(kappa * SQRT_2PI * LOG2E);
+  g.amp = (float)(SQRT_2PI * kappa * fmax(fmax(f.s[0], f.s[1]), f.s[2]));
+  g.pad0 = g.pad1 = g.pad2 = 0.f;
   double rgb[3] = {0.0, 0.0, 0.0};
   if (sh) {
     double d[3] = {means[3 * i] - c.center[0], means[3 * i + 1] - c.center[1],

@@ -35,4 +35,29 @@ cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t
 
 int sort_launches(int end_bit) { return 1 + (end_bit + 7) / 8; }
 
+// Heavy-tiles-first launch order: tiles sorted by descending list length, so
+// the longest tiles start in the first wave (longest-processing-time first).
+__global__ void k_tile_len(const uint2* ranges, uint32_t* len, uint32_t* ids, int n) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    uint2 r = ranges[t];
+    len[t] = r.y - r.x;
+    ids[t] = (uint32_t)t;
+  }
+}
+
+cudaError_t tile_order_temp_bytes(int n_tiles, size_t* bytes) {
+  return cub::DeviceRadixSort::SortPairsDescending(nullptr, *bytes, (const uint32_t*)nullptr,
+                                                   (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                                   (uint32_t*)nullptr, n_tiles);
+}
+
+cudaError_t tile_order(void* tmp, size_t tmp_bytes, const uint2* ranges, uint32_t* len_in,
+                       uint32_t* len_out, uint32_t* ids_in, uint32_t* ids_out, int n_tiles,
+                       cudaStream_t st) {
+  k_tile_len<<<(n_tiles + 255) / 256, 256, 0, st>>>(ranges, len_in, ids_in, n_tiles);
+  return cub::DeviceRadixSort::SortPairsDescending(tmp, tmp_bytes, len_in, len_out, ids_in,
+                                                   ids_out, n_tiles, 0, 32, st);
+}
+
 }  // namespace vg
