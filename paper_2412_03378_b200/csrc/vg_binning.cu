@@ -44,6 +44,69 @@ __global__ void k_total(int64_t n, const uint32_t* count, const uint32_t* offset
   total[0] = n > 0 ? (uint64_t)offset[n - 1] + count[n - 1] : 0;
 }
 
+// --- depth-presorted binning: Gaussians are first sorted by float32 depth,
+// pairs are emitted in that order with 16-bit tile keys, and a stable sort by
+// tile alone then yields (tile, depth, index) order.
+
+__global__ void k_iota(int64_t n, uint32_t* ids) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ perm,
+                                const uint32_t* __restrict__ count, uint32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = count[perm[i]];
+}
+
+__global__ void __launch_bounds__(256) k_duplicate_sorted(int64_t n, const uint32_t* __restrict__ perm,
+                                                          const uint32_t* __restrict__ offset,
+                                                          const uint32_t* __restrict__ count_sorted,
+                                                          const int4* __restrict__ rect, int ntx,
+                                                          uint16_t* __restrict__ keys,
+                                                          uint32_t* __restrict__ vals) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t cnt = count_sorted[i];
+  if (!cnt) return;
+  uint32_t g = perm[i];
+  uint32_t o = offset[i];
+  int4 r = rect[g];
+  for (int y = r.y; y <= r.w; ++y)
+    for (int x = r.x; x <= r.z; ++x) {
+      keys[o] = (uint16_t)(y * ntx + x);
+      vals[o] = g;
+      ++o;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ranges16(int64_t P, const uint16_t* __restrict__ keys,
+                                                  uint2* __restrict__ ranges) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  uint32_t t = keys[i];
+  if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
+  if (i == P - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+}
+
+void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st) {
+  if (n > 0) k_iota<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, ids);
+}
+void launch_gather_counts(int64_t n, const uint32_t* perm, const uint32_t* count, uint32_t* out,
+                          cudaStream_t st) {
+  if (n > 0) k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, count, out);
+}
+void launch_duplicate_sorted(int64_t n, const uint32_t* perm, const uint32_t* offset,
+                             const uint32_t* count_sorted, const int4* rect, int ntx,
+                             uint16_t* keys, uint32_t* vals, cudaStream_t st) {
+  if (n > 0)
+    k_duplicate_sorted<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, offset, count_sorted,
+                                                                     rect, ntx, keys, vals);
+}
+void launch_ranges16(int64_t P, const uint16_t* keys, uint2* ranges, cudaStream_t st) {
+  if (P > 0) k_ranges16<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges);
+}
+
 void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,
                       const float* depth, int ntx, uint64_t* keys, uint32_t* vals,
                       cudaStream_t st) {

@@ -60,16 +60,8 @@ __device__ __forceinline__ F2 f2(float a, float b) {
   return r;
 }
 __device__ __forceinline__ F2 f2s(float a) { return f2(a, a); }
-__device__ __forceinline__ float lo(F2 x) {
-  float a, b;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
-  return a;
-}
-__device__ __forceinline__ float hi(F2 x) {
-  float a, b;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
-  return b;
-}
+__device__ __forceinline__ float lo(F2 x) { return __uint_as_float((unsigned)(x.v & 0xffffffffull)); }
+__device__ __forceinline__ float hi(F2 x) { return __uint_as_float((unsigned)(x.v >> 32)); }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
   F2 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));

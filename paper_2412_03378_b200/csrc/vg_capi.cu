@@ -48,6 +48,7 @@ struct vg_context {
   Buf keys0, keys1, vals0, vals1;
   Buf ranges, n_act, scan_tmp, sort_tmp, total;
   Buf tlen, tord, ord_tmp;  // heavy-first tile order
+  Buf dkey, perm, cnt_s, dsort_tmp;  // depth pre-sort of the Gaussians
   uint64_t* total_host = nullptr;
   // state of the last prepare
   vg_scene scene{};
@@ -55,7 +56,7 @@ struct vg_context {
   vg_options opt{};
   int64_t pairs = 0;
   int n_tiles = 0;
-  uint64_t* keys = nullptr;  // sorted buffers
+  uint16_t* keys = nullptr;  // sorted buffers (tile ids)
   uint32_t* vals = nullptr;
   bool prepared = false;
   bool have_fwd = false;
@@ -145,7 +146,8 @@ void vg_destroy(vg_context* c) {
   cudaDeviceSynchronize();
   Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
                 &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
-                &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp};
+                &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp, &c->dkey,
+                &c->perm, &c->cnt_s, &c->dsort_tmp};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -235,6 +237,9 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
     VG_TRY(ensure(c->rect, sizeof(int4) * (size_t)n, st));
     VG_TRY(ensure(c->count, sizeof(uint32_t) * (size_t)n, st));
     VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)n, st));
+    VG_TRY(ensure(c->dkey, sizeof(uint32_t) * (size_t)n, st));
+    VG_TRY(ensure(c->perm, sizeof(uint32_t) * 2 * (size_t)n, st));
+    VG_TRY(ensure(c->cnt_s, sizeof(uint32_t) * (size_t)n, st));
     if (grow_acc) VG_TRY(ensure(c->acc, accb, st, true));
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
@@ -242,56 +247,71 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
                         (int4*)c->rect.p, (uint32_t*)c->count.p, st);
     }
     VG_LAUNCHED(c, 1);
+    // Gaussians in (float32 depth, index) order
+    uint32_t* ids_in = (uint32_t*)c->perm.p + n;
+    uint32_t* perm = (uint32_t*)c->perm.p;
+    launch_iota(n, ids_in, st);
+    VG_LAUNCHED(c, 1);
     size_t tmp = 0;
+    VG_CUDA(depth_sort_temp_bytes(n, &tmp));
+    VG_TRY(ensure(c->dsort_tmp, tmp, st));
+    {
+      ProfScope ps(c, VG_K_SORT, st);
+      VG_CUDA(depth_sort(c->dsort_tmp.p, c->dsort_tmp.bytes, (const uint32_t*)c->depth.p,
+                         (uint32_t*)c->dkey.p, ids_in, perm, n, st));
+    }
+    c->launches += 5;
+    launch_gather_counts(n, perm, (const uint32_t*)c->count.p, (uint32_t*)c->cnt_s.p, st);
+    VG_LAUNCHED(c, 1);
     VG_CUDA(scan_temp_bytes(n, &tmp));
     VG_TRY(ensure(c->scan_tmp, tmp, st));
     {
       ProfScope ps(c, VG_K_SCAN, st);
-      VG_CUDA(exclusive_scan(c->scan_tmp.p, c->scan_tmp.bytes, (const uint32_t*)c->count.p,
+      VG_CUDA(exclusive_scan(c->scan_tmp.p, c->scan_tmp.bytes, (const uint32_t*)c->cnt_s.p,
                              (uint32_t*)c->offset.p, n, st));
     }
     VG_LAUNCHED(c, 1);
-    launch_total(n, (const uint32_t*)c->count.p, (const uint32_t*)c->offset.p,
+    launch_total(n, (const uint32_t*)c->cnt_s.p, (const uint32_t*)c->offset.p,
                  (uint64_t*)c->total.p, st);
     VG_LAUNCHED(c, 1);
     VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     VG_CUDA(cudaStreamSynchronize(st));
     uint64_t P = *c->total_host;
-    if (P > 0xffffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^32");
+    if (P > 0x7fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^31");
     c->pairs = (int64_t)P;
   }
   const int64_t P = c->pairs;
   if (P > 0) {
-    VG_TRY(ensure(c->keys0, sizeof(uint64_t) * (size_t)P, st));
-    VG_TRY(ensure(c->keys1, sizeof(uint64_t) * (size_t)P, st));
+    if (c->n_tiles > 65536) return fail(VG_EINVAL, "more than 65536 tiles");
+    VG_TRY(ensure(c->keys0, sizeof(uint16_t) * (size_t)P, st));
+    VG_TRY(ensure(c->keys1, sizeof(uint16_t) * (size_t)P, st));
     VG_TRY(ensure(c->vals0, sizeof(uint32_t) * (size_t)P, st));
     VG_TRY(ensure(c->vals1, sizeof(uint32_t) * (size_t)P, st));
     {
       ProfScope ps(c, VG_K_DUPLICATE, st);
-      launch_duplicate(n, (const uint32_t*)c->count.p, (const uint32_t*)c->offset.p,
-                       (const int4*)c->rect.p, (const float*)c->depth.p, k.ntx,
-                       (uint64_t*)c->keys0.p, (uint32_t*)c->vals0.p, st);
+      launch_duplicate_sorted(n, (const uint32_t*)c->perm.p, (const uint32_t*)c->offset.p,
+                              (const uint32_t*)c->cnt_s.p, (const int4*)c->rect.p, k.ntx,
+                              (uint16_t*)c->keys0.p, (uint32_t*)c->vals0.p, st);
     }
     VG_LAUNCHED(c, 1);
-    int tile_bits = 0;
+    int tile_bits = 1;
     while ((1 << tile_bits) < c->n_tiles) ++tile_bits;
-    int end_bit = 32 + tile_bits;
     size_t tmp = 0;
-    VG_CUDA(sort_temp_bytes(P, end_bit, &tmp));
+    VG_CUDA(tile_sort_temp_bytes(P, tile_bits, &tmp));
     VG_TRY(ensure(c->sort_tmp, tmp, st));
     int which = 0;
     {
       ProfScope ps(c, VG_K_SORT, st);
-      VG_CUDA(radix_sort_pairs(c->sort_tmp.p, c->sort_tmp.bytes, (uint64_t*)c->keys0.p,
-                               (uint64_t*)c->keys1.p, (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p,
-                               P, end_bit, &which, st));
+      VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, (uint16_t*)c->keys0.p,
+                        (uint16_t*)c->keys1.p, (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P,
+                        tile_bits, &which, st));
     }
-    c->launches += sort_launches(end_bit);
-    c->keys = which ? (uint64_t*)c->keys1.p : (uint64_t*)c->keys0.p;
+    c->launches += sort_launches(tile_bits);
+    c->keys = which ? (uint16_t*)c->keys1.p : (uint16_t*)c->keys0.p;
     c->vals = which ? (uint32_t*)c->vals1.p : (uint32_t*)c->vals0.p;
     {
       ProfScope ps(c, VG_K_RANGES, st);
-      launch_ranges(P, c->keys, (uint2*)c->ranges.p, st);
+      launch_ranges16(P, c->keys, (uint2*)c->ranges.p, st);
     }
     VG_LAUNCHED(c, 1);
   } else {
@@ -331,7 +351,7 @@ int vg_pair_count(vg_context* c, int64_t* out) {
   return VG_OK;
 }
 
-__global__ void k_tile_lists(int64_t P, const uint64_t* keys, const uint32_t* vals,
+__global__ void k_tile_lists(int64_t P, const uint32_t* vals,
                              const uint2* ranges, int n_tiles, int32_t* prims, int32_t* offsets) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < P) prims[i] = (int32_t)vals[i];
@@ -364,7 +384,7 @@ int vg_tile_lists(vg_context* c, int32_t* prims, int32_t* offsets, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   int64_t work = c->pairs > c->n_tiles + 1 ? c->pairs : c->n_tiles + 1;
   k_tile_lists<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
-      c->pairs, c->keys, c->vals, (const uint2*)c->ranges.p, c->n_tiles, prims, offsets);
+      c->pairs, c->vals, (const uint2*)c->ranges.p, c->n_tiles, prims, offsets);
   VG_LAUNCHED(c, 1);
   return VG_OK;
 }

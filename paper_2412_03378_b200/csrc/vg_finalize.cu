@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(128) k_finalize(FinalIn in, CamK c, vg_grads g
   float raw[13] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x};
   bool any = false;
   for (int k = 0; k < 13; ++k) any |= raw[k] != 0.f;
+  if (!any && g.accumulate) return;  // nothing to add for this view
   if (any) { float4 z = make_float4(0.f, 0.f, 0.f, 0.f); a4[0] = z; a4[1] = z; a4[2] = z; a4[3] = z; }
 
   double dmu[3] = {0, 0, 0}, ds[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0}, dth = 0, dk = 0;

@@ -35,6 +35,34 @@ cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t
 
 int sort_launches(int end_bit) { return 1 + (end_bit + 7) / 8; }
 
+// Gaussians by float32 view depth (positive floats sort as their bit
+// patterns); values start as the identity so equal depths keep index order.
+cudaError_t depth_sort_temp_bytes(int64_t n, size_t* bytes) {
+  return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, (const uint32_t*)nullptr,
+                                         (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                         (uint32_t*)nullptr, (int)n);
+}
+cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out,
+                       const uint32_t* ids_in, uint32_t* ids_out, int64_t n, cudaStream_t st) {
+  return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, ids_in, ids_out,
+                                         (int)n, 0, 32, st);
+}
+
+// Stable sort of the depth-ordered pairs by their 16-bit tile id.
+cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, size_t* bytes) {
+  cub::DoubleBuffer<uint16_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+  return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, k, v, (int)n, 0, end_bit);
+}
+cudaError_t tile_sort(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
+                      uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st) {
+  cub::DoubleBuffer<uint16_t> k(k0, k1);
+  cub::DoubleBuffer<uint32_t> v(v0, v1);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k, v, (int)n, 0, end_bit, st);
+  *which = k.selector;
+  return e;
+}
+
 // Heavy-tiles-first launch order: tiles sorted by descending list length, so
 // the longest tiles start in the first wave (longest-processing-time first).
 __global__ void k_tile_len(const uint2* ranges, uint32_t* len, uint32_t* ids, int n) {
