@@ -147,7 +147,7 @@ def run_gpu(args):
 
     from paper_2412_03378_b200 import _lib
     from paper_2412_03378_b200.engine import Engine
-    from paper_2412_03378_b200.raster import DeviceScene
+    from paper_2412_03378_b200.multiview import ViewShardedStep, shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -156,32 +156,20 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=dev)
     cfg = load_config(args.config, args.views)
     tomo = cfg.tomography
-    my_views = list(range(rank, len(cfg.cameras), ws))
+    my_views = shard(len(cfg.cameras), ws, rank)
     eng = Engine(local)
     ds = eng.upload(cfg.scene)
-    grads = eng.new_grads(ds)
     cams = cfg.cameras
     H, W = int(cams[0].height), int(cams[0].width)
     tshape = (H, W) if tomo else (H, W, 3)
     targets = {v: torch.from_numpy(cfg.target(v, tshape)).to(dev) for v in my_views}
-    loss = torch.zeros((), dtype=torch.float64, device=dev)
+    runner = ViewShardedStep(eng, ds, cams, targets, world=ws, rank=rank, tomography=tomo,
+                             parallel=cfg.parallel, extent=cfg.extent)
+    grads = runner.grads
+    loss = runner.loss
 
-    def step(scene_dev, tgts, gbuf):
-        loss.zero_()
-        for j, v in enumerate(my_views):
-            cam = cams[v]
-            if tomo:
-                eng.prepare(scene_dev, cam, tomo=True, parallel=cfg.parallel, extent=cfg.extent)
-                img = eng.tomo_forward()
-                eng.tomo_backward_l2(img, tgts[v], gbuf, accumulate=j > 0, loss=loss)
-            else:
-                eng.prepare(scene_dev, cam)
-                color, tfin, _ = eng.forward()
-                eng.backward_l2(color, tfin, tgts[v], gbuf, accumulate=j > 0, loss=loss)
-        if ws > 1:
-            dist.all_reduce(gbuf.flat)
-            dist.all_reduce(loss)
-        return loss
+    def step(scene_dev, tgts, gbuf=None):
+        return runner(scene_dev, tgts)
 
     for _ in range(args.warmup):
         step(ds, targets, grads)
@@ -228,7 +216,7 @@ def run_gpu(args):
     # --- end to end: host buffers in, host buffers out
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step)
+        e2e = run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner)
 
     result = None
     if rank == 0:
@@ -252,7 +240,7 @@ def run_gpu(args):
     return result
 
 
-def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step):
+def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
     import torch
     from paper_2412_03378_b200.raster import DeviceScene
     s = cfg.scene
@@ -263,7 +251,7 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step):
     htgt = {v: torch.from_numpy(cfg.target(v, tshape)).pin_memory() for v in my_views}
     dev_scene = DeviceScene(cfg.scene, dev.index)
     dtg = {v: torch.empty(tshape, dtype=torch.float32, device=dev) for v in my_views}
-    grads = eng.new_grads(dev_scene)
+    grads = runner.grads
     hgrad = torch.empty(grads.flat.shape, dtype=torch.float32).pin_memory()
     hloss = torch.empty((), dtype=torch.float64).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host.values()) + \
@@ -275,7 +263,7 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step):
             getattr(dev_scene, k).copy_(t.view(getattr(dev_scene, k).shape), non_blocking=True)
         for v in my_views:
             dtg[v].copy_(htgt[v], non_blocking=True)
-        loss = step(dev_scene, dtg, grads)
+        loss = step(dev_scene, dtg)
         hgrad.copy_(grads.flat, non_blocking=True)
         hloss.copy_(loss, non_blocking=True)
 

@@ -88,9 +88,16 @@ typedef struct {
 } vg_scene;
 
 /* grad.SceneGrads (grad.py:41-69) as device pointers.  Any pointer may be
- * NULL to skip that output.  With accumulate != 0 the results are ADDED to
- * the existing contents (multi-view gradient accumulation); otherwise they
- * overwrite. */
+ * NULL to skip that output.  `accumulate` selects how a backward call writes:
+ *   VG_OVERWRITE  this view's gradients overwrite every output;
+ *   VG_ADD        this view's gradients are added to every output;
+ *   VG_DEFER      multi-view accumulation: colour/SH gradients, d_background
+ *                 and visible are added now, the per-Gaussian geometry chain
+ *                 (means/scales/rotations/thetas/kappas) is summed over views
+ *                 inside the context and written by vg_finalize_grads. */
+#define VG_OVERWRITE 0
+#define VG_ADD 1
+#define VG_DEFER 2
 typedef struct {
   float* d_means;      /* N*3 */
   float* d_scales;     /* N*3 */
@@ -101,7 +108,7 @@ typedef struct {
   float* d_sh;         /* N*48, only with vg_scene.sh */
   float* d_background; /* 3   */
   uint8_t* visible;    /* N   (OR-accumulated) */
-  int32_t accumulate;
+  int32_t accumulate;  /* VG_OVERWRITE, VG_ADD or VG_DEFER */
   int32_t _pad;
 } vg_grads;
 
@@ -167,6 +174,11 @@ int vg_tomo_backward(vg_context* ctx, const float* d_image, vg_grads* grads, voi
  * sum((image-target)^2) added to *loss_sum. */
 int vg_tomo_backward_l2(vg_context* ctx, const float* image, const float* target,
                         double* loss_sum, vg_grads* grads, void* stream);
+
+/* Write the geometry gradients accumulated by VG_DEFER backward calls
+ * (analytic_param_chain, grad.py:242-259) into grads (overwrite when
+ * grads->accumulate == VG_OVERWRITE, else add) and reset the accumulator. */
+int vg_finalize_grads(vg_context* ctx, vg_grads* grads, void* stream);
 
 /* Number of kernels this context launched since creation (bench accounting). */
 int64_t vg_launch_count(vg_context* ctx);

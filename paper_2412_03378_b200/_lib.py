@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libvolgauss_b200.so")
 
 VG_OK, VG_EINVAL, VG_ECUDA, VG_ENOMEM = 0, 1, 2, 3
 VG_PINHOLE, VG_PARALLEL = 0, 1
+VG_OVERWRITE, VG_ADD, VG_DEFER = 0, 1, 2
 ABI_VERSION = 1
 
 
@@ -66,6 +67,7 @@ EXPORTS = {
     "vg_tomo_backward_l2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(VgGrads), C.c_void_p]),
     "vg_launch_count": (C.c_int64, [C.c_void_p]),
+    "vg_finalize_grads": (C.c_int, [C.c_void_p, C.POINTER(VgGrads), C.c_void_p]),
     "vg_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "vg_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "vg_probe_peaks": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -49,6 +49,7 @@ struct vg_context {
   Buf ranges, n_act, scan_tmp, sort_tmp, total;
   Buf tlen, tord, ord_tmp;  // heavy-first tile order
   Buf dkey, perm, cnt_s, dsort_tmp;  // depth pre-sort of the Gaussians
+  Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
   uint64_t* total_host = nullptr;
   // state of the last prepare
   vg_scene scene{};
@@ -147,7 +148,7 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
                 &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
                 &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp, &c->dkey,
-                &c->perm, &c->cnt_s, &c->dsort_tmp};
+                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -241,10 +242,13 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
     VG_TRY(ensure(c->perm, sizeof(uint32_t) * 2 * (size_t)n, st));
     VG_TRY(ensure(c->cnt_s, sizeof(uint32_t) * (size_t)n, st));
     if (grow_acc) VG_TRY(ensure(c->acc, accb, st, true));
+    if (c->lacc.bytes < sizeof(float) * 12 * (size_t)n)
+      VG_TRY(ensure(c->lacc, sizeof(float) * 12 * (size_t)n, st, true));
+    VG_TRY(ensure(c->frame, sizeof(float) * 12 * (size_t)n, st));
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
-                        (int4*)c->rect.p, (uint32_t*)c->count.p, st);
+                        (int4*)c->rect.p, (uint32_t*)c->count.p, (float*)c->frame.p, st);
     }
     VG_LAUNCHED(c, 1);
     // Gaussians in (float32 depth, index) order
@@ -442,9 +446,52 @@ int vg_n_active(vg_context* c, int32_t* out, void* stream) {
 
 static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
   if (!g) return fail(VG_EINVAL, "grads is NULL");
-  if (!g->accumulate) {
+  if (g->accumulate < VG_OVERWRITE || g->accumulate > VG_DEFER)
+    return fail(VG_EINVAL, "grads.accumulate must be VG_OVERWRITE, VG_ADD or VG_DEFER");
+  if (g->accumulate == VG_OVERWRITE) {
+    const size_t n = (size_t)c->scene.n;
     if (g->d_background) VG_CUDA(cudaMemsetAsync(g->d_background, 0, 3 * sizeof(float), st));
-    if (g->visible && c->scene.n) VG_CUDA(cudaMemsetAsync(g->visible, 0, (size_t)c->scene.n, st));
+    if (g->visible && n) VG_CUDA(cudaMemsetAsync(g->visible, 0, n, st));
+    if (g->d_colors && n) VG_CUDA(cudaMemsetAsync(g->d_colors, 0, 3 * n * sizeof(float), st));
+    if (g->d_sh && c->scene.sh && n) VG_CUDA(cudaMemsetAsync(g->d_sh, 0, 48 * n * sizeof(float), st));
+  }
+  return VG_OK;
+}
+
+// After a backward blend: rotate this view's accumulators into the
+// view-independent ones (and add colour / SH gradients), then -- unless the
+// caller defers -- run the float64 parameter chain.
+static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
+  const int64_t n = c->scene.n;
+  if (n <= 0) return VG_OK;
+  {
+    ProfScope ps(c, VG_K_FINALIZE, st);
+    launch_view_accumulate(n, c->scene, c->cam, (const float*)c->frame.p, (float*)c->acc.p,
+                           (float*)c->lacc.p, *g, st);
+  }
+  VG_LAUNCHED(c, 1);
+  if (g->accumulate != VG_DEFER) {
+    {
+      ProfScope ps(c, VG_K_FINALIZE, st);
+      launch_finalize_params(n, c->scene, (float*)c->lacc.p, *g, st);
+    }
+    VG_LAUNCHED(c, 1);
+  }
+  return VG_OK;
+}
+
+int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
+  if (!c || !g) return fail(VG_EINVAL, "vg_finalize_grads: NULL argument");
+  if (!c->prepared) return fail(VG_EINVAL, "vg_finalize_grads: no scene on this context");
+  vg_grads gg = *g;
+  gg.accumulate = g->accumulate == VG_OVERWRITE ? VG_OVERWRITE : VG_ADD;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->scene.n > 0) {
+    {
+      ProfScope ps(c, VG_K_FINALIZE, st);
+      launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, gg, st);
+    }
+    VG_LAUNCHED(c, 1);
   }
   return VG_OK;
 }
@@ -483,11 +530,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                         st);
     }
     VG_LAUNCHED(c, 1);
-    {
-      ProfScope ps(c, VG_K_FINALIZE, st);
-      launch_finalize(c->scene.n, c->scene, c->cam, (float*)c->acc.p, *g, st);
-    }
-    VG_LAUNCHED(c, 1);
+    VG_TRY(finish_view(c, g, st));
   } else {
     // empty scene: d_background = sum of d_color (grad.py:126-128) -- the
     // blend kernel still runs over the (empty) tiles to form it.
@@ -543,13 +586,7 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
                     target, scale, loss_sum, (float*)c->acc.p, vis, st);
   }
   VG_LAUNCHED(c, 1);
-  if (c->scene.n > 0) {
-    {
-      ProfScope ps(c, VG_K_FINALIZE, st);
-      launch_finalize(c->scene.n, c->scene, c->cam, (float*)c->acc.p, *g, st);
-    }
-    VG_LAUNCHED(c, 1);
-  }
+  VG_TRY(finish_view(c, g, st));
   return VG_OK;
 }
 

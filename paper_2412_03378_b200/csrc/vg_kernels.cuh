@@ -32,7 +32,7 @@ struct BwdIO {
 };
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, int4* rect, uint32_t* count, cudaStream_t st);
+                       float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st);
 void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,
                       const float* depth, int ntx, uint64_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t st);
@@ -52,8 +52,10 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
                      const float* d_image,
                      const float* image, const float* target, float loss_scale, double* loss_sum,
                      float* acc, uint8_t* visible, cudaStream_t st);
-void launch_finalize(int64_t n, const vg_scene& s, const CamK& c, float* acc, const vg_grads& g,
-                     cudaStream_t st);
+void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
+                            float* acc, float* lacc, const vg_grads& g, cudaStream_t st);
+void launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, const vg_grads& g,
+                            cudaStream_t st);
 
 // radix sort / scan (vg_sort.cu)
 cudaError_t scan_temp_bytes(int64_t n, size_t* bytes);

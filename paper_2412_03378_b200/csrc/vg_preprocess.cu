@@ -16,6 +16,7 @@ struct PrepOut {
   float* depth;        // sort key (float32 view depth)
   int4* rect;          // tile rectangle x0, y0, x1, y1 (inclusive)
   uint32_t* count;     // tiles overlapped (0 = not binned)
+  float* frame;        // e1, e2, e3 in whitened-local coordinates (12 floats)
 };
 
 __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __restrict__ means,
@@ -121,6 +122,10 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   } else if (colors) {
     rgb[0] = colors[3 * i]; rgb[1] = colors[3 * i + 1]; rgb[2] = colors[3 * i + 2];
   }
+  float4* fr = reinterpret_cast<float4*>(o.frame + 12 * i);
+  fr[0] = make_float4((float)f.e[0], (float)f.e[1], (float)f.e[2], (float)f.e[3]);
+  fr[1] = make_float4((float)f.e[4], (float)f.e[5], (float)f.e[6], (float)f.e[7]);
+  fr[2] = make_float4((float)f.e[8], 0.f, 0.f, 0.f);
   g.cr = (float)rgb[0];
   g.cg = (float)rgb[1];
   g.cb = (float)rgb[2];
@@ -128,9 +133,9 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
 }
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, int4* rect, uint32_t* count, cudaStream_t st) {
+                       float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st) {
   if (n <= 0) return;
-  PrepOut o{rec, depth, rect, count};
+  PrepOut o{rec, depth, rect, count, frame};
   int blocks = (int)((n + 255) / 256);
   k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
                                        s.sh, c, bin_cut, o);

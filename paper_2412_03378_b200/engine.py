@@ -101,6 +101,13 @@ class Engine:
             return out / color.numel()
         return out
 
+    def finalize(self, grads, accumulate=True):
+        """Write the geometry gradients of all VG_DEFER backward calls since
+        the last finalize into `grads` (added unless accumulate=False)."""
+        g = grads.struct(accumulate)
+        _lib.check(self.lib.vg_finalize_grads(self.ctx.handle, ctypes.byref(g), self.stream()),
+                   "vg_finalize_grads")
+
     def tomo_forward(self, slot=0, intensity=False):
         H, W = int(self.cam.height), int(self.cam.width)
         img = self._buf(("img", slot), (H, W), self.torch.float32)

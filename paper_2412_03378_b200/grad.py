@@ -95,13 +95,14 @@ class GradBuffers:
         self.visible = torch.zeros(max(n, 1), dtype=torch.uint8, device=device)
 
     def struct(self, accumulate=False):
+        """vg_grads view; accumulate: False/VG_OVERWRITE, True/VG_ADD or VG_DEFER."""
         g = _lib.VgGrads()
         for name in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_kappas",
                      "d_background"):
             setattr(g, name, _lib.ptr(self.views[name]).value)
         g.d_sh = _lib.ptr(self.views["d_sh"]).value if self.views["d_sh"] is not None else None
         g.visible = _lib.ptr(self.visible).value
-        g.accumulate = 1 if accumulate else 0
+        g.accumulate = int(accumulate) if not isinstance(accumulate, bool) else (1 if accumulate else 0)
         return g
 
     def zero_(self):

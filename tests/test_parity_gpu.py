@@ -186,6 +186,16 @@ def test_multiview_accumulation_and_order_independence():
         parts.append(one.flat.clone())
     total = sum(parts)
     check_field(acc.flat.cpu().numpy(), total.cpu().numpy(), "accumulated grads", rtol=1e-4, atol=1e-6)
+    # the deferred multi-view step (one float64 parameter-chain pass per step)
+    from paper_2412_03378_b200.multiview import ViewShardedStep
+    targets = {v: torch.tensor(cfg.target(v, (64, 64, 3)), device="cuda") for v in range(3)}
+    step = ViewShardedStep(eng, ds, cfg.cameras, targets)
+    step()
+    check_field(step.grads.flat.cpu().numpy(), total.cpu().numpy(), "deferred step grads",
+                rtol=1e-4, atol=1e-6)
+    step()   # a second step starts from clean accumulators
+    check_field(step.grads.flat.cpu().numpy(), total.cpu().numpy(), "second step grads",
+                rtol=1e-4, atol=1e-6)
 
 
 def test_full_size_large_view_tiles_and_sampled_pixels():
