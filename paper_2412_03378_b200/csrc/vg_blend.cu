@@ -293,12 +293,12 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
   const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
   const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
-  const int len = (int)(r.y - r.x);
-  F2 T = f2s(1.f), Cr = f2s(0.f), Cg = f2s(0.f), Cb = f2s(0.f);
-  // per-pixel floor of the transmittance factor: 1 - clamp while active,
-  // 1 once the pixel stopped (or lies outside the image) so alpha = 0 after.
+  // Pixels outside the image start (and stay) at T = 0: never active.
+  F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f);
+  F2 Cr = f2s(0.f), Cg = f2s(0.f), Cb = f2s(0.f);
+  // floor of the transmittance factor: 1 - clamp while active, 1 once stopped
   float fl0 = G.in0 ? p.cc : 1.f, fl1 = G.in1 ? p.cc : 1.f;
-  int nc0 = 0, nc1 = 0, na0 = len, na1 = len;
+  int nc0 = 0, nc1 = 0, na0 = 0, na1 = 0;
   bool done = !(G.in0 || G.in1);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     if (__syncthreads_count(done) == NT) break;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
     }
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);
-    const int jb = (int)(base - r.x);
+    const int jb = (int)(base - r.x) + 1;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
       const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
       unsigned bits = __ballot_sync(FULL, vb);
@@ -316,30 +316,40 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
         const SRec s = sm[k];
+        if (STOP) {
+          // active iff the transmittance in front is >= stop (raster.py:384-385);
+          // n_act = 1 + index of the last active processed entry
+          const bool a0 = lo(T) >= p.stop, a1 = hi(T) >= p.stop;
+          fl0 = a0 ? p.cc : 1.f;
+          fl1 = a1 ? p.cc : 1.f;
+          na0 = a0 ? jb + k : na0;
+          na1 = a1 ? jb + k : na1;
+        }
         const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
         float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
         if (CUT) {
-          if (om0 > p.omcut) om0 = 1.f;
-          if (om1 > p.omcut) om1 = 1.f;
+          const bool c0 = om0 > p.omcut, c1 = om1 > p.omcut;
+          om0 = c0 ? 1.f : om0;
+          om1 = c1 ? 1.f : om1;
+          nc0 += c0 ? 0 : 1;
+          nc1 += c1 ? 0 : 1;
+        } else {
+          nc0 += om0 < 1.f;
+          nc1 += om1 < 1.f;
         }
-        nc0 += om0 < 1.f;
-        nc1 += om1 < 1.f;
         const F2 om = f2(om0, om1);
-        const F2 a = sub2(f2s(1.f), om);
-        const F2 w = mul2(a, T);
+        const F2 w = mul2(sub2(f2s(1.f), om), T);
         Cr = fma2(w, f2s(s.d.x), Cr);
         Cg = fma2(w, f2s(s.d.y), Cg);
         Cb = fma2(w, f2s(s.d.z), Cb);
         T = mul2(T, om);
-        if (STOP) {
-          const int j1 = jb + k + 1;
-          if (fl0 < 1.f && lo(T) < p.stop) { fl0 = 1.f; na0 = j1; }
-          if (fl1 < 1.f && hi(T) < p.stop) { fl1 = 1.f; na1 = j1; }
-        }
       }
-      if (STOP) done = fl0 == 1.f && fl1 == 1.f;
+      if (STOP) done = !(lo(T) >= p.stop) && !(hi(T) >= p.stop);
     }
   }
+  const int len = (int)(r.y - r.x);
+  if (!STOP || lo(T) >= p.stop) na0 = len;
+  if (!STOP || hi(T) >= p.stop) na1 = len;
   const float t0 = lo(T), t1 = hi(T);
   if (G.in0) {
     const int pix = G.row0 * p.width + G.col;
@@ -363,31 +373,36 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
 
 // ---------------------------------------------------------------------------
 // per-pair gradient terms (shared by the render and cone-beam backward):
-// fills v[0..9] with h (rho rho^T + w^ w^T), h rho, h summed over 2 pixels.
+// fills v[0..9] with the two pixels' sum of h (rho rho^T + w^ w^T), h rho, h.
+// With s = D / |w|^2, rho = s (-w_par q1, -w_par q2, X), w^ = (q1, q2, w_par)/|w|:
+//   A11 = q1^2 k1, A12 = q1 k1 q2, A22 = k1 q2^2, A13 = q1 k2, A23 = k2 q2,
+//   A33 = h (s^2 X^2 + w_par^2 / |w|^2),  k1 = h (s^2 w_par^2 + 1/|w|^2),
+//   k2 = h w_par (1/|w|^2 - s^2 X); q1 is shared by the lane's two pixels.
+__device__ __forceinline__ float hsum(F2 x) { return lo(x) + hi(x); }
+
 __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s, F2 h,
                                                    float (&v)[16]) {
   const F2 ri = mul2(e.rs, e.rs);
-  const F2 dr = mul2(f2s(s.c.z), ri);
-  const F2 t = mul2(dr, e.wp);
-  const F2 r1 = mul2(t, f2s(-e.q1));
-  const F2 r2 = neg2(mul2(t, e.q2));
-  const F2 r3 = mul2(dr, e.X);
-  const F2 w1 = mul2(e.rs, f2s(e.q1));
-  const F2 w2 = mul2(e.rs, e.q2);
-  const F2 w3 = mul2(e.rs, e.wp);
-  const F2 hr1 = mul2(h, r1), hr2 = mul2(h, r2), hr3 = mul2(h, r3);
-  const F2 hw1 = mul2(h, w1), hw2 = mul2(h, w2), hw3 = mul2(h, w3);
-  F2 A;
-  A = fma2(hr1, r1, mul2(hw1, w1)); v[0] = lo(A) + hi(A);
-  A = fma2(hr1, r2, mul2(hw1, w2)); v[1] = lo(A) + hi(A);
-  A = fma2(hr1, r3, mul2(hw1, w3)); v[2] = lo(A) + hi(A);
-  A = fma2(hr2, r2, mul2(hw2, w2)); v[3] = lo(A) + hi(A);
-  A = fma2(hr2, r3, mul2(hw2, w3)); v[4] = lo(A) + hi(A);
-  A = fma2(hr3, r3, mul2(hw3, w3)); v[5] = lo(A) + hi(A);
-  v[6] = lo(hr1) + hi(hr1);
-  v[7] = lo(hr2) + hi(hr2);
-  v[8] = lo(hr3) + hi(hr3);
-  v[9] = lo(h) + hi(h);
+  const F2 sD = mul2(f2s(s.c.z), ri);
+  const F2 s2 = mul2(sD, sD);
+  const F2 wp2 = mul2(e.wp, e.wp);
+  const F2 k1 = mul2(h, fma2(s2, wp2, ri));
+  const F2 hw = mul2(h, e.wp);
+  const F2 k2 = mul2(hw, fma2(neg2(s2), e.X, ri));
+  const F2 k1q2 = mul2(k1, e.q2);
+  const float q1 = e.q1;
+  v[0] = q1 * q1 * hsum(k1);
+  v[1] = q1 * hsum(k1q2);
+  v[2] = q1 * hsum(k2);
+  v[3] = hsum(mul2(k1q2, e.q2));
+  v[4] = hsum(mul2(k2, e.q2));
+  v[5] = hsum(mul2(h, fma2(s2, mul2(e.X, e.X), mul2(ri, wp2))));
+  const F2 hs = mul2(h, sD);
+  const F2 hsw = mul2(hs, e.wp);
+  v[6] = -q1 * hsum(hsw);
+  v[7] = -hsum(mul2(hsw, e.q2));
+  v[8] = hsum(mul2(hs, e.X));
+  v[9] = hsum(h);
 }
 
 // ---------------------------------------------------------------------------
@@ -470,44 +485,44 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
         bits &= bits - 1;
         const int j = jb + k;
         const SRec s = sm[k];
-        const bool act0 = j < nav[0], act1 = j < nav[1];
         const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        // inactive entries (j >= n_act) get a floor of 1: alpha = 0, no change
+        const bool act0 = j < nav[0], act1 = j < nav[1];
         float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
         float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-        bool cut0 = false, cut1 = false;
-        if (CUT) {
-          cut0 = om0 > p.omcut;
-          cut1 = om1 > p.omcut;
-          if (cut0) om0 = 1.f;
-          if (cut1) om1 = 1.f;
-        }
+        // cut: skipped below alpha_cut (raster.py:363-365) or inactive
+        const bool cut0 = CUT ? om0 > p.omcut : !act0;
+        const bool cut1 = CUT ? om1 > p.omcut : !act1;
+        om0 = cut0 ? 1.f : om0;
+        om1 = cut1 ? 1.f : om1;
         const F2 om = f2(om0, om1);
-        const F2 a = sub2(f2s(1.f), om);
-        const F2 contrib = mul2(a, T);
+        const F2 contrib = mul2(sub2(f2s(1.f), om), T);
         const F2 Tn = mul2(T, om);
         const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
         P = fma2(dot, contrib, P);
-        // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
-        const bool live0 = act0 && !cut0 && lo(e.ex) > p.cc;
-        const bool live1 = act1 && !cut1 && hi(e.ex) > p.cc;
-        const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
-        const F2 h = mul2(de, e.G);
-        float v[16];
-        pinhole_grad_terms(e, s, h, v);
-        const F2 dr_ = mul2(contrib, dcr), dg_ = mul2(contrib, dcg), db_ = mul2(contrib, dcb);
-        v[10] = lo(dr_) + hi(dr_);
-        v[11] = lo(dg_) + hi(dg_);
-        v[12] = lo(db_) + hi(db_);
-        v[13] = v[14] = v[15] = 0.f;
         T = Tn;
+        // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
+        const bool live0 = !cut0 && lo(e.ex) > p.cc;
+        const bool live1 = !cut1 && hi(e.ex) > p.cc;
         const bool vis = om0 < 1.f || om1 < 1.f;
-        const bool nz = vis || live0 || live1;
-        if (__any_sync(FULL, nz)) {
-          const uint32_t gid = __float_as_uint(s.c.w);
-          const bool any_vis = __any_sync(FULL, vis);
-          if (lane == 0 && any_vis) io.visible[gid] = 1;
-          flush_acc(v, lane, gid, io.acc);
+        const bool any_live = __any_sync(FULL, live0 || live1);
+        const bool any_vis = __any_sync(FULL, vis);
+        if (!(any_live || any_vis)) continue;
+        float v[16];
+        if (any_live) {
+          const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
+          pinhole_grad_terms(e, s, mul2(de, e.G), v);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 10; ++q) v[q] = 0.f;
         }
+        v[10] = hsum(mul2(contrib, dcr));
+        v[11] = hsum(mul2(contrib, dcg));
+        v[12] = hsum(mul2(contrib, dcb));
+        v[13] = v[14] = v[15] = 0.f;
+        const uint32_t gid = __float_as_uint(s.c.w);
+        if (lane == 0 && any_vis) io.visible[gid] = 1;
+        flush_acc(v, lane, gid, io.acc);
       }
     }
   }

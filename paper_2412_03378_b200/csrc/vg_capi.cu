@@ -50,6 +50,7 @@ struct vg_context {
   Buf tlen, tord, ord_tmp;  // heavy-first tile order
   Buf dkey, perm, cnt_s, dsort_tmp;  // depth pre-sort of the Gaussians
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
+  Buf cacc;                          // colour / SH gradient accumulators, SoA [3|48][N]
   uint64_t* total_host = nullptr;
   // state of the last prepare
   vg_scene scene{};
@@ -148,7 +149,7 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
                 &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
                 &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp, &c->dkey,
-                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc};
+                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc, &c->cacc};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -245,6 +246,10 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
     if (c->lacc.bytes < sizeof(float) * 12 * (size_t)n)
       VG_TRY(ensure(c->lacc, sizeof(float) * 12 * (size_t)n, st, true));
     VG_TRY(ensure(c->frame, sizeof(float) * 12 * (size_t)n, st));
+    {
+      const size_t cb = sizeof(float) * (s->sh ? 48 : 3) * (size_t)n;
+      if (c->cacc.bytes < cb) VG_TRY(ensure(c->cacc, cb, st, true));
+    }
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
@@ -452,8 +457,6 @@ static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
     const size_t n = (size_t)c->scene.n;
     if (g->d_background) VG_CUDA(cudaMemsetAsync(g->d_background, 0, 3 * sizeof(float), st));
     if (g->visible && n) VG_CUDA(cudaMemsetAsync(g->visible, 0, n, st));
-    if (g->d_colors && n) VG_CUDA(cudaMemsetAsync(g->d_colors, 0, 3 * n * sizeof(float), st));
-    if (g->d_sh && c->scene.sh && n) VG_CUDA(cudaMemsetAsync(g->d_sh, 0, 48 * n * sizeof(float), st));
   }
   return VG_OK;
 }
@@ -467,15 +470,16 @@ static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
   {
     ProfScope ps(c, VG_K_FINALIZE, st);
     launch_view_accumulate(n, c->scene, c->cam, (const float*)c->frame.p, (float*)c->acc.p,
-                           (float*)c->lacc.p, *g, st);
+                           (float*)c->lacc.p, (float*)c->cacc.p, st);
   }
   VG_LAUNCHED(c, 1);
   if (g->accumulate != VG_DEFER) {
+    int k = 0;
     {
       ProfScope ps(c, VG_K_FINALIZE, st);
-      launch_finalize_params(n, c->scene, (float*)c->lacc.p, *g, st);
+      k = launch_finalize_params(n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p, *g, st);
     }
-    VG_LAUNCHED(c, 1);
+    VG_LAUNCHED(c, k);
   }
   return VG_OK;
 }
@@ -487,11 +491,12 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   gg.accumulate = g->accumulate == VG_OVERWRITE ? VG_OVERWRITE : VG_ADD;
   cudaStream_t st = (cudaStream_t)stream;
   if (c->scene.n > 0) {
+    int k = 0;
     {
       ProfScope ps(c, VG_K_FINALIZE, st);
-      launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, gg, st);
+      k = launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p, gg, st);
     }
-    VG_LAUNCHED(c, 1);
+    VG_LAUNCHED(c, k);
   }
   return VG_OK;
 }

@@ -30,12 +30,11 @@ namespace vg {
 struct ViewAccIn {
   int64_t n;
   const float* means;
-  const float* sh;       // optional SH-3 coefficients (for the basis only)
+  const float* sh;       // optional SH-3 coefficients (selects the SH pull-back)
   const float* frame;    // n * 12: e1, e2, e3 (whitened-local), pad
   float* acc;            // n * 16 per-view accumulators (zeroed here)
   float* lacc;           // n * 12 view-independent accumulators
-  float* d_colors;       // n * 3 (added), may be NULL
-  float* d_sh;           // n * 48 (added), may be NULL
+  float* cacc;           // [3 or 48][n] colour / SH gradient accumulators (SoA: coalesced)
 };
 
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
@@ -75,28 +74,59 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   l1.x += Al[4]; l1.y += Al[5]; l1.z += Bl[0]; l1.w += Bl[1];
   l2.x += Bl[2]; l2.y += raw[9];
   l4[0] = l0; l4[1] = l1; l4[2] = l2;
-  // colour: dL/dRGB of this view, and its SH pull-back (DC band basis = 1)
+  // colour: dL/dRGB of this view, or its SH pull-back (DC band basis = 1)
   const float dc[3] = {raw[10], raw[11], raw[12]};
   if (dc[0] == 0.f && dc[1] == 0.f && dc[2] == 0.f) return;
-  if (in.d_colors) {
-    in.d_colors[3 * i] += dc[0];
-    in.d_colors[3 * i + 1] += dc[1];
-    in.d_colors[3 * i + 2] += dc[2];
+  const int64_t n = in.n;
+  if (!in.sh) {
+    in.cacc[i] += dc[0];
+    in.cacc[n + i] += dc[1];
+    in.cacc[2 * n + i] += dc[2];
+    return;
   }
-  if (in.d_sh && in.sh) {
-    double d[3] = {in.means[3 * i] - c.center[0], in.means[3 * i + 1] - c.center[1],
-                   in.means[3 * i + 2] - c.center[2]};
-    const double dn = sqrt(dot3(d, d));
-    d[0] /= dn; d[1] /= dn; d[2] /= dn;
-    double b[16];
-    sh_basis(d, b);
-    float* o = in.d_sh + 48 * i;
+  double d[3] = {in.means[3 * i] - c.center[0], in.means[3 * i + 1] - c.center[1],
+                 in.means[3 * i + 2] - c.center[2]};
+  const double dn = sqrt(dot3(d, d));
+  d[0] /= dn; d[1] /= dn; d[2] /= dn;
+  double b[16];
+  sh_basis(d, b);
 #pragma unroll
-    for (int l = 0; l < 16; ++l) {
-      const float bl = (float)b[l];
-      o[3 * l] = fmaf(bl, dc[0], o[3 * l]);
-      o[3 * l + 1] = fmaf(bl, dc[1], o[3 * l + 1]);
-      o[3 * l + 2] = fmaf(bl, dc[2], o[3 * l + 2]);
+  for (int l = 0; l < 16; ++l) {
+    const float bl = (float)b[l];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float* o = in.cacc + (int64_t)(3 * l + ch) * n + i;
+      *o = fmaf(bl, dc[ch], *o);
+    }
+  }
+}
+
+// Colour / SH gradients from the SoA accumulators into the caller's AoS
+// layout (N*3 or N*16*3), 32 Gaussians per block transposed through shared
+// memory so both sides are coalesced; zeroes the accumulators.
+template <int W>
+__global__ void __launch_bounds__(256) k_color_out(int64_t n, float* cacc, float* out, int add) {
+  __shared__ float t[32][W + 1];
+  const int64_t g0 = (int64_t)blockIdx.x * 32;
+  for (int k = threadIdx.x; k < 32 * W; k += blockDim.x) {
+    const int comp = k / 32, gi = k % 32;
+    const int64_t g = g0 + gi;
+    float v = 0.f;
+    if (g < n) {
+      float* p = cacc + (int64_t)comp * n + g;
+      v = *p;
+      if (v != 0.f) *p = 0.f;
+    }
+    t[gi][comp] = v;
+  }
+  __syncthreads();
+  if (!out) return;
+  for (int k = threadIdx.x; k < 32 * W; k += blockDim.x) {
+    const int gi = k / W, comp = k % W;
+    const int64_t g = g0 + gi;
+    if (g < n) {
+      float* o = out + g * W + comp;
+      *o = add ? *o + t[gi][comp] : t[gi][comp];
     }
   }
 }
@@ -190,17 +220,27 @@ __global__ void __launch_bounds__(128) k_finalize_params(FinalIn in, vg_grads g)
 }
 
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
-                            float* acc, float* lacc, const vg_grads& g, cudaStream_t st) {
+                            float* acc, float* lacc, float* cacc, cudaStream_t st) {
   if (n <= 0) return;
-  ViewAccIn in{n, s.means, s.sh, frame, acc, lacc, g.d_colors, s.sh ? g.d_sh : nullptr};
+  ViewAccIn in{n, s.means, s.sh, frame, acc, lacc, cacc};
   k_view_accumulate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, c);
 }
 
-void launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, const vg_grads& g,
-                            cudaStream_t st) {
-  if (n <= 0) return;
+int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
+                           const vg_grads& g, cudaStream_t st) {
+  if (n <= 0) return 0;
   FinalIn in{n, s.scales, s.rotations, s.thetas, lacc};
   k_finalize_params<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, g);
+  const unsigned blocks = (unsigned)((n + 31) / 32);
+  const int add = g.accumulate != 0;
+  if (s.sh) {
+    k_color_out<48><<<blocks, 256, 0, st>>>(n, cacc, g.d_sh, add);
+    // d_colors (dL/d evaluated RGB) is not tracked separately for SH scenes
+    if (g.d_colors && !add) cudaMemsetAsync(g.d_colors, 0, sizeof(float) * 3 * (size_t)n, st);
+  } else {
+    k_color_out<3><<<blocks, 256, 0, st>>>(n, cacc, g.d_colors, add);
+  }
+  return 2;
 }
 
 }  // namespace vg

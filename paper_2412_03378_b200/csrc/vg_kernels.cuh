@@ -53,9 +53,10 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
                      const float* image, const float* target, float loss_scale, double* loss_sum,
                      float* acc, uint8_t* visible, cudaStream_t st);
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
-                            float* acc, float* lacc, const vg_grads& g, cudaStream_t st);
-void launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, const vg_grads& g,
-                            cudaStream_t st);
+                            float* acc, float* lacc, float* cacc, cudaStream_t st);
+// returns the number of kernels launched
+int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
+                           const vg_grads& g, cudaStream_t st);
 
 // radix sort / scan (vg_sort.cu)
 cudaError_t scan_temp_bytes(int64_t n, size_t* bytes);
