@@ -1,0 +1,69 @@
+"""Summarise ncu outputs into markdown for profiles/.
+
+    python tools/ncu_summary.py launches <launches.csv>      # per-kernel device time (cold, serialised)
+    python tools/ncu_summary.py full <report.ncu-rep>        # --set full key metrics per kernel
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = defaultdict(lambda: [0, 0.0])
+    for d in data:
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = d["Kernel Name"].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += float(d["Metric Value"].replace(",", ""))
+    tot = sum(v[1] for v in agg.values())
+    print("| kernel | launches | total us | share |")
+    print("|---|---|---|---|")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| `{k}` | {v[0]} | {v[1] / 1e3:.1f} | {100 * v[1] / tot:.1f}% |")
+
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration (ns)"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__inst_executed_pipe_xu.sum.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("sm__inst_executed_pipe_lsu.sum.pct_of_peak_sustained_active", "LSU pipe %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
+    ("dram__bytes_read.sum", "DRAM read (B)"),
+    ("dram__bytes_write.sum", "DRAM write (B)"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+]
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    idx = {h: i for i, h in enumerate(hdr)}
+    print("| kernel | " + " | ".join(k[1] for k in KEYS) + " |")
+    print("|---" * (len(KEYS) + 1) + "|")
+    for r in rows[2:]:
+        name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")
+        vals = [r[idx[k]] if k in idx else "" for k, _ in KEYS]
+        print(f"| `{name}` | " + " | ".join(vals) + " |")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
