@@ -274,7 +274,9 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
 // ---------------------------------------------------------------------------
 // K5 forward blend (raster.render)
 
-template <bool STOP, bool CUT>
+__device__ unsigned long long g_vg_stats[4];  // debug: processed / visible warp-entries, list entries
+
+template <bool STOP, bool CUT, bool STATS = false>
 __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
                                                    float* __restrict__ final_t,
                                                    int* __restrict__ n_contrib,
                                                    int* __restrict__ n_act) {
+  unsigned long long st_proc = 0, st_vis = 0, st_tot = 0;
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   const int tile = order[blockIdx.x];
@@ -343,9 +346,19 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
         Cg = fma2(w, f2s(s.d.y), Cg);
         Cb = fma2(w, f2s(s.d.z), Cb);
         T = mul2(T, om);
+        if (STATS) {
+          st_proc++;
+          st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
+        }
       }
+      if (STATS) st_tot += min(32, nb - c);
       if (STOP) done = !(lo(T) >= p.stop) && !(hi(T) >= p.stop);
     }
+  }
+  if (STATS && lane == 0) {
+    atomicAdd(&g_vg_stats[0], st_proc);
+    atomicAdd(&g_vg_stats[1], st_vis);
+    atomicAdd(&g_vg_stats[2], st_tot);
   }
   const int len = (int)(r.y - r.x);
   if (!STOP || lo(T) >= p.stop) na0 = len;
@@ -706,4 +719,20 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
 #undef VG_TB
 }
 
+}  // namespace vg
+
+namespace vg {
+// Debug statistics of one forward pass: {processed warp-entries, of which any
+// pixel had alpha > 0, list entries walked per warp}.  Not on the hot path.
+int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                        const uint32_t* order, const BlendParams& p, float* color, float* final_t,
+                        int* n_contrib, int* n_act, unsigned long long* out, cudaStream_t st) {
+  unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbolAsync(g_vg_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  k_render_fwd<true, true, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color,
+                                                        final_t, n_contrib, n_act);
+  cudaMemcpyFromSymbolAsync(out, g_vg_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return (int)cudaGetLastError();
+}
 }  // namespace vg

@@ -441,6 +441,17 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   return VG_OK;
 }
 
+// Debug (not in the public header): forward-pass culling statistics.
+int vg_debug_forward_stats(vg_context* c, float* color, float* final_t, int32_t* n_contrib,
+                           unsigned long long* out4, void* stream) {
+  if (!c || !c->prepared) return fail(VG_EINVAL, "vg_debug_forward_stats: not prepared");
+  BlendParams p = blend_params(c);
+  int e = debug_forward_stats(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                              (const uint32_t*)c->tord.p, p, color, final_t, n_contrib,
+                              (int*)c->n_act.p, out4, (cudaStream_t)stream);
+  return e ? fail(VG_ECUDA, "debug stats launch failed") : VG_OK;
+}
+
 int vg_n_active(vg_context* c, int32_t* out, void* stream) {
   if (!c || !out) return fail(VG_EINVAL, "vg_n_active: NULL argument");
   if (!c->have_fwd) return fail(VG_EINVAL, "vg_n_active: no forward on this context");

@@ -41,6 +41,9 @@ void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, cudaStream_t st);
+int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                        const uint32_t* order, const BlendParams& p, float* color, float* final_t,
+                        int* n_contrib, int* n_act, unsigned long long* out, cudaStream_t st);
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
                        const BwdIO& io, cudaStream_t st);
