@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
                                                    BlendParams p, float* __restrict__ color,
                                                    float* __restrict__ final_t,
                                                    int* __restrict__ n_contrib,
-                                                   int* __restrict__ n_act) {
+                                                   int* __restrict__ n_act,
+                                                   uint32_t* __restrict__ vmask, int vm_words) {
   unsigned long long st_proc = 0, st_vis = 0, st_tot = 0;
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
       const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
       unsigned bits = __ballot_sync(FULL, vb);
+      unsigned seen = 0;  // entries of this chunk with a visible pixel in this warp's block
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
@@ -346,10 +348,19 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
         Cg = fma2(w, f2s(s.d.y), Cg);
         Cb = fma2(w, f2s(s.d.z), Cb);
         T = mul2(T, om);
+        if (vmask && __any_sync(FULL, om0 < 1.f || om1 < 1.f)) seen |= 1u << (k - c);
         if (STATS) {
           st_proc++;
           st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
         }
+      }
+      if (vmask && seen && lane == 0) {
+        // record (entry, warp) visibility for the backward: bit g of this warp's row
+        const uint32_t g = base + c;
+        uint32_t* row = vmask + (size_t)warp * vm_words + (g >> 5);
+        const uint32_t sh = g & 31u;
+        atomicOr(row, seen << sh);
+        if (sh) atomicOr(row + 1, seen >> (32u - sh));
       }
       if (STATS) st_tot += min(32, nb - c);
       if (STOP) done = !(lo(T) >= p.stop) && !(hi(T) >= p.stop);
@@ -426,7 +437,9 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
                                                    const uint32_t* __restrict__ order,
-                                                   BlendParams p, BwdIO io) {
+                                                   BlendParams p, BwdIO io,
+                                                   const uint32_t* __restrict__ vmask,
+                                                   int vm_words) {
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   __shared__ int s_maxna;
@@ -485,14 +498,28 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
     __syncthreads();
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
-      if (i < end) smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut);
+      if (i < end) {
+        const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
+        if (!vmask) smask[sidx] = (uint8_t)m;
+      }
     }
     __syncthreads();
     const int jb = (int)(base - r.x);
     const int nb = min(min((int)BATCH, (int)(end - base)), warp_na - jb);
     for (int c = 0; c < nb; c += 32) {
-      const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
-      unsigned bits = __ballot_sync(FULL, vb);
+      unsigned bits;
+      if (vmask) {
+        // exact: the entries where the forward saw a visible pixel in this block
+        const uint32_t g = base + c;
+        const uint32_t* row = vmask + (size_t)warp * vm_words + (g >> 5);
+        const uint32_t sh = g & 31u;
+        bits = __ldg(row) >> sh;
+        if (sh) bits |= __ldg(row + 1) << (32u - sh);
+        if (nb - c < 32) bits &= (1u << (nb - c)) - 1u;
+      } else {
+        const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
+        bits = __ballot_sync(FULL, vb);
+      }
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
@@ -671,10 +698,11 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
 
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
-                       float* color, float* final_t, int* n_contrib, int* n_act, cudaStream_t st) {
+                       float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
+                       int vm_words, cudaStream_t st) {
 #define VG_RF(S, C)                                                                             \
   k_render_fwd<S, C><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color, final_t,       \
-                                             n_contrib, n_act)
+                                             n_contrib, n_act, vmask, vm_words)
   if (stop && cut) VG_RF(true, true);
   else if (stop) VG_RF(true, false);
   else if (cut) VG_RF(false, true);
@@ -684,8 +712,9 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
 
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
-                       const BwdIO& io, cudaStream_t st) {
-#define VG_RB(C, L) k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io)
+                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
+#define VG_RB(C, L) \
+  k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
   if (cut) {
     if (loss) VG_RB(true, 1); else VG_RB(true, 0);
   } else {
@@ -730,7 +759,7 @@ int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, cons
   unsigned long long z[4] = {0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(g_vg_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   k_render_fwd<true, true, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color,
-                                                        final_t, n_contrib, n_act);
+                                                        final_t, n_contrib, n_act, nullptr, 0);
   cudaMemcpyFromSymbolAsync(out, g_vg_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   return (int)cudaGetLastError();

@@ -51,6 +51,9 @@ struct vg_context {
   Buf dkey, perm, cnt_s, dsort_tmp;  // depth pre-sort of the Gaussians
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
   Buf cacc;                          // colour / SH gradient accumulators, SoA [3|48][N]
+  Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
+  int vm_words = 0;
+  bool vmask_valid = false;
   uint64_t* total_host = nullptr;
   // state of the last prepare
   vg_scene scene{};
@@ -149,7 +152,7 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
                 &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
                 &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp, &c->dkey,
-                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc, &c->cacc};
+                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc, &c->cacc, &c->vmask};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -347,6 +350,7 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
 
 int vg_set_options(vg_context* c, const vg_options* opt) {
   if (!c || !opt) return fail(VG_EINVAL, "vg_set_options: NULL argument");
+  if (opt->alpha_cut != c->opt.alpha_cut) c->vmask_valid = false;
   c->opt.early_stop = opt->early_stop;
   c->opt.alpha_cut = opt->alpha_cut;
   c->opt.alpha_clamp = opt->alpha_clamp;
@@ -429,12 +433,25 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   if (c->cam.projection != VG_PINHOLE) return fail(VG_EINVAL, "render needs a pinhole camera");
   cudaStream_t st = (cudaStream_t)stream;
   BlendParams p = blend_params(c);
+  // with alpha_cut > 0, "live => not cut => visible": the forward records
+  // which (entry, warp block) pairs had a visible pixel and the backward
+  // walks exactly those
+  const bool use_vm = c->opt.alpha_cut > 0 && c->pairs > 0;
+  uint32_t* vm = nullptr;
+  if (use_vm) {
+    c->vm_words = (int)((c->pairs + 31) / 32) + 1;
+    const size_t bytes = sizeof(uint32_t) * 4 * (size_t)c->vm_words;
+    VG_TRY(ensure(c->vmask, bytes, st));
+    VG_CUDA(cudaMemsetAsync(c->vmask.p, 0, bytes, st));
+    vm = (uint32_t*)c->vmask.p;
+  }
+  c->vmask_valid = use_vm;
   {
     ProfScope ps(c, VG_K_RENDER_FWD, st);
     launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                       (const uint32_t*)c->tord.p, p,
                       c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
-                      (int*)c->n_act.p, st);
+                      (int*)c->n_act.p, vm, c->vm_words, st);
   }
   VG_LAUNCHED(c, 1);
   c->have_fwd = true;
@@ -541,9 +558,10 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
   if (c->scene.n > 0) {
     {
       ProfScope ps(c, VG_K_RENDER_BWD, st);
+      const bool vm = c->vmask_valid && c->opt.alpha_cut > 0;
       launch_render_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                         (const uint32_t*)c->tord.p, p, c->opt.alpha_cut > 0, target ? 1 : 0, io,
-                        st);
+                        vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st);
     }
     VG_LAUNCHED(c, 1);
     VG_TRY(finish_view(c, g, st));
@@ -551,7 +569,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     // empty scene: d_background = sum of d_color (grad.py:126-128) -- the
     // blend kernel still runs over the (empty) tiles to form it.
     launch_render_bwd(c->n_tiles, nullptr, nullptr, (const uint2*)c->ranges.p,
-                      (const uint32_t*)c->tord.p, p, false, target ? 1 : 0, io, st);
+                      (const uint32_t*)c->tord.p, p, false, target ? 1 : 0, io, nullptr, 0, st);
     VG_LAUNCHED(c, 1);
   }
   return VG_OK;

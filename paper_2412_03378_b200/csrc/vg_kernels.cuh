@@ -38,15 +38,18 @@ void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, 
 void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t st);
 void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
                   cudaStream_t st);
+// vmask (optional): per-warp bit rows of vm_words words marking the list
+// entries where the forward saw a visible pixel (the backward's work list).
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
-                       float* color, float* final_t, int* n_contrib, int* n_act, cudaStream_t st);
+                       float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
+                       int vm_words, cudaStream_t st);
 int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                         const uint32_t* order, const BlendParams& p, float* color, float* final_t,
                         int* n_contrib, int* n_act, unsigned long long* out, cudaStream_t st);
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
-                       const BwdIO& io, cudaStream_t st);
+                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st);
 void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
                      float* image, float* intensity, cudaStream_t st);

@@ -57,7 +57,9 @@ def full(path):
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
     idx = {h: i for i, h in enumerate(hdr)}
-    print("| kernel | " + " | ".join(k[1] for k in KEYS) + " |")
+    units = rows[1]
+    print("| kernel | " + " | ".join(f"{k[1]} [{units[idx[k[0]]]}]" if k[0] in idx else k[1]
+                                    for k in KEYS) + " |")
     print("|---" * (len(KEYS) + 1) + "|")
     for r in rows[2:]:
         name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "")
