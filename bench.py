@@ -229,8 +229,7 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
-            "config": {"workload": f"config {'3' if args.config == 'large' else args.config}: "
-                                   + cfg.description,
+            "config": {"workload": cfg.description,
                        "views_per_step": len(cams), "pixels_per_step": px_step,
                        "gaussians": len(cfg.scene), "parallelism": f"views sharded over {ws} GPU(s)",
                        "l2_flush": "inputs larger than L2 (scene + SH coefficients > 126 MB)"},
@@ -418,8 +417,10 @@ def run_reference(args):
     cfg = load_config(args.config, args.views)
     samples = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(cfg, args.cpu_tiles or 16, seed=i, budget_s=20.0)
-        if i >= args.warmup:
+        warm = i < args.warmup
+        r = cpu_sample(cfg, 8 if warm else (args.cpu_tiles or 64), seed=i,
+                       budget_s=3.0 if warm else 12.0)
+        if not warm:
             samples.append(r)
     val = statistics.mean(r["value"] for r in samples)
     ms_step = len(cfg.cameras) * cfg.cameras[0].height * cfg.cameras[0].width / (val * 1e6) * 1e3
@@ -428,8 +429,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
             "impl": "reference",
-            "config": {"workload": f"config {'3' if args.config == 'large' else args.config}: "
-                                   + cfg.description, "views_per_step": len(cfg.cameras)},
+            "config": {"workload": cfg.description, "views_per_step": len(cfg.cameras)},
             "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(val, 6)},
             "e2e": {"value": round(val, 6), "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
