@@ -257,12 +257,21 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
         sum(t.numel() * t.element_size() for t in htgt.values())
     d2h = hgrad.numel() * 4 + 8
 
+    copy_stream = torch.cuda.Stream(device=dev)
+    main = torch.cuda.current_stream(dev)
+    ev = {v: torch.cuda.Event() for v in my_views}
+
     def one():
+        # scene first (every view needs it); the per-view targets stream in on
+        # a side stream and each view waits only for its own target
         for k, t in host.items():
             getattr(dev_scene, k).copy_(t.view(getattr(dev_scene, k).shape), non_blocking=True)
-        for v in my_views:
-            dtg[v].copy_(htgt[v], non_blocking=True)
-        loss = step(dev_scene, dtg)
+        copy_stream.wait_stream(main)
+        with torch.cuda.stream(copy_stream):
+            for v in my_views:
+                dtg[v].copy_(htgt[v], non_blocking=True)
+                ev[v].record(copy_stream)
+        loss = runner(dev_scene, dtg, ready=ev)
         hgrad.copy_(grads.flat, non_blocking=True)
         hloss.copy_(loss, non_blocking=True)
 

@@ -244,6 +244,33 @@ __device__ __forceinline__ void flush_acc(float (&v)[16], int lane, uint32_t gid
   if (!(lane & 1) && idx < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + idx, s);
 }
 
+// Warp reduction of 13 per-lane values through a shared-memory transpose:
+// each lane stores its 16-float row (4 x STS.128, row stride 20 floats), then
+// lane l sums column (l & 15) over the 16 rows of its half-warp (half 1 walks
+// its rows rotated by 4 so the two halves hit disjoint banks), and one
+// shuffle joins the halves; lanes 0..12 add the result to global memory.
+// ~39 instructions instead of ~61 for the shuffle/select butterfly.
+constexpr int RED_STRIDE = 20;
+__device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, float* red,
+                                               uint32_t gid, float* acc) {
+  float4* row = reinterpret_cast<float4*>(red + lane * RED_STRIDE);
+  row[0] = make_float4(v[0], v[1], v[2], v[3]);
+  row[1] = make_float4(v[4], v[5], v[6], v[7]);
+  row[2] = make_float4(v[8], v[9], v[10], v[11]);
+  row[3] = make_float4(v[12], 0.f, 0.f, 0.f);
+  __syncwarp();
+  const int col = lane & 15, half = lane >> 4;
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int r = half * 16 + ((k + 4 * half) & 15);
+    s += red[r * RED_STRIDE + col];
+  }
+  __syncwarp();
+  s += __shfl_xor_sync(FULL, s, 16);
+  if (lane < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + lane, s);
+}
+
 // Block sum of 3 floats + 1 double into global (d_background, loss).
 __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double l, float* out3,
                                             double* outl) {
@@ -443,6 +470,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   __shared__ int s_maxna;
+  __shared__ __align__(16) float sred[(NT / 32) * 32 * RED_STRIDE];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -562,7 +590,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
         v[13] = v[14] = v[15] = 0.f;
         const uint32_t gid = __float_as_uint(s.c.w);
         if (lane == 0 && any_vis) io.visible[gid] = 1;
-        flush_acc(v, lane, gid, io.acc);
+        flush_acc_smem(v, lane, sred + warp * 32 * RED_STRIDE, gid, io.acc);
       }
     }
   }

@@ -67,6 +67,7 @@ class ViewShardedStep:
         self.extent = extent
         self.group = group
         self.grads = engine.new_grads(dscene)
+        self.ready = None
         self.loss = torch.zeros((), dtype=torch.float64, device=engine.device)
 
     def _view(self, v, accumulate):
@@ -76,6 +77,9 @@ class ViewShardedStep:
         if not accumulate:
             self.grads.zero_()
         accumulate = VG_DEFER
+        if self.ready is not None and v in self.ready:
+            # the target of this view is still streaming in on a copy stream
+            self.eng.torch.cuda.current_stream(self.eng.device).wait_event(self.ready[v])
         eng, cam = self.eng, self.cams[v]
         if self.tomo:
             eng.prepare(self.ds, cam, tomo=True, parallel=self.parallel, extent=self.extent)
@@ -88,10 +92,13 @@ class ViewShardedStep:
             eng.backward_l2(color, tfin, self.targets[v], self.grads, accumulate=accumulate,
                             loss=self.loss)
 
-    def __call__(self, dscene=None, targets=None):
+    def __call__(self, dscene=None, targets=None, ready=None):
+        """Run the step.  `ready` optionally maps view -> CUDA event that the
+        view's target upload recorded (host->device copies overlap compute)."""
         if dscene is not None:
             self.ds = dscene
         if targets is not None:
             self.targets = targets
+        self.ready = ready
         return sharded_step(self.views, self._view, self.grads.flat, self.loss, self.group,
                             finish=lambda: self.eng.finalize(self.grads, accumulate=True))
