@@ -59,11 +59,12 @@ __global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ perm,
   if (i < n) out[i] = count[perm[i]];
 }
 
+template <typename KeyT>
 __global__ void __launch_bounds__(256) k_duplicate_sorted(int64_t n, const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ offset,
                                                           const uint32_t* __restrict__ count_sorted,
                                                           const int4* __restrict__ rect, int ntx,
-                                                          uint16_t* __restrict__ keys,
+                                                          KeyT* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -74,14 +75,15 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(int64_t n, const uint3
   int4 r = rect[g];
   for (int y = r.y; y <= r.w; ++y)
     for (int x = r.x; x <= r.z; ++x) {
-      keys[o] = (uint16_t)(y * ntx + x);
+      keys[o] = (KeyT)(y * ntx + x);
       vals[o] = g;
       ++o;
     }
 }
 
-__global__ void __launch_bounds__(256) k_ranges16(int64_t P, const uint16_t* __restrict__ keys,
-                                                  uint2* __restrict__ ranges) {
+template <typename KeyT>
+__global__ void __launch_bounds__(256) k_tile_ranges(int64_t P, const KeyT* __restrict__ keys,
+                                                     uint2* __restrict__ ranges) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   uint32_t t = keys[i];
@@ -97,14 +99,22 @@ void launch_gather_counts(int64_t n, const uint32_t* perm, const uint32_t* count
   if (n > 0) k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, count, out);
 }
 void launch_duplicate_sorted(int64_t n, const uint32_t* perm, const uint32_t* offset,
-                             const uint32_t* count_sorted, const int4* rect, int ntx,
-                             uint16_t* keys, uint32_t* vals, cudaStream_t st) {
-  if (n > 0)
-    k_duplicate_sorted<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, offset, count_sorted,
-                                                                     rect, ntx, keys, vals);
+                             const uint32_t* count_sorted, const int4* rect, int ntx, void* keys,
+                             bool wide, uint32_t* vals, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (wide)
+    k_duplicate_sorted<uint32_t><<<g, 256, 0, st>>>(n, perm, offset, count_sorted, rect, ntx,
+                                                    (uint32_t*)keys, vals);
+  else
+    k_duplicate_sorted<uint16_t><<<g, 256, 0, st>>>(n, perm, offset, count_sorted, rect, ntx,
+                                                    (uint16_t*)keys, vals);
 }
-void launch_ranges16(int64_t P, const uint16_t* keys, uint2* ranges, cudaStream_t st) {
-  if (P > 0) k_ranges16<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges);
+void launch_tile_ranges(int64_t P, const void* keys, bool wide, uint2* ranges, cudaStream_t st) {
+  if (P <= 0) return;
+  const unsigned g = (unsigned)((P + 255) / 256);
+  if (wide) k_tile_ranges<uint32_t><<<g, 256, 0, st>>>(P, (const uint32_t*)keys, ranges);
+  else k_tile_ranges<uint16_t><<<g, 256, 0, st>>>(P, (const uint16_t*)keys, ranges);
 }
 
 void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,

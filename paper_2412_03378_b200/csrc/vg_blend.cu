@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   __shared__ int s_maxna;
-  __shared__ __align__(16) float sred[(NT / 32) * 32 * RED_STRIDE];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -590,7 +589,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
         v[13] = v[14] = v[15] = 0.f;
         const uint32_t gid = __float_as_uint(s.c.w);
         if (lane == 0 && any_vis) io.visible[gid] = 1;
-        flush_acc_smem(v, lane, sred + warp * 32 * RED_STRIDE, gid, io.acc);
+        flush_acc(v, lane, gid, io.acc);
       }
     }
   }

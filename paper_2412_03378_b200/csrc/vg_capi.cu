@@ -61,7 +61,7 @@ struct vg_context {
   vg_options opt{};
   int64_t pairs = 0;
   int n_tiles = 0;
-  uint16_t* keys = nullptr;  // sorted buffers (tile ids)
+  void* keys = nullptr;      // sorted tile ids (uint16, or uint32 beyond 65536 tiles)
   uint32_t* vals = nullptr;
   bool prepared = false;
   bool have_fwd = false;
@@ -294,36 +294,37 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
   }
   const int64_t P = c->pairs;
   if (P > 0) {
-    if (c->n_tiles > 65536) return fail(VG_EINVAL, "more than 65536 tiles");
-    VG_TRY(ensure(c->keys0, sizeof(uint16_t) * (size_t)P, st));
-    VG_TRY(ensure(c->keys1, sizeof(uint16_t) * (size_t)P, st));
+    const bool wide = c->n_tiles > 65536;
+    const size_t kb = wide ? sizeof(uint32_t) : sizeof(uint16_t);
+    VG_TRY(ensure(c->keys0, kb * (size_t)P, st));
+    VG_TRY(ensure(c->keys1, kb * (size_t)P, st));
     VG_TRY(ensure(c->vals0, sizeof(uint32_t) * (size_t)P, st));
     VG_TRY(ensure(c->vals1, sizeof(uint32_t) * (size_t)P, st));
     {
       ProfScope ps(c, VG_K_DUPLICATE, st);
       launch_duplicate_sorted(n, (const uint32_t*)c->perm.p, (const uint32_t*)c->offset.p,
                               (const uint32_t*)c->cnt_s.p, (const int4*)c->rect.p, k.ntx,
-                              (uint16_t*)c->keys0.p, (uint32_t*)c->vals0.p, st);
+                              c->keys0.p, wide, (uint32_t*)c->vals0.p, st);
     }
     VG_LAUNCHED(c, 1);
     int tile_bits = 1;
     while ((1 << tile_bits) < c->n_tiles) ++tile_bits;
     size_t tmp = 0;
-    VG_CUDA(tile_sort_temp_bytes(P, tile_bits, &tmp));
+    VG_CUDA(tile_sort_temp_bytes(P, tile_bits, wide, &tmp));
     VG_TRY(ensure(c->sort_tmp, tmp, st));
     int which = 0;
     {
       ProfScope ps(c, VG_K_SORT, st);
-      VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, (uint16_t*)c->keys0.p,
-                        (uint16_t*)c->keys1.p, (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P,
-                        tile_bits, &which, st));
+      VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, c->keys0.p, c->keys1.p,
+                        (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P, tile_bits, wide, &which,
+                        st));
     }
     c->launches += sort_launches(tile_bits);
-    c->keys = which ? (uint16_t*)c->keys1.p : (uint16_t*)c->keys0.p;
+    c->keys = which ? c->keys1.p : c->keys0.p;
     c->vals = which ? (uint32_t*)c->vals1.p : (uint32_t*)c->vals0.p;
     {
       ProfScope ps(c, VG_K_RANGES, st);
-      launch_ranges16(P, c->keys, (uint2*)c->ranges.p, st);
+      launch_tile_ranges(P, c->keys, wide, (uint2*)c->ranges.p, st);
     }
     VG_LAUNCHED(c, 1);
   } else {

@@ -75,17 +75,18 @@ int sort_launches(int end_bit);
 cudaError_t depth_sort_temp_bytes(int64_t n, size_t* bytes);
 cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out,
                        const uint32_t* ids_in, uint32_t* ids_out, int64_t n, cudaStream_t st);
-cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, size_t* bytes);
-cudaError_t tile_sort(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
-                      uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st);
+cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, bool wide, size_t* bytes);
+cudaError_t tile_sort(void* tmp, size_t tmp_bytes, void* k0, void* k1, uint32_t* v0, uint32_t* v1,
+                      int64_t n, int end_bit, bool wide, int* which, cudaStream_t st);
 // binning kernels over the depth order (vg_binning.cu)
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
 void launch_gather_counts(int64_t n, const uint32_t* perm, const uint32_t* count, uint32_t* out,
                           cudaStream_t st);
+// tile keys are uint16 when n_tiles <= 65536 (wide = false), else uint32
 void launch_duplicate_sorted(int64_t n, const uint32_t* perm, const uint32_t* offset,
-                             const uint32_t* count_sorted, const int4* rect, int ntx,
-                             uint16_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_ranges16(int64_t P, const uint16_t* keys, uint2* ranges, cudaStream_t st);
+                             const uint32_t* count_sorted, const int4* rect, int ntx, void* keys,
+                             bool wide, uint32_t* vals, cudaStream_t st);
+void launch_tile_ranges(int64_t P, const void* keys, bool wide, uint2* ranges, cudaStream_t st);
 // heavy-tiles-first order: tile ids sorted by descending list length
 cudaError_t tile_order_temp_bytes(int n_tiles, size_t* bytes);
 cudaError_t tile_order(void* tmp, size_t tmp_bytes, const uint2* ranges, uint32_t* len_in,

@@ -48,19 +48,31 @@ cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uin
                                          (int)n, 0, 32, st);
 }
 
-// Stable sort of the depth-ordered pairs by their 16-bit tile id.
-cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, size_t* bytes) {
-  cub::DoubleBuffer<uint16_t> k(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
-  return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, k, v, (int)n, 0, end_bit);
-}
-cudaError_t tile_sort(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
-                      uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st) {
-  cub::DoubleBuffer<uint16_t> k(k0, k1);
+// Stable sort of the depth-ordered pairs by their tile id: 16-bit keys up to
+// 65536 tiles (two 8-bit passes at 1080p), 32-bit keys beyond (e.g. 8K).
+template <typename K>
+static cudaError_t tile_sort_t(void* tmp, size_t* tmp_bytes, K* k0, K* k1, uint32_t* v0,
+                               uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st) {
+  cub::DoubleBuffer<K> k(k0, k1);
   cub::DoubleBuffer<uint32_t> v(v0, v1);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k, v, (int)n, 0, end_bit, st);
-  *which = k.selector;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, *tmp_bytes, k, v, (int)n, 0, end_bit, st);
+  if (which) *which = k.selector;
   return e;
+}
+cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, bool wide, size_t* bytes) {
+  if (wide)
+    return tile_sort_t<uint32_t>(nullptr, bytes, nullptr, nullptr, nullptr, nullptr, n, end_bit,
+                                 nullptr, 0);
+  return tile_sort_t<uint16_t>(nullptr, bytes, nullptr, nullptr, nullptr, nullptr, n, end_bit,
+                               nullptr, 0);
+}
+cudaError_t tile_sort(void* tmp, size_t tmp_bytes, void* k0, void* k1, uint32_t* v0, uint32_t* v1,
+                      int64_t n, int end_bit, bool wide, int* which, cudaStream_t st) {
+  if (wide)
+    return tile_sort_t<uint32_t>(tmp, &tmp_bytes, (uint32_t*)k0, (uint32_t*)k1, v0, v1, n,
+                                 end_bit, which, st);
+  return tile_sort_t<uint16_t>(tmp, &tmp_bytes, (uint16_t*)k0, (uint16_t*)k1, v0, v1, n, end_bit,
+                               which, st);
 }
 
 // Heavy-tiles-first launch order: tiles sorted by descending list length, so

@@ -198,20 +198,27 @@ def test_multiview_accumulation_and_order_independence():
                 rtol=1e-4, atol=1e-6)
 
 
-def test_full_size_large_view_tiles_and_sampled_pixels():
-    """Config 3 (N=1M, 1920x1080) first view: every tile list bit-exact
-    against the oracle's float32-key order, and a sample of tiles rendered
-    and back-propagated against the float64 oracle."""
-    import torch
-    from paper_2412_03378_b200 import configs
-    cfg = configs.large()
-    s = cfg.scene
-    cam = cfg.cameras[0]
+def _f64_scene(s, colors=True):
     from types import SimpleNamespace
-    colors = s.colors  # per-view SH colour is checked separately; use DC RGB here
-    scene = SimpleNamespace(means=s.means.astype(np.float64), scales=s.scales.astype(np.float64),
-                            rotations=s.rotations.astype(np.float64), thetas=s.thetas.astype(np.float64),
-                            colors=colors.astype(np.float64), background=np.zeros(3))
+    return SimpleNamespace(means=s.means.astype(np.float64), scales=s.scales.astype(np.float64),
+                           rotations=s.rotations.astype(np.float64),
+                           thetas=s.thetas.astype(np.float64),
+                           colors=s.colors.astype(np.float64), background=np.zeros(3))
+
+
+def _tile_mask(oprep, tiles, H, W):
+    mask = np.zeros((H, W), dtype=bool)
+    for t in tiles:
+        ty, tx = divmod(t, oprep.tiles_x)
+        mask[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+    return mask
+
+
+def _full_size_check(scene, cam, n_random=5, seed=5):
+    """Every tile list bit-exact against the oracle's float32-key order; a
+    seeded sample of tiles (incl. the three heaviest) rendered and
+    back-propagated against the float64 oracle (d_color vanishes outside the
+    sampled tiles and on knife-edge pixels, on both sides)."""
     prep = vg().prepare(scene, cam)
     oprep = O.prepare(scene, cam, key_dtype=np.float32)
     assert prep.pair_count() == len(oprep.pair_prim)
@@ -219,23 +226,116 @@ def test_full_size_large_view_tiles_and_sampled_pixels():
     assert np.array_equal(offs.cpu().numpy(), oprep.tile_start)
     assert np.array_equal(prims.cpu().numpy(), oprep.pair_prim)
     out = vg().render(scene, cam, prep=prep)
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(seed)
     busy = np.argsort(np.diff(oprep.tile_start))[-3:]
-    tiles = sorted(set(busy.tolist()) | set(rng.integers(0, oprep.tiles_x * oprep.tiles_y, 5).tolist()))
+    tiles = sorted(set(busy.tolist()) |
+                   set(rng.integers(0, oprep.tiles_x * oprep.tiles_y, n_random).tolist()))
     ref = O.render(scene, cam, prep=oprep, tiles=tiles)
-    mask = np.zeros((cam.height, cam.width), dtype=bool)
-    for t in tiles:
-        ty, tx = divmod(t, oprep.tiles_x)
-        mask[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
-    col = np.where(mask[..., None], out.color, ref.color)
-    tf = np.where(mask, out.final_transmittance, ref.final_transmittance)
-    check_image(np.where(mask[..., None], col, 0), np.where(mask[..., None], ref.color, 0), oprep, scene, {}, "large color")
-    check_image(np.where(mask, tf, 0), np.where(mask, ref.final_transmittance, 0), oprep, scene, {}, "large T")
-    # backward restricted to the sampled tiles (d_color vanishes elsewhere),
-    # knife-edge pixels excluded on both sides
+    mask = _tile_mask(oprep, tiles, cam.height, cam.width)
+    check_image(np.where(mask[..., None], out.color, 0), np.where(mask[..., None], ref.color, 0),
+                oprep, scene, {}, "color")
+    check_image(np.where(mask, out.final_transmittance, 0), np.where(mask, ref.final_transmittance, 0),
+                oprep, scene, {}, "T")
     knife = knife_edge_mask(oprep, scene, {}, tiles=tiles)
     dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)) * (mask & ~knife)[..., None]
     g = vg().backward(scene, cam, dc, prep=prep)
     rg = O.backward(scene, cam, dc, prep=oprep, tiles=tiles)
     for f in GRAD_FIELDS:
-        check_field(getattr(g, f), getattr(rg, f), f"large {f}")
+        check_field(getattr(g, f), getattr(rg, f), f)
+
+
+def test_full_size_large_view_tiles_and_sampled_pixels():
+    """Config 3 (N=1M, 1920x1080), first view."""
+    from paper_2412_03378_b200 import configs
+    cfg = configs.large()
+    _full_size_check(_f64_scene(cfg.scene), cfg.cameras[0])
+
+
+def test_full_size_opaque_view():
+    """Config 4 (N=500k flattened disks, kappa 20-200, 1024x1024): early
+    termination on most pixels."""
+    from paper_2412_03378_b200 import configs
+    cfg = configs.opaque()
+    _full_size_check(_f64_scene(cfg.scene), cfg.cameras[3], seed=7)
+
+
+def test_full_size_tomography_parallel_view():
+    """Config 5 (N=200k, 512x512 parallel-beam detector): tile lists exact,
+    sampled tiles of the line-integral image and the masked adjoint against
+    the float64 oracle."""
+    from paper_2412_03378_b200 import configs
+    cfg = configs.tomography()
+    scene = _f64_scene(cfg.scene)
+    cam = cfg.cameras[17]
+    prep = vg().tomo_prepare(scene, cam, parallel=True, extent=cfg.extent)
+    oprep = O.tomo_prepare(scene, cam, parallel=True, extent=cfg.extent, key_dtype=np.float32)
+    prims, offs = prep.tile_lists_device()
+    assert np.array_equal(offs.cpu().numpy(), oprep.tile_start)
+    assert np.array_equal(np.sort(prims.cpu().numpy()), np.sort(oprep.pair_prim))
+    img = vg().tomo_forward(scene, cam, prep=prep)
+    rng = np.random.default_rng(3)
+    tiles = sorted(set(rng.integers(0, oprep.tiles_x * oprep.tiles_y, 6).tolist()) |
+                   set(np.argsort(np.diff(oprep.tile_start))[-2:].tolist()))
+    ref = O.tomo_forward(scene, cam, prep=oprep, tiles=tiles)
+    mask = _tile_mask(oprep, tiles, cam.height, cam.width)
+    check_field(np.where(mask, img, 0), np.where(mask, ref, 0), "tomo image")
+    w = rng.uniform(0.1, 1.0, (cam.height, cam.width)) * mask
+    g = vg().tomo_backward(scene, cam, w, prep=prep)
+    rg = O.tomo_backward(scene, cam, w, prep=oprep, tiles=tiles)
+    for f in ["d_means", "d_scales", "d_rotations", "d_thetas", "d_kappas"]:
+        check_field(getattr(g, f), getattr(rg, f), f"tomo {f}")
+
+
+def test_more_than_65536_tiles_uses_wide_keys():
+    """4400x4000 = 68750 tiles: 32-bit tile keys; lists and sampled pixels
+    still match."""
+    from paper_2412_03378_b200 import configs
+    from paper_2412_03378_b200.camera import look_at
+    cfg = configs.medium(n=4000, size=64, n_views=1)
+    cam = look_at([0.0, 1.0, -5.0], [0, 0, 0], width=4400, height=4000, fov_x_deg=60.0)
+    _full_size_check(_f64_scene(cfg.scene), cam, n_random=4, seed=11)
+
+
+def test_forward_is_deterministic():
+    scene, cam, d = load_case("mini_opaque")
+    a = vg().render(scene, cam)
+    b = vg().render(scene, cam)
+    assert np.array_equal(a.color, b.color)
+    assert np.array_equal(a.final_transmittance, b.final_transmittance)
+    assert np.array_equal(a.n_contrib, b.n_contrib)
+
+
+def test_degenerate_inputs():
+    """Scales below the 1e-7 floor (dead scale gradients), unnormalised
+    quaternions, a primitive straddling the near plane and one covering the
+    whole screen: lists, images and gradients still match the oracle."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(2)
+    n = 40
+    means = rng.uniform(-0.8, 0.8, (n, 3))
+    scales = rng.uniform(0.05, 0.3, (n, 3))
+    scales[0, 1] = 1e-9                      # floored, dead gradient (grad.py:257)
+    quats = rng.standard_normal((n, 4)) * 3.0  # unnormalised
+    means[1] = [0.0, 0.0, -2.995]            # 5 mm in front of the camera (z_near 0.01)
+    scales[2] = [2.5, 2.5, 2.5]              # covers every tile
+    means[2] = [0.0, 0.0, 0.5]
+    f32 = lambda a: a.astype(np.float32).astype(np.float64)
+    scene = SimpleNamespace(means=f32(means), scales=f32(scales), rotations=f32(quats),
+                            thetas=f32(rng.uniform(0.05, 0.6, n)), colors=f32(rng.uniform(0, 1, (n, 3))),
+                            background=np.array([0.1, 0.2, 0.3]))
+    cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=50, height=34, fov_x_deg=60.0)
+    prep = vg().prepare(scene, cam)
+    ref_lists = O.prepare(scene, cam, key_dtype=np.float32).lists()
+    for gl, rl in zip(prep.grid.tiles, ref_lists):
+        assert np.array_equal(gl, rl)
+    out = vg().render(scene, cam)
+    ref = O.render(scene, cam)
+    oprep = O.prepare(scene, cam)
+    check_image(out.color, ref.color, oprep, scene, {}, "degenerate color")
+    knife = knife_edge_mask(oprep, scene, {})
+    dc = rng.uniform(-1, 1, (34, 50, 3)) * ~knife[..., None]
+    g = vg().backward(scene, cam, dc)
+    rg = O.backward(scene, cam, dc)
+    for f in GRAD_FIELDS:
+        check_field(getattr(g, f), getattr(rg, f), f"degenerate {f}")
+    assert g.d_scales[0, 1] == 0.0
