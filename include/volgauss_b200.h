@@ -127,6 +127,15 @@ void vg_destroy(vg_context* ctx);
 int vg_prepare(vg_context* ctx, const vg_scene* scene, const vg_camera* cam,
                const vg_options* opt, void* stream);
 
+/* vg_prepare split in two for pipelining: _async enqueues projection, the
+ * depth sort and the pair-count scan and returns without waiting; _finish
+ * waits only for that count (an event, not the stream), then enqueues the
+ * pair duplication, tile sort and ranges.  Issuing view v+1's _async on one
+ * context before view v's blend on another hides the count read-back. */
+int vg_prepare_async(vg_context* ctx, const vg_scene* scene, const vg_camera* cam,
+                     const vg_options* opt, void* stream);
+int vg_prepare_finish(vg_context* ctx, void* stream);
+
 /* Update the blend flags (early_stop, alpha_cut, alpha_clamp) of a prepared
  * context without re-binning -- render(prep=...) may pass flags that differ
  * from prepare's (raster.py:410-418).  bin_cut and tile_size are ignored. */

@@ -53,6 +53,9 @@ EXPORTS = {
     "vg_destroy": (None, [C.c_void_p]),
     "vg_prepare": (C.c_int, [C.c_void_p, C.POINTER(VgScene), C.POINTER(VgCamera),
                              C.POINTER(VgOptions), C.c_void_p]),
+    "vg_prepare_async": (C.c_int, [C.c_void_p, C.POINTER(VgScene), C.POINTER(VgCamera),
+                                   C.POINTER(VgOptions), C.c_void_p]),
+    "vg_prepare_finish": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vg_set_options": (C.c_int, [C.c_void_p, C.POINTER(VgOptions)]),
     "vg_pair_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "vg_tile_lists": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

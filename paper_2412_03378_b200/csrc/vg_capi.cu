@@ -65,6 +65,8 @@ struct vg_context {
   uint32_t* vals = nullptr;
   bool prepared = false;
   bool have_fwd = false;
+  bool pending = false;          // vg_prepare_async issued, finish outstanding
+  cudaEvent_t count_ready = nullptr;
   // event profiling (vg_profile)
   bool prof = false;
   std::vector<cudaEvent_t> pool;
@@ -141,6 +143,11 @@ int vg_create(vg_context** out, int32_t device) {
     delete c;
     return fail(VG_ENOMEM, "vg_create: pinned alloc failed");
   }
+  if (cudaEventCreateWithFlags(&c->count_ready, cudaEventDisableTiming) != cudaSuccess) {
+    cudaFreeHost(c->total_host);
+    delete c;
+    return fail(VG_ECUDA, "vg_create: event creation failed");
+  }
   *out = c;
   return VG_OK;
 }
@@ -157,6 +164,7 @@ void vg_destroy(vg_context* c) {
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  if (c->count_ready) cudaEventDestroy(c->count_ready);
   delete c;
 }
 
@@ -209,8 +217,8 @@ static int make_cam(const vg_camera* cam, CamK& k) {
   return VG_OK;
 }
 
-int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_options* opt,
-               void* stream) {
+int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
+                     const vg_options* opt, void* stream) {
   if (!c || !s || !opt) return fail(VG_EINVAL, "vg_prepare: NULL argument");
   if (opt->tile_size != TILE) return fail(VG_EINVAL, "only tile_size=16 is supported");
   if (s->n < 0) return fail(VG_EINVAL, "negative primitive count");
@@ -287,7 +295,24 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
                  (uint64_t*)c->total.p, st);
     VG_LAUNCHED(c, 1);
     VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    VG_CUDA(cudaStreamSynchronize(st));
+    VG_CUDA(cudaEventRecord(c->count_ready, st));
+  }
+  c->pending = true;
+  return VG_OK;
+}
+
+int vg_prepare_finish(vg_context* c, void* stream) {
+  if (!c) return fail(VG_EINVAL, "vg_prepare_finish: NULL context");
+  if (!c->pending) return fail(VG_EINVAL, "vg_prepare_finish: no vg_prepare_async pending");
+  c->pending = false;
+  cudaStream_t st = (cudaStream_t)stream;
+  VG_CUDA(cudaSetDevice(c->device));
+  const int64_t n = c->scene.n;
+  const CamK& k = c->cam;
+  c->pairs = 0;
+  if (n > 0) {
+    // the only host synchronisation of the pipeline: the pair count sizes the sort
+    VG_CUDA(cudaEventSynchronize(c->count_ready));
     uint64_t P = *c->total_host;
     if (P > 0x7fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^31");
     c->pairs = (int64_t)P;
@@ -347,6 +372,12 @@ int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_
   }
   c->prepared = true;
   return VG_OK;
+}
+
+int vg_prepare(vg_context* c, const vg_scene* s, const vg_camera* cam, const vg_options* opt,
+               void* stream) {
+  VG_TRY(vg_prepare_async(c, s, cam, opt, stream));
+  return vg_prepare_finish(c, stream);
 }
 
 int vg_set_options(vg_context* c, const vg_options* opt) {

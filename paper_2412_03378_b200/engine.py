@@ -54,16 +54,24 @@ class Engine:
 
     # -- pipeline ----------------------------------------------------------
     def prepare(self, ds, cam, *, tomo=False, parallel=False, extent=1.6):
+        self.prepare_async(ds, cam, tomo=tomo, parallel=parallel, extent=extent)
+        self.prepare_finish()
+
+    def prepare_async(self, ds, cam, *, tomo=False, parallel=False, extent=1.6):
+        """First half of prepare (no host wait); see vg_prepare_async."""
         es, ac, cl = self.flags
         bin_cut = TOMO_BIN_CUT if tomo else ac
         opt = _lib.make_options(TILE_SIZE, es, ac, cl, bin_cut)
         c = _lib.make_camera(cam, _lib.VG_PARALLEL if parallel else _lib.VG_PINHOLE,
                              extent if parallel else 0.0)
         s = ds.struct()
-        _lib.check(self.lib.vg_prepare(self.ctx.handle, ctypes.byref(s), ctypes.byref(c),
-                                       ctypes.byref(opt), self.stream()), "vg_prepare")
+        _lib.check(self.lib.vg_prepare_async(self.ctx.handle, ctypes.byref(s), ctypes.byref(c),
+                                             ctypes.byref(opt), self.stream()), "vg_prepare_async")
         self.cam = cam
         self.dscene = ds
+
+    def prepare_finish(self):
+        _lib.check(self.lib.vg_prepare_finish(self.ctx.handle, self.stream()), "vg_prepare_finish")
 
     def forward(self, slot=0):
         H, W = int(self.cam.height), int(self.cam.width)

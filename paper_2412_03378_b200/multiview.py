@@ -52,12 +52,23 @@ def sharded_step(views, view_fn, flat, loss, group=None, finish=None):
 
 class ViewShardedStep:
     """One training step of the analytic rasterizer over a camera set, on
-    this rank's share of the views (engine.Engine on the local GPU)."""
+    this rank's share of the views.
+
+    Two device contexts (engine.Engine) alternate between views: view v+1's
+    binning front half (projection, depth sort, pair-count scan) is enqueued
+    before view v's blend kernels, so the one host wait of the pipeline (the
+    pair count that sizes the sort) never leaves the GPU idle.  Both contexts
+    defer the float64 parameter chain, which runs once per step per context
+    (vg_finalize_grads adds both into the same flat buffer)."""
 
     def __init__(self, engine, dscene, cameras, targets, *, world=1, rank=0, tomography=False,
-                 parallel=False, extent=1.6, group=None):
+                 parallel=False, extent=1.6, group=None, pipeline=True):
         import torch
+        from .engine import Engine
         self.eng = engine
+        self.engines = [engine]
+        if pipeline:
+            self.engines.append(Engine(engine.ctx.device, *engine.flags))
         self.ds = dscene
         self.cams = cameras
         self.targets = targets
@@ -67,30 +78,52 @@ class ViewShardedStep:
         self.extent = extent
         self.group = group
         self.grads = engine.new_grads(dscene)
-        self.ready = None
         self.loss = torch.zeros((), dtype=torch.float64, device=engine.device)
+        self.ready = None
 
-    def _view(self, v, accumulate):
-        # every view defers the float64 parameter chain to one finalize pass;
-        # the flat buffer is zeroed before the first view
+    def _begin(self, eng, v):
+        kw = dict(tomo=True, parallel=self.parallel, extent=self.extent) if self.tomo else {}
+        eng.prepare_async(self.ds, self.cams[v], **kw)
+
+    def _blend(self, eng, v):
         from ._lib import VG_DEFER
-        if not accumulate:
-            self.grads.zero_()
-        accumulate = VG_DEFER
         if self.ready is not None and v in self.ready:
             # the target of this view is still streaming in on a copy stream
-            self.eng.torch.cuda.current_stream(self.eng.device).wait_event(self.ready[v])
-        eng, cam = self.eng, self.cams[v]
+            eng.torch.cuda.current_stream(eng.device).wait_event(self.ready[v])
         if self.tomo:
-            eng.prepare(self.ds, cam, tomo=True, parallel=self.parallel, extent=self.extent)
             img = eng.tomo_forward()
-            eng.tomo_backward_l2(img, self.targets[v], self.grads, accumulate=accumulate,
+            eng.tomo_backward_l2(img, self.targets[v], self.grads, accumulate=VG_DEFER,
                                  loss=self.loss)
         else:
-            eng.prepare(self.ds, cam)
             color, tfin, _ = eng.forward()
-            eng.backward_l2(color, tfin, self.targets[v], self.grads, accumulate=accumulate,
+            eng.backward_l2(color, tfin, self.targets[v], self.grads, accumulate=VG_DEFER,
                             loss=self.loss)
+
+    def _run_views(self):
+        views = self.views
+        self.grads.zero_()
+        self._used = set()
+        if not views:
+            return
+        engs = self.engines
+        self._used = {0} | ({1} if len(views) > 1 and len(engs) > 1 else set())
+        self._begin(engs[0], views[0])
+        engs[0].prepare_finish()
+        for j, v in enumerate(views):
+            cur = engs[j % len(engs)]
+            nxt = engs[(j + 1) % len(engs)]
+            last = j + 1 >= len(views)
+            if not last and nxt is not cur:
+                self._begin(nxt, views[j + 1])       # enqueued before this view's blend
+            self._blend(cur, v)
+            if not last:
+                if nxt is cur:
+                    self._begin(nxt, views[j + 1])
+                nxt.prepare_finish()                 # its count is already on the host
+
+    def _finish(self):
+        for i in sorted(getattr(self, "_used", ())):
+            self.engines[i].finalize(self.grads, accumulate=True)
 
     def __call__(self, dscene=None, targets=None, ready=None):
         """Run the step.  `ready` optionally maps view -> CUDA event that the
@@ -100,5 +133,8 @@ class ViewShardedStep:
         if targets is not None:
             self.targets = targets
         self.ready = ready
-        return sharded_step(self.views, self._view, self.grads.flat, self.loss, self.group,
-                            finish=lambda: self.eng.finalize(self.grads, accumulate=True))
+        self.loss.zero_()
+        self._run_views()
+        self._finish()
+        reduce_across_ranks(self.grads.flat, self.loss, self.group)
+        return self.loss
