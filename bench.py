@@ -187,8 +187,9 @@ def run_gpu(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    eng.ctx.profile(True)
-    l0 = eng.launches()
+    for e in runner.engines:
+        e.ctx.profile(True)
+    l0 = sum(e.launches() for e in runner.engines)
     st = torch.cuda.current_stream(dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -198,9 +199,13 @@ def run_gpu(args):
     e1.record(st)
     torch.cuda.synchronize()
     ms_total = e0.elapsed_time(e1)
-    launches = eng.launches() - l0
-    prof = eng.ctx.profile_read()
-    eng.ctx.profile(False)
+    launches = sum(e.launches() for e in runner.engines) - l0
+    prof = {}
+    for e in runner.engines:
+        for k, (ms, cnt) in e.ctx.profile_read().items():
+            a, b = prof.get(k, (0.0, 0))
+            prof[k] = (a + ms, b + cnt)
+        e.ctx.profile(False)
     clk = clocks.stop()
     loss_val = float(loss) / (len(cams) * math.prod(tshape))
     if ws > 1:

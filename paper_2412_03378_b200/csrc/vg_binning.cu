@@ -59,6 +59,8 @@ __global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ perm,
   if (i < n) out[i] = count[perm[i]];
 }
 
+// One thread per Gaussian in depth order writes its pairs; rectangles of more
+// than 8 tiles are written by the whole warp (coalesced, load-balanced).
 template <typename KeyT>
 __global__ void __launch_bounds__(256) k_duplicate_sorted(int64_t n, const uint32_t* __restrict__ perm,
                                                           const uint32_t* __restrict__ offset,
@@ -66,19 +68,42 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(int64_t n, const uint3
                                                           const int4* __restrict__ rect, int ntx,
                                                           KeyT* __restrict__ keys,
                                                           uint32_t* __restrict__ vals) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t cnt = count_sorted[i];
-  if (!cnt) return;
-  uint32_t g = perm[i];
-  uint32_t o = offset[i];
-  int4 r = rect[g];
-  for (int y = r.y; y <= r.w; ++y)
-    for (int x = r.x; x <= r.z; ++x) {
-      keys[o] = (KeyT)(y * ntx + x);
-      vals[o] = g;
-      ++o;
+  const unsigned FULLM = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t cnt = i < n ? count_sorted[i] : 0u;
+  uint32_t g = 0, o = 0;
+  int4 r = make_int4(0, 0, -1, -1);
+  if (cnt) {
+    g = perm[i];
+    o = offset[i];
+    r = rect[g];
+  }
+  if (cnt && cnt <= 8) {
+    for (int y = r.y; y <= r.w; ++y)
+      for (int x = r.x; x <= r.z; ++x) {
+        keys[o] = (KeyT)(y * ntx + x);
+        vals[o] = g;
+        ++o;
+      }
+  }
+  unsigned big = __ballot_sync(FULLM, cnt > 8);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t bc = __shfl_sync(FULLM, cnt, src), bo = __shfl_sync(FULLM, o, src);
+    const uint32_t bg = __shfl_sync(FULLM, g, src);
+    const int x0 = __shfl_sync(FULLM, r.x, src), y0 = __shfl_sync(FULLM, r.y, src);
+    const int w = __shfl_sync(FULLM, r.z, src) - x0 + 1;
+    const float inv_w = 1.0f / (float)w;
+    for (uint32_t idx = lane; idx < bc; idx += 32) {
+      // floor((idx + 0.5) / w) is exact in float for idx < 2^21
+      const int dy = (int)((float)idx * inv_w + 0.5f * inv_w);
+      const int dx = (int)idx - dy * w;
+      keys[bo + idx] = (KeyT)((y0 + dy) * ntx + x0 + dx);
+      vals[bo + idx] = bg;
     }
+  }
 }
 
 template <typename KeyT>

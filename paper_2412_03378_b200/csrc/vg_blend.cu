@@ -641,6 +641,12 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
   }
 }
 
+// Tomography adjoint, Gaussian-parallel.  The line-integral sum has no
+// ordering (tomo.py:43-47), so instead of a warp per pixel block (which needs
+// a 13-value warp reduction for every pair) each thread owns one
+// (Gaussian, tile) pair and walks the tile's 256 pixels -- d_image staged once
+// per tile in shared memory and read as a broadcast -- accumulating its 10
+// gradient sums in registers; one 10-lane-op atomic flush per pair.
 template <int RAY, int LOSS>
 __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
                                                  const uint32_t* __restrict__ vals,
@@ -653,32 +659,29 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
                                                  float* __restrict__ acc,
                                                  uint8_t* __restrict__ visible) {
   __shared__ SRec sm[BATCH];
+  __shared__ float sde[TILE_PIX];
+  __shared__ float slp[TILE_PIX];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int lane = threadIdx.x & 31;
-  const LaneGeo G = lane_geo(p, tx, ty);
-  const float lx = (float)G.lxi;
-  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
-  const F2 Lp = RAY == VG_PINHOLE ? f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1))
-                                  : f2s(0.f);
   const uint2 r = ranges[tile];
-  float dev[2] = {0.f, 0.f};
   double lossv = 0.0;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const bool in = q ? G.in1 : G.in0;
-    if (!in) continue;
-    const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
-    if (LOSS == 0) {
-      dev[q] = d_image[pix];
-    } else {
-      const float rr = image[pix] - target[pix];
-      lossv += (double)rr * rr;
-      dev[q] = loss_scale * rr;
+  for (int q = threadIdx.x; q < TILE_PIX; q += NT) {
+    const int col = tx * TILE + (q & 15), row = ty * TILE + (q >> 4);
+    float de = 0.f;
+    if (col < p.width && row < p.height) {
+      const int pix = row * p.width + col;
+      if (LOSS == 0) {
+        de = d_image[pix];
+      } else {
+        const float rr = image[pix] - target[pix];
+        lossv += (double)rr * rr;
+        de = loss_scale * rr;
+      }
     }
+    sde[q] = de;
+    slp[q] = RAY == VG_PINHOLE ? pixel_lp(p, col, row) : 0.f;
   }
   if (LOSS) block_flush(0.f, 0.f, 0.f, lossv, nullptr, loss_sum);
-  const F2 de = f2(dev[0], dev[1]);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     __syncthreads();
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
@@ -687,35 +690,67 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
     }
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);
-    for (int k = 0; k < nb; ++k) {
+    for (int k = threadIdx.x; k < nb; k += NT) {
       const SRec s = sm[k];
-      const Pair2 e = RAY == VG_PINHOLE ? eval_pinhole2(s, lx, ly, Lp) : eval_parallel2(s, lx, ly);
-      const F2 h = mul2(de, e.G);
-      float v[16];
-      if (RAY == VG_PINHOLE) {
-        pinhole_grad_terms(e, s, h, v);
-      } else {
-        // rho = -(q1, q2, 0), w_hat = (0, 0, 1)
-        const F2 hq1 = mul2(h, f2s(e.q1)), hq2 = mul2(h, e.q2);
-        F2 t;
-        t = mul2(hq1, f2s(e.q1)); v[0] = lo(t) + hi(t);
-        t = mul2(hq1, e.q2); v[1] = lo(t) + hi(t);
-        v[2] = 0.f;
-        t = mul2(hq2, e.q2); v[3] = lo(t) + hi(t);
-        v[4] = 0.f;
-        v[5] = lo(h) + hi(h);
-        v[6] = -(lo(hq1) + hi(hq1));
-        v[7] = -(lo(hq2) + hi(hq2));
-        v[8] = 0.f;
-        v[9] = v[5];
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+      float b0 = 0.f, b1 = 0.f, b2 = 0.f, hs = 0.f, gmax = 0.f;
+      for (int ly = 0; ly < TILE; ++ly) {
+        const float fy = (float)ly;
+        const float t2 = fmaf(s.b.z, fy, s.a.y);
+        const float tw = fmaf(s.c.y, fy, s.a.z);
+#pragma unroll 4
+        for (int lx = 0; lx < TILE; ++lx) {
+          const float fx = (float)lx;
+          const float d = sde[ly * TILE + lx];
+          const float q1 = fmaf(s.b.x, fx, s.a.x);
+          const float q2 = fmaf(s.b.y, fx, t2);
+          const float X = fmaf(q1, q1, q2 * q2);
+          if (RAY == VG_PINHOLE) {
+            const float wp = fmaf(s.c.x, fx, tw);
+            const float rs = rsqf(fmaf(wp, wp, X));
+            const float ri = rs * rs;
+            const float G = rs * ex2f(fmaf(-s.a.w, X * ri, slp[ly * TILE + lx]));
+            gmax = fmaxf(gmax, G);
+            const float h = d * G;
+            // factored h (rho rho^T + w^ w^T), h rho (see pinhole_grad_terms)
+            const float sD = s.c.z * ri, s2 = sD * sD, wp2 = wp * wp;
+            const float k1 = h * fmaf(s2, wp2, ri);
+            const float k2 = h * wp * fmaf(-s2, X, ri);
+            const float k1q1 = k1 * q1;
+            a0 = fmaf(k1q1, q1, a0);
+            a1 = fmaf(k1q1, q2, a1);
+            a2 = fmaf(k2, q1, a2);
+            a3 = fmaf(k1 * q2, q2, a3);
+            a4 = fmaf(k2, q2, a4);
+            a5 = fmaf(h, fmaf(s2, X * X, ri * wp2), a5);
+            const float hsD = h * sD, hsw = hsD * wp;
+            b0 = fmaf(-hsw, q1, b0);
+            b1 = fmaf(-hsw, q2, b1);
+            b2 = fmaf(hsD, X, b2);
+            hs += h;
+          } else {
+            const float G = s.c.z * ex2f(-C_HALF_LOG2E * X);
+            gmax = fmaxf(gmax, G);
+            const float h = d * G;
+            // rho = -(q1, q2, 0), w^ = (0, 0, 1)
+            const float hq1 = h * q1, hq2 = h * q2;
+            a0 = fmaf(hq1, q1, a0);
+            a1 = fmaf(hq1, q2, a1);
+            a3 = fmaf(hq2, q2, a3);
+            b0 -= hq1;
+            b1 -= hq2;
+            hs += h;
+          }
+        }
       }
-      v[10] = v[11] = v[12] = v[13] = v[14] = v[15] = 0.f;
-      const bool vis = (G.in0 && lo(e.E2) > 0.f) || (G.in1 && hi(e.E2) > 0.f);
-      if (__any_sync(FULL, vis)) {
-        const uint32_t gid = __float_as_uint(s.c.w);
-        if (lane == 0) visible[gid] = 1;
-        flush_acc(v, lane, gid, acc);
-      }
+      if (RAY != VG_PINHOLE) a5 = hs;
+      const uint32_t gid = __float_as_uint(s.c.w);
+      float* o = acc + (size_t)gid * ACC_STRIDE;
+      const float vv[10] = {a0, a1, a2, a3, a4, a5, b0, b1, b2, hs};
+#pragma unroll
+      for (int q = 0; q < 10; ++q)
+        if (vv[q] != 0.f) atomicAdd(o + q, vv[q]);
+      if (gmax > 0.f && s.b.w > 0.f) visible[gid] = 1;
     }
   }
 }
