@@ -1,44 +1,14 @@
 // K2 duplicate + K4 tile ranges (raster._build_grid, raster.py:222-260).
 //
-// The (tile, depth) pairs are emitted in Gaussian-index order, each
-// Gaussian's tiles in row-major order of its rectangle, as 64-bit keys
-// (tile << 32 | float bits of depth) with the Gaussian id as value.  A
-// stable LSD radix sort over the low 32 + ceil(log2 n_tiles) bits then
-// yields the reference's lexsort((prim, depth, tile)) order with float32
-// depth keys (view depth is > z_near > 0, so IEEE bits sort as unsigned).
+// The Gaussians are first sorted by float32 view depth (IEEE bits of a
+// positive float sort as unsigned; the sort is stable over the identity
+// permutation, so equal depths keep index order).  Pairs are then emitted in
+// that order, each Gaussian's tiles row-major over its rectangle, with the
+// tile id as key; a stable sort by tile alone yields the reference's
+// lexsort((prim, depth, tile)) order with float32 depth keys.
 #include "vg_kernels.cuh"
 
 namespace vg {
-
-__global__ void __launch_bounds__(256) k_duplicate(int64_t n, const uint32_t* __restrict__ count,
-                                                   const uint32_t* __restrict__ offset,
-                                                   const int4* __restrict__ rect,
-                                                   const float* __restrict__ depth, int ntx,
-                                                   uint64_t* __restrict__ keys,
-                                                   uint32_t* __restrict__ vals) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  uint32_t cnt = count[i];
-  if (!cnt) return;
-  uint32_t o = offset[i];
-  int4 r = rect[i];
-  uint64_t lo = (uint64_t)__float_as_uint(depth[i]);
-  for (int y = r.y; y <= r.w; ++y)
-    for (int x = r.x; x <= r.z; ++x) {
-      keys[o] = ((uint64_t)(y * ntx + x) << 32) | lo;
-      vals[o] = (uint32_t)i;
-      ++o;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_ranges(int64_t P, const uint64_t* __restrict__ keys,
-                                                uint2* __restrict__ ranges) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  uint32_t t = (uint32_t)(keys[i] >> 32);
-  if (i == 0 || (uint32_t)(keys[i - 1] >> 32) != t) ranges[t].x = (uint32_t)i;
-  if (i == P - 1 || (uint32_t)(keys[i + 1] >> 32) != t) ranges[t].y = (uint32_t)(i + 1);
-}
 
 __global__ void k_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total) {
   total[0] = n > 0 ? (uint64_t)offset[n - 1] + count[n - 1] : 0;
@@ -140,19 +110,6 @@ void launch_tile_ranges(int64_t P, const void* keys, bool wide, uint2* ranges, c
   const unsigned g = (unsigned)((P + 255) / 256);
   if (wide) k_tile_ranges<uint32_t><<<g, 256, 0, st>>>(P, (const uint32_t*)keys, ranges);
   else k_tile_ranges<uint16_t><<<g, 256, 0, st>>>(P, (const uint16_t*)keys, ranges);
-}
-
-void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,
-                      const float* depth, int ntx, uint64_t* keys, uint32_t* vals,
-                      cudaStream_t st) {
-  if (n <= 0) return;
-  k_duplicate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, count, offset, rect, depth, ntx,
-                                                            keys, vals);
-}
-
-void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t st) {
-  if (P <= 0) return;
-  k_ranges<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges);
 }
 
 void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,

@@ -33,9 +33,8 @@ struct BwdIO {
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
                        float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st);
-void launch_duplicate(int64_t n, const uint32_t* count, const uint32_t* offset, const int4* rect,
-                      const float* depth, int ntx, uint64_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, cudaStream_t st);
+void launch_records(int64_t n, const vg_scene& s, const CamK& c, const uint32_t* count, GRec* rec,
+                    float* frame, cudaStream_t st);
 void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
                   cudaStream_t st);
 // vmask (optional): per-warp bit rows of vm_words words marking the list
@@ -68,9 +67,6 @@ int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cac
 cudaError_t scan_temp_bytes(int64_t n, size_t* bytes);
 cudaError_t exclusive_scan(void* tmp, size_t tmp_bytes, const uint32_t* in, uint32_t* out,
                            int64_t n, cudaStream_t st);
-cudaError_t sort_temp_bytes(int64_t n, int end_bit, size_t* bytes);
-cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t* k1, uint32_t* v0,
-                             uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st);
 int sort_launches(int end_bit);
 cudaError_t depth_sort_temp_bytes(int64_t n, size_t* bytes);
 cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out,

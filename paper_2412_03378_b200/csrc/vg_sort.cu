@@ -1,6 +1,8 @@
-// K3 radix sort + the count scan.  Round-1 implementation uses CUB's device
-// radix sort / scan (library, like cuBLAS for a GEMM); see DESIGN.md for the
-// hand-written onesweep replacement planned for the next round.
+// K3 radix sorts + the count scan.  Round 1 uses CUB's onesweep device radix
+// sort / scan (library, like cuBLAS for a GEMM): the 32-bit depth sort of the
+// Gaussians, the 16/32-bit stable tile sort of the pairs, and the tiny
+// heavy-tiles-first order sort.  See DESIGN.md for the planned hand-written
+// replacement.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -16,21 +18,6 @@ cudaError_t scan_temp_bytes(int64_t n, size_t* bytes) {
 cudaError_t exclusive_scan(void* tmp, size_t tmp_bytes, const uint32_t* in, uint32_t* out,
                            int64_t n, cudaStream_t st) {
   return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, (int)n, st);
-}
-
-cudaError_t sort_temp_bytes(int64_t n, int end_bit, size_t* bytes) {
-  cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
-  return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, k, v, (int)n, 0, end_bit);
-}
-
-cudaError_t radix_sort_pairs(void* tmp, size_t tmp_bytes, uint64_t* k0, uint64_t* k1, uint32_t* v0,
-                             uint32_t* v1, int64_t n, int end_bit, int* which, cudaStream_t st) {
-  cub::DoubleBuffer<uint64_t> k(k0, k1);
-  cub::DoubleBuffer<uint32_t> v(v0, v1);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k, v, (int)n, 0, end_bit, st);
-  *which = k.selector;
-  return e;
 }
 
 int sort_launches(int end_bit) { return 1 + (end_bit + 7) / 8; }
