@@ -99,8 +99,14 @@ __device__ __forceinline__ float d0(float lo_, float hi_) {
 
 // Stage one record for the tile at pixel origin (x0, y0); return the 4-bit
 // mask of 8x8 warp blocks the Gaussian may reach with alpha >= cut.
+// Bound per block: e = K beta exp(-expo/2) with K = kappa sqrt(2pi),
+//   beta = |d'| / |w| <= min(s_max, dmax / sqrt(w_par_min^2 + X_min)),
+//   expo = D^2 X / (w_par^2 + X) >= D^2 X_min / (w_par_max^2 + X_min),
+// X_min / w_par ranges from interval arithmetic over the block (q1, q2, w_par
+// are affine in the pixel offset), dmax = max |d'| over the block's corners.
 __device__ __forceinline__ uint32_t stage(SRec* sm, int slot, const GRec* __restrict__ rec,
-                                          uint32_t gid, int x0, int y0, bool cull, float ecut) {
+                                          uint32_t gid, int x0, int y0, bool cull, float ecut,
+                                          const float* __restrict__ dmax4 = nullptr) {
   const GRec g = rec[gid];
   float bu = (float)((double)x0 + 0.5 - g.u);
   float bv = (float)((double)y0 + 0.5 - g.v);
@@ -115,10 +121,9 @@ __device__ __forceinline__ uint32_t stage(SRec* sm, int slot, const GRec* __rest
   sm[slot] = s;
   if (!cull) return 0xFu;
   if (!(g.amp > ecut)) return 0u;  // alpha < cut at every pixel
-  float R2 = 2.f * __logf(g.amp / ecut);
-  float D2 = g.D * g.D;
-  if (D2 <= R2 * 1.001f) return 0xFu;
-  float k2 = R2 / (D2 - R2) * 1.001f + 1e-30f;
+  const float K = g.kap2 * 0.69314718f;  // kappa sqrt(2 pi)
+  const float D2 = g.D * g.D;
+  const float inv_ecut = 1.f / ecut;
   uint32_t m = 0;
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -133,11 +138,34 @@ __device__ __forceinline__ uint32_t stage(SRec* sm, int slot, const GRec* __rest
     float whi = c3 + fmaxf(nxa, nxb) + fmaxf(nya, nyb);
     float t1 = d0(fminf(q1a, q1b), fmaxf(q1a, q1b));
     float t2 = d0(q2lo, q2hi);
-    float Xmin = (t1 * t1 + t2 * t2) * 0.999f;
-    float wmax2 = fmaxf(wlo * wlo, whi * whi);
-    if (Xmin <= k2 * wmax2) m |= 1u << b;
+    const float Xmin = (t1 * t1 + t2 * t2) * 0.999f;
+    const float wmax2 = fmaxf(wlo * wlo, whi * whi) * 1.001f;
+    const float wd = d0(wlo, whi);
+    const float wmin2 = wd * wd * 0.999f;
+    float A = g.amp;
+    if (dmax4) A = fminf(A, K * dmax4[b] * rsqf(fmaxf(wmin2 + Xmin, 1e-30f)));
+    A *= 1.001f;
+    if (!(A > ecut)) continue;
+    const float L = __logf(A * inv_ecut);
+    if (D2 * Xmin <= 2.f * L * (wmax2 + Xmin)) m |= 1u << b;
   }
   return m;
+}
+
+// max |d'| = max sqrt(1 + X^2 + Y^2) over the corners of each 8x8 block of a tile
+__device__ __forceinline__ void block_dmax(const BlendParams& p, int tx, int ty, float* out4) {
+  if (threadIdx.x < 4) {
+    const int b = threadIdx.x;
+    float best = 0.f;
+    for (int cy = 0; cy < 2; ++cy)
+      for (int cx = 0; cx < 2; ++cx) {
+        const float col = (float)(tx * TILE + 8 * (b & 1) + 7 * cx) + 0.5f;
+        const float row = (float)(ty * TILE + 8 * (b >> 1) + 7 * cy) + 0.5f;
+        const float X = (col - p.cx) / p.fx, Y = (row - p.cy) / p.fy;
+        best = fmaxf(best, fmaf(X, X, fmaf(Y, Y, 1.f)));
+      }
+    out4[b] = sqrtf(best) * 1.0001f;
+  }
 }
 
 struct Pair2 {
@@ -316,6 +344,7 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
   unsigned long long st_proc = 0, st_vis = 0, st_tot = 0;
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
+  __shared__ float sdmax[4];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -324,6 +353,7 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
   const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
   const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
+  block_dmax(p, tx, ty, sdmax);
   // Pixels outside the image start (and stay) at T = 0: never active.
   F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f);
   F2 Cr = f2s(0.f), Cg = f2s(0.f), Cb = f2s(0.f);
@@ -335,7 +365,8 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
     if (__syncthreads_count(done) == NT) break;
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
-      if (i < r.y) smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut);
+      if (i < r.y)
+        smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut, sdmax);
     }
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);

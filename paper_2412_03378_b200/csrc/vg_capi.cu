@@ -266,7 +266,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
                         (int4*)c->rect.p, (uint32_t*)c->count.p, (float*)c->frame.p, st);
     }
-    VG_LAUNCHED(c, 2);
+    VG_LAUNCHED(c, 1);
     // Gaussians in (float32 depth, index) order
     uint32_t* ids_in = (uint32_t*)c->perm.p + n;
     uint32_t* perm = (uint32_t*)c->perm.p;

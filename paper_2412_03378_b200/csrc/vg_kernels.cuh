@@ -33,8 +33,6 @@ struct BwdIO {
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
                        float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st);
-void launch_records(int64_t n, const vg_scene& s, const CamK& c, const uint32_t* count, GRec* rec,
-                    float* frame, cudaStream_t st);
 void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
                   cudaStream_t st);
 // vmask (optional): per-warp bit rows of vm_words words marking the list

@@ -4,10 +4,9 @@
 // core.py:81-153): view transform, validity z > z_near, EWA screen
 // covariance with 0.3 px^2 dilation, lambda_max, the amplitude-aware bin
 // radius, the tile rectangle and its tile count, kappa, and the 64-byte blend
-// record the tile kernels gather.  This translation unit holds only the
-// binning half and is compiled with -fmad=false so its arithmetic rounds like
-// the reference's numpy float64 (tile lists must match bit for bit); the blend
-// records are built by vg_records.cu (FMA allowed) for binned Gaussians only.
+// record the tile kernels gather.  Compiled with -fmad=false so the binning
+// arithmetic rounds like the reference's numpy float64 (tile lists must match
+// bit for bit).
 #include "vg_kernels.cuh"
 
 namespace vg {
@@ -30,22 +29,7 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Frame f;
-  // binning needs only R, s and the view-space mean (raster.py:175-209)
-  quat_rotmat(rots + 4 * i, f.R, nullptr);
-  for (int k = 0; k < 3; ++k) f.s[k] = fmax((double)scales[3 * i + k], SCALE_FLOOR);
-  {
-    const double m3[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
-    for (int j = 0; j < 3; ++j)
-      f.v[j] = c.R[j * 3 + 0] * m3[0] + c.R[j * 3 + 1] * m3[1] + c.R[j * 3 + 2] * m3[2] + c.t[j];
-  }
-  bool ok = c.projection != VG_PINHOLE || f.v[2] > c.z_near;
-  if (c.projection == VG_PINHOLE) {
-    f.pu = c.fx * f.v[0] / f.v[2] + c.cx;
-    f.pv = c.fy * f.v[1] / f.v[2] + c.cy;
-  } else {
-    f.pu = (f.v[0] / c.extent + 1.0) * 0.5 * c.width;
-    f.pv = (f.v[1] / c.extent + 1.0) * 0.5 * c.height;
-  }
+  bool ok = make_frame(c, means + 3 * i, scales + 3 * i, rots + 4 * i, f);
   uint32_t cnt = 0;
   int4 rect = make_int4(0, 0, -1, -1);
   double kappa = kappa_of((double)thetas[i], f.s, nullptr, nullptr);
@@ -108,6 +92,52 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   o.count[i] = cnt;
   o.rect[i] = rect;
   o.depth[i] = (float)f.v[2];
+  if (!cnt) return;
+  // --- blend record
+  GRec g;
+  g.u = f.pu;
+  g.v = f.pv;
+  g.P11 = (float)f.P11;
+  g.P21 = (float)f.P21;
+  g.P22 = (float)f.P22;
+  g.n1 = (float)f.n1;
+  g.n2 = (float)f.n2;
+  g.wm = (float)f.wm;
+  g.cD2 = (float)(0.5 * LOG2E * f.D * f.D);
+  g.D = (float)(c.projection == VG_PINHOLE ? f.D : f.beta);
+  g.kap2 = (float)(kappa * SQRT_2PI * LOG2E);
+  g.amp = (float)(SQRT_2PI * kappa * fmax(fmax(f.s[0], f.s[1]), f.s[2]));
+  g.pad0 = g.pad1 = g.pad2 = 0.f;
+  double rgb[3] = {0.0, 0.0, 0.0};
+  if (sh) {
+    double d[3] = {means[3 * i] - c.center[0], means[3 * i + 1] - c.center[1],
+                   means[3 * i + 2] - c.center[2]};
+    double dn = sqrt(dot3(d, d));
+    d[0] /= dn; d[1] /= dn; d[2] /= dn;
+    double b[16];
+    sh_basis(d, b);
+    // 192 contiguous bytes per Gaussian: 12 x 16-byte loads (not 48 scalar ones)
+    const float4* q4 = reinterpret_cast<const float4*>(sh + 48 * i);
+    float q[48];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      const float4 v = __ldg(q4 + k);
+      q[4 * k] = v.x; q[4 * k + 1] = v.y; q[4 * k + 2] = v.z; q[4 * k + 3] = v.w;
+    }
+#pragma unroll
+    for (int l = 0; l < 16; ++l)
+      for (int ch = 0; ch < 3; ++ch) rgb[ch] += b[l] * q[l * 3 + ch];
+  } else if (colors) {
+    rgb[0] = colors[3 * i]; rgb[1] = colors[3 * i + 1]; rgb[2] = colors[3 * i + 2];
+  }
+  float4* fr = reinterpret_cast<float4*>(o.frame + 12 * i);
+  fr[0] = make_float4((float)f.e[0], (float)f.e[1], (float)f.e[2], (float)f.e[3]);
+  fr[1] = make_float4((float)f.e[4], (float)f.e[5], (float)f.e[6], (float)f.e[7]);
+  fr[2] = make_float4((float)f.e[8], 0.f, 0.f, 0.f);
+  g.cr = (float)rgb[0];
+  g.cg = (float)rgb[1];
+  g.cb = (float)rgb[2];
+  o.rec[i] = g;
 }
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
@@ -117,7 +147,6 @@ void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_c
   int blocks = (int)((n + 255) / 256);
   k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
                                        s.sh, c, bin_cut, o);
-  launch_records(n, s, c, count, rec, frame, st);
 }
 
 }  // namespace vg
