@@ -40,8 +40,13 @@ struct ViewAccIn {
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= in.n) return;
+  // all loads issued up front (one memory round trip instead of three)
   float4* a4 = reinterpret_cast<float4*>(in.acc + 16 * i);
+  const float4* f4 = reinterpret_cast<const float4*>(in.frame + 12 * i);
+  float4* l4 = reinterpret_cast<float4*>(in.lacc + 12 * i);
   const float4 x0 = a4[0], x1 = a4[1], x2 = a4[2], x3 = a4[3];
+  const float4 f0 = __ldg(f4), f1 = __ldg(f4 + 1), f2 = __ldg(f4 + 2);
+  float4 l0 = l4[0], l1 = l4[1], l2 = l4[2];
   const float raw[13] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x};
   bool any = false;
 #pragma unroll
@@ -50,8 +55,6 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   a4[0] = z; a4[1] = z; a4[2] = z; a4[3] = z;
   // rotate into the whitened-local frame: A_loc = sum_ab A_e[a][b] e_a e_b^T
-  const float4* f4 = reinterpret_cast<const float4*>(in.frame + 12 * i);
-  const float4 f0 = f4[0], f1 = f4[1], f2 = f4[2];
   const float e[3][3] = {{f0.x, f0.y, f0.z}, {f0.w, f1.x, f1.y}, {f1.z, f1.w, f2.x}};
   const float Ae[3][3] = {{raw[0], raw[1], raw[2]}, {raw[1], raw[3], raw[4]}, {raw[2], raw[4], raw[5]}};
   float T1[3][3];
@@ -68,8 +71,6 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   float Bl[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) Bl[j] = fmaf(e[0][j], raw[6], fmaf(e[1][j], raw[7], e[2][j] * raw[8]));
-  float4* l4 = reinterpret_cast<float4*>(in.lacc + 12 * i);
-  float4 l0 = l4[0], l1 = l4[1], l2 = l4[2];
   l0.x += Al[0]; l0.y += Al[1]; l0.z += Al[2]; l0.w += Al[3];
   l1.x += Al[4]; l1.y += Al[5]; l1.z += Bl[0]; l1.w += Bl[1];
   l2.x += Bl[2]; l2.y += raw[9];
