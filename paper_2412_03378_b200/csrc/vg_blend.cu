@@ -487,35 +487,68 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
   v[9] = hsum(h);
 }
 
-// ---------------------------------------------------------------------------
-// K6 backward blend (grad.backward tile_job + e_chain)
+// One entry of the backward replay for the lane's two pixels (shared by the
+// staged and the warp-independent kernels): recompute alpha exactly as the
+// forward did, advance T and the running suffix, form dL/de for live pixels,
+// and flush the warp's 13 accumulator sums for this Gaussian.
+template <bool CUT>
+__device__ __forceinline__ void bwd_entry(const SRec& s, int j, float lx, F2 ly, F2 Lp,
+                                          const int (&nav)[2], F2 dcr, F2 dcg, F2 dcb, F2 tot,
+                                          const BlendParams& p, F2& T, F2& P, int lane,
+                                          const BwdIO& io) {
+  const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+  // inactive entries (j >= n_act) get a floor of 1: alpha = 0, no change
+  const bool act0 = j < nav[0], act1 = j < nav[1];
+  float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
+  float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
+  // cut: skipped below alpha_cut (raster.py:363-365) or inactive
+  const bool cut0 = CUT ? om0 > p.omcut : !act0;
+  const bool cut1 = CUT ? om1 > p.omcut : !act1;
+  om0 = cut0 ? 1.f : om0;
+  om1 = cut1 ? 1.f : om1;
+  const F2 om = f2(om0, om1);
+  const F2 contrib = mul2(sub2(f2s(1.f), om), T);
+  const F2 Tn = mul2(T, om);
+  const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
+  P = fma2(dot, contrib, P);
+  T = Tn;
+  // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
+  const bool live0 = !cut0 && lo(e.ex) > p.cc;
+  const bool live1 = !cut1 && hi(e.ex) > p.cc;
+  const bool vis = om0 < 1.f || om1 < 1.f;
+  const bool any_live = __any_sync(FULL, live0 || live1);
+  const bool any_vis = __any_sync(FULL, vis);
+  if (!(any_live || any_vis)) return;
+  float v[16];
+  if (any_live) {
+    const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
+    pinhole_grad_terms(e, s, mul2(de, e.G), v);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 10; ++q) v[q] = 0.f;
+  }
+  v[10] = hsum(mul2(contrib, dcr));
+  v[11] = hsum(mul2(contrib, dcg));
+  v[12] = hsum(mul2(contrib, dcb));
+  v[13] = v[14] = v[15] = 0.f;
+  const uint32_t gid = __float_as_uint(s.c.w);
+  if (lane == 0 && any_vis) io.visible[gid] = 1;
+  flush_acc(v, lane, gid, io.acc);
+}
 
-template <bool CUT, int LOSS>
-__global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
-                                                   const uint32_t* __restrict__ vals,
-                                                   const uint2* __restrict__ ranges,
-                                                   const uint32_t* __restrict__ order,
-                                                   BlendParams p, BwdIO io,
-                                                   const uint32_t* __restrict__ vmask,
-                                                   int vm_words) {
-  __shared__ SRec sm[BATCH];
-  __shared__ uint8_t smask[BATCH];
-  __shared__ int s_maxna;
-  const int tile = order[blockIdx.x];
-  const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const LaneGeo G = lane_geo(p, tx, ty);
-  const float lx = (float)G.lxi;
-  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
-  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
-  const uint2 r = ranges[tile];
-  float dcv[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-  float totv[2] = {0.f, 0.f}, Tfv[2] = {1.f, 1.f};
-  int nav[2] = {0, 0};
+// Per-pixel prologue of the backward: upstream gradient (explicit or fused
+// L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
+template <int LOSS>
+__device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo& G, const BwdIO& io,
+                                             float (&dcv)[2][3], float (&totv)[2], int (&nav)[2],
+                                             int* s_maxna) {
+  float Tfv[2] = {1.f, 1.f};
   double lossv = 0.0;
-  if (threadIdx.x == 0) s_maxna = 0;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
+    dcv[q][0] = dcv[q][1] = dcv[q][2] = 0.f;
+    totv[q] = 0.f;
+    nav[q] = 0;
     const bool in = q ? G.in1 : G.in0;
     if (!in) continue;
     const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
@@ -540,13 +573,120 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
   }
   __syncthreads();
   const int my_na = max(nav[0], nav[1]);
-  if (my_na) atomicMax(&s_maxna, my_na);
-  int warp_na = my_na;
-  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
+  if (my_na && s_maxna) atomicMax(s_maxna, my_na);
   block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
               dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
               LOSS ? io.loss_sum : nullptr);
   __syncthreads();
+}
+
+__device__ __forceinline__ SRec derive_srec(const GRec& g, uint32_t gid, int x0, int y0) {
+  const float bu = (float)((double)x0 + 0.5 - g.u);
+  const float bv = (float)((double)y0 + 0.5 - g.v);
+  SRec s;
+  s.a = make_float4(g.P11 * bu, fmaf(g.P22, bv, g.P21 * bu), fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm)),
+                    g.cD2);
+  s.b = make_float4(g.P11, g.P21, g.P22, g.kap2);
+  s.c = make_float4(g.n1, g.n2, g.D, __uint_as_float(gid));
+  s.d = make_float4(g.cr, g.cg, g.cb, 0.f);
+  return s;
+}
+
+__device__ __forceinline__ GRec load_rec(const GRec* __restrict__ rec, uint32_t gid) {
+  return rec[gid];
+}
+
+// K6, warp-independent (alpha_cut > 0): the forward's bitmask names exactly
+// the (entry, warp block) pairs with a visible pixel, so each warp fetches only
+// those records itself -- the chunk's Gaussian ids with one coalesced load,
+// each record with broadcast loads prefetched one entry ahead -- with no
+// shared-memory staging and no CTA-wide barrier in the replay loop.
+template <int LOSS>
+__global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ rec,
+                                                      const uint32_t* __restrict__ vals,
+                                                      const uint2* __restrict__ ranges,
+                                                      const uint32_t* __restrict__ order,
+                                                      BlendParams p, BwdIO io,
+                                                      const uint32_t* __restrict__ vmask,
+                                                      int vm_words) {
+  const int tile = order[blockIdx.x];
+  const int tx = tile % p.ntx, ty = tile / p.ntx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
+  const uint2 r = ranges[tile];
+  float dcv[2][3], totv[2];
+  int nav[2];
+  bwd_prologue<LOSS>(p, G, io, dcv, totv, nav, nullptr);
+  int warp_na = max(nav[0], nav[1]);
+  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
+  const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
+           dcb = f2(dcv[0][2], dcv[1][2]);
+  const F2 tot = f2(totv[0], totv[1]);
+  F2 T = f2s(1.f), P = f2s(0.f);
+  const uint32_t* row = vmask + (size_t)warp * vm_words;
+  const int x0 = tx * TILE, y0 = ty * TILE;
+  for (int c = 0; c < warp_na; c += 32) {
+    const uint32_t g0 = r.x + c;
+    const uint32_t sh = g0 & 31u;
+    unsigned bits = __ldg(row + (g0 >> 5)) >> sh;
+    if (sh) bits |= __ldg(row + (g0 >> 5) + 1) << (32u - sh);
+    const int nb = warp_na - c;
+    if (nb < 32) bits &= (1u << nb) - 1u;
+    if (!bits) continue;
+    const uint32_t my_gid = (c + lane < warp_na) ? __ldg(vals + g0 + lane) : 0u;
+    int k = __ffs(bits) - 1;
+    bits &= bits - 1;
+    uint32_t gid = __shfl_sync(FULL, my_gid, k);
+    GRec cur = load_rec(rec, gid);
+    while (true) {
+      const int kn = bits ? __ffs(bits) - 1 : -1;
+      uint32_t gidn = __shfl_sync(FULL, my_gid, kn < 0 ? 0 : kn);
+      GRec nxt;
+      if (kn >= 0) {
+        bits &= bits - 1;
+        nxt = load_rec(rec, gidn);
+      }
+      const SRec s = derive_srec(cur, gid, x0, y0);
+      bwd_entry<true>(s, c + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+      if (kn < 0) break;
+      cur = nxt;
+      k = kn;
+      gid = gidn;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 backward blend (grad.backward tile_job + e_chain)
+
+template <bool CUT, int LOSS>
+__global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const uint2* __restrict__ ranges,
+                                                   const uint32_t* __restrict__ order,
+                                                   BlendParams p, BwdIO io,
+                                                   const uint32_t* __restrict__ vmask,
+                                                   int vm_words) {
+  __shared__ SRec sm[BATCH];
+  __shared__ uint8_t smask[BATCH];
+  __shared__ int s_maxna;
+  const int tile = order[blockIdx.x];
+  const int tx = tile % p.ntx, ty = tile / p.ntx;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const LaneGeo G = lane_geo(p, tx, ty);
+  const float lx = (float)G.lxi;
+  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
+  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
+  const uint2 r = ranges[tile];
+  float dcv[2][3], totv[2];
+  int nav[2];
+  if (threadIdx.x == 0) s_maxna = 0;
+  bwd_prologue<LOSS>(p, G, io, dcv, totv, nav, &s_maxna);
+  int warp_na = max(nav[0], nav[1]);
+  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
   const uint32_t end = r.x + (uint32_t)s_maxna;
   const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
            dcb = f2(dcv[0][2], dcv[1][2]);
@@ -581,46 +721,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
-        const int j = jb + k;
-        const SRec s = sm[k];
-        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
-        // inactive entries (j >= n_act) get a floor of 1: alpha = 0, no change
-        const bool act0 = j < nav[0], act1 = j < nav[1];
-        float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
-        float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-        // cut: skipped below alpha_cut (raster.py:363-365) or inactive
-        const bool cut0 = CUT ? om0 > p.omcut : !act0;
-        const bool cut1 = CUT ? om1 > p.omcut : !act1;
-        om0 = cut0 ? 1.f : om0;
-        om1 = cut1 ? 1.f : om1;
-        const F2 om = f2(om0, om1);
-        const F2 contrib = mul2(sub2(f2s(1.f), om), T);
-        const F2 Tn = mul2(T, om);
-        const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
-        P = fma2(dot, contrib, P);
-        T = Tn;
-        // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
-        const bool live0 = !cut0 && lo(e.ex) > p.cc;
-        const bool live1 = !cut1 && hi(e.ex) > p.cc;
-        const bool vis = om0 < 1.f || om1 < 1.f;
-        const bool any_live = __any_sync(FULL, live0 || live1);
-        const bool any_vis = __any_sync(FULL, vis);
-        if (!(any_live || any_vis)) continue;
-        float v[16];
-        if (any_live) {
-          const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
-          pinhole_grad_terms(e, s, mul2(de, e.G), v);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 10; ++q) v[q] = 0.f;
-        }
-        v[10] = hsum(mul2(contrib, dcr));
-        v[11] = hsum(mul2(contrib, dcg));
-        v[12] = hsum(mul2(contrib, dcb));
-        v[13] = v[14] = v[15] = 0.f;
-        const uint32_t gid = __float_as_uint(s.c.w);
-        if (lane == 0 && any_vis) io.visible[gid] = 1;
-        flush_acc(v, lane, gid, io.acc);
+        bwd_entry<CUT>(sm[k], jb + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
       }
     }
   }
@@ -808,6 +909,11 @@ void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
 #define VG_RB(C, L) \
   k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
+  if (cut && vmask) {
+    if (loss) k_render_bwd_vm<1><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
+    else k_render_bwd_vm<0><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
+    return;
+  }
   if (cut) {
     if (loss) VG_RB(true, 1); else VG_RB(true, 0);
   } else {
