@@ -597,10 +597,10 @@ __device__ __forceinline__ GRec load_rec(const GRec* __restrict__ rec, uint32_t 
 }
 
 // K6, warp-independent (alpha_cut > 0): the forward's bitmask names exactly
-// the (entry, warp block) pairs with a visible pixel, so each warp fetches only
-// those records itself -- the chunk's Gaussian ids with one coalesced load,
-// each record with broadcast loads prefetched one entry ahead -- with no
-// shared-memory staging and no CTA-wide barrier in the replay loop.
+// the (entry, warp block) pairs with a visible pixel, so each warp stages only
+// those records itself -- per 32-entry chunk, lane i gathers the i-th visible
+// record into the warp's shared-memory slice (all loads in flight at once) --
+// with no CTA-wide barrier in the replay loop.
 template <int LOSS>
 __global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ rec,
                                                       const uint32_t* __restrict__ vals,
@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ r
                                                       BlendParams p, BwdIO io,
                                                       const uint32_t* __restrict__ vmask,
                                                       int vm_words) {
+  __shared__ SRec wstage[NT];  // 32 staged records per warp
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -628,6 +629,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ r
   F2 T = f2s(1.f), P = f2s(0.f);
   const uint32_t* row = vmask + (size_t)warp * vm_words;
   const int x0 = tx * TILE, y0 = ty * TILE;
+  SRec* wsm = wstage + warp * 32;
   for (int c = 0; c < warp_na; c += 32) {
     const uint32_t g0 = r.x + c;
     const uint32_t sh = g0 & 31u;
@@ -636,26 +638,20 @@ __global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ r
     const int nb = warp_na - c;
     if (nb < 32) bits &= (1u << nb) - 1u;
     if (!bits) continue;
-    const uint32_t my_gid = (c + lane < warp_na) ? __ldg(vals + g0 + lane) : 0u;
-    int k = __ffs(bits) - 1;
-    bits &= bits - 1;
-    uint32_t gid = __shfl_sync(FULL, my_gid, k);
-    GRec cur = load_rec(rec, gid);
-    while (true) {
-      const int kn = bits ? __ffs(bits) - 1 : -1;
-      uint32_t gidn = __shfl_sync(FULL, my_gid, kn < 0 ? 0 : kn);
-      GRec nxt;
-      if (kn >= 0) {
-        bits &= bits - 1;
-        nxt = load_rec(rec, gidn);
-      }
-      const SRec s = derive_srec(cur, gid, x0, y0);
-      bwd_entry<true>(s, c + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
-      if (kn < 0) break;
-      cur = nxt;
-      k = kn;
-      gid = gidn;
+    // lane i stages the i-th visible entry of the chunk (all loads in flight at once)
+    const int m = __popc(bits);
+    const int kk = (int)__fns(bits, 0, lane + 1);  // position of the (lane+1)-th set bit
+    if (lane < m) {
+      const uint32_t gid = __ldg(vals + g0 + kk);
+      wsm[lane] = derive_srec(rec[gid], gid, x0, y0);
     }
+    __syncwarp();
+    for (int q = 0; q < m; ++q) {
+      const int k = __ffs(bits) - 1;
+      bits &= bits - 1;
+      bwd_entry<true>(wsm[q], c + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+    }
+    __syncwarp();
   }
 }
 

@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -66,6 +67,8 @@ struct vg_context {
   bool prepared = false;
   bool have_fwd = false;
   bool pending = false;          // vg_prepare_async issued, finish outstanding
+  bool use_cub = false;          // VG_CUB_SORT=1: CUB onesweep instead of vg_radix (A/B)
+  uint32_t* perm_ptr = nullptr;  // depth order of the last prepare
   cudaEvent_t count_ready = nullptr;
   // event profiling (vg_profile)
   bool prof = false;
@@ -133,6 +136,10 @@ int vg_create(vg_context** out, int32_t device) {
   VG_CUDA(cudaSetDevice(device));
   vg_context* c = new vg_context();
   c->device = device;
+  {
+    const char* e = getenv("VG_CUB_SORT");
+    c->use_cub = e && e[0] == '1';
+  }
   // keep freed stream-ordered allocations cached in the device pool
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -267,20 +274,33 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
                         (int4*)c->rect.p, (uint32_t*)c->count.p, (float*)c->frame.p, st);
     }
     VG_LAUNCHED(c, 1);
-    // Gaussians in (float32 depth, index) order
-    uint32_t* ids_in = (uint32_t*)c->perm.p + n;
-    uint32_t* perm = (uint32_t*)c->perm.p;
-    launch_iota(n, ids_in, st);
+    // Gaussians in (float32 depth, index) order: hand-written radix sort of
+    // the depth bits over the identity permutation (stable => index order)
+    uint32_t* ids0 = (uint32_t*)c->perm.p + n;
+    uint32_t* ids1 = (uint32_t*)c->perm.p;
+    launch_iota(n, ids0, st);
     VG_LAUNCHED(c, 1);
-    size_t tmp = 0;
-    VG_CUDA(depth_sort_temp_bytes(n, &tmp));
-    VG_TRY(ensure(c->dsort_tmp, tmp, st));
+    uint32_t* perm = ids1;
     {
       ProfScope ps(c, VG_K_SORT, st);
-      VG_CUDA(depth_sort(c->dsort_tmp.p, c->dsort_tmp.bytes, (const uint32_t*)c->depth.p,
-                         (uint32_t*)c->dkey.p, ids_in, perm, n, st));
+      if (c->use_cub) {
+        size_t tmp = 0;
+        VG_CUDA(depth_sort_temp_bytes(n, &tmp));
+        VG_TRY(ensure(c->dsort_tmp, tmp, st));
+        VG_CUDA(depth_sort(c->dsort_tmp.p, c->dsort_tmp.bytes, (const uint32_t*)c->depth.p,
+                           (uint32_t*)c->dkey.p, ids0, ids1, n, st));
+        c->launches += 5;
+      } else {
+        VG_TRY(ensure(c->dsort_tmp, radix_temp_bytes(n, 32), st));
+        int which = 0, nl = 0;
+        VG_CUDA(radix_sort_u32(c->dsort_tmp.p, c->dsort_tmp.bytes, (uint32_t*)c->depth.p,
+                               (uint32_t*)c->dkey.p, ids0, ids1, n, 32, &which, &nl, st));
+        c->launches += nl;
+        perm = which ? ids1 : ids0;
+      }
     }
-    c->launches += 5;
+    c->perm_ptr = perm;
+    size_t tmp = 0;
     launch_gather_counts(n, perm, (const uint32_t*)c->count.p, (uint32_t*)c->cnt_s.p, st);
     VG_LAUNCHED(c, 1);
     VG_CUDA(scan_temp_bytes(n, &tmp));
@@ -314,7 +334,7 @@ int vg_prepare_finish(vg_context* c, void* stream) {
     // the only host synchronisation of the pipeline: the pair count sizes the sort
     VG_CUDA(cudaEventSynchronize(c->count_ready));
     uint64_t P = *c->total_host;
-    if (P > 0x7fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^31");
+    if (P > 0x3fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^30");
     c->pairs = (int64_t)P;
   }
   const int64_t P = c->pairs;
@@ -327,24 +347,38 @@ int vg_prepare_finish(vg_context* c, void* stream) {
     VG_TRY(ensure(c->vals1, sizeof(uint32_t) * (size_t)P, st));
     {
       ProfScope ps(c, VG_K_DUPLICATE, st);
-      launch_duplicate_sorted(n, (const uint32_t*)c->perm.p, (const uint32_t*)c->offset.p,
+      launch_duplicate_sorted(n, c->perm_ptr, (const uint32_t*)c->offset.p,
                               (const uint32_t*)c->cnt_s.p, (const int4*)c->rect.p, k.ntx,
                               c->keys0.p, wide, (uint32_t*)c->vals0.p, st);
     }
     VG_LAUNCHED(c, 1);
     int tile_bits = 1;
     while ((1 << tile_bits) < c->n_tiles) ++tile_bits;
-    size_t tmp = 0;
-    VG_CUDA(tile_sort_temp_bytes(P, tile_bits, wide, &tmp));
-    VG_TRY(ensure(c->sort_tmp, tmp, st));
     int which = 0;
     {
       ProfScope ps(c, VG_K_SORT, st);
-      VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, c->keys0.p, c->keys1.p,
-                        (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P, tile_bits, wide, &which,
-                        st));
+      if (c->use_cub) {
+        size_t tmp = 0;
+        VG_CUDA(tile_sort_temp_bytes(P, tile_bits, wide, &tmp));
+        VG_TRY(ensure(c->sort_tmp, tmp, st));
+        VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, c->keys0.p, c->keys1.p,
+                          (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P, tile_bits, wide, &which,
+                          st));
+        c->launches += sort_launches(tile_bits);
+      } else {
+        VG_TRY(ensure(c->sort_tmp, radix_temp_bytes(P, tile_bits), st));
+        int nl = 0;
+        if (wide)
+          VG_CUDA(radix_sort_u32(c->sort_tmp.p, c->sort_tmp.bytes, (uint32_t*)c->keys0.p,
+                                 (uint32_t*)c->keys1.p, (uint32_t*)c->vals0.p,
+                                 (uint32_t*)c->vals1.p, P, tile_bits, &which, &nl, st));
+        else
+          VG_CUDA(radix_sort_u16(c->sort_tmp.p, c->sort_tmp.bytes, (uint16_t*)c->keys0.p,
+                                 (uint16_t*)c->keys1.p, (uint32_t*)c->vals0.p,
+                                 (uint32_t*)c->vals1.p, P, tile_bits, &which, &nl, st));
+        c->launches += nl;
+      }
     }
-    c->launches += sort_launches(tile_bits);
     c->keys = which ? c->keys1.p : c->keys0.p;
     c->vals = which ? (uint32_t*)c->vals1.p : (uint32_t*)c->vals0.p;
     {

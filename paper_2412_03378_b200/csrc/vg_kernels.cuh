@@ -81,6 +81,14 @@ void launch_duplicate_sorted(int64_t n, const uint32_t* perm, const uint32_t* of
                              const uint32_t* count_sorted, const int4* rect, int ntx, void* keys,
                              bool wide, uint32_t* vals, cudaStream_t st);
 void launch_tile_ranges(int64_t P, const void* keys, bool wide, uint2* ranges, cudaStream_t st);
+// hand-written onesweep radix sort (vg_radix.cu); result buffer in *which
+size_t radix_temp_bytes(int64_t n, int key_bits);
+cudaError_t radix_sort_u32(void* tmp, size_t tmp_bytes, uint32_t* k0, uint32_t* k1, uint32_t* v0,
+                           uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
+                           cudaStream_t st);
+cudaError_t radix_sort_u16(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
+                           uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
+                           cudaStream_t st);
 // heavy-tiles-first order: tile ids sorted by descending list length
 cudaError_t tile_order_temp_bytes(int n_tiles, size_t* bytes);
 cudaError_t tile_order(void* tmp, size_t tmp_bytes, const uint2* ranges, uint32_t* len_in,
