@@ -580,81 +580,6 @@ __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo
   __syncthreads();
 }
 
-__device__ __forceinline__ SRec derive_srec(const GRec& g, uint32_t gid, int x0, int y0) {
-  const float bu = (float)((double)x0 + 0.5 - g.u);
-  const float bv = (float)((double)y0 + 0.5 - g.v);
-  SRec s;
-  s.a = make_float4(g.P11 * bu, fmaf(g.P22, bv, g.P21 * bu), fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm)),
-                    g.cD2);
-  s.b = make_float4(g.P11, g.P21, g.P22, g.kap2);
-  s.c = make_float4(g.n1, g.n2, g.D, __uint_as_float(gid));
-  s.d = make_float4(g.cr, g.cg, g.cb, 0.f);
-  return s;
-}
-
-__device__ __forceinline__ GRec load_rec(const GRec* __restrict__ rec, uint32_t gid) {
-  return rec[gid];
-}
-
-// K6, warp-independent (alpha_cut > 0): the forward's bitmask names exactly
-// the (entry, warp block) pairs with a visible pixel, so each warp stages only
-// those records itself -- per 32-entry chunk, lane i gathers the i-th visible
-// record into the warp's shared-memory slice (all loads in flight at once) --
-// with no CTA-wide barrier in the replay loop.
-template <int LOSS>
-__global__ void __launch_bounds__(NT) k_render_bwd_vm(const GRec* __restrict__ rec,
-                                                      const uint32_t* __restrict__ vals,
-                                                      const uint2* __restrict__ ranges,
-                                                      const uint32_t* __restrict__ order,
-                                                      BlendParams p, BwdIO io,
-                                                      const uint32_t* __restrict__ vmask,
-                                                      int vm_words) {
-  __shared__ SRec wstage[NT];  // 32 staged records per warp
-  const int tile = order[blockIdx.x];
-  const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const LaneGeo G = lane_geo(p, tx, ty);
-  const float lx = (float)G.lxi;
-  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
-  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
-  const uint2 r = ranges[tile];
-  float dcv[2][3], totv[2];
-  int nav[2];
-  bwd_prologue<LOSS>(p, G, io, dcv, totv, nav, nullptr);
-  int warp_na = max(nav[0], nav[1]);
-  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
-  const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
-           dcb = f2(dcv[0][2], dcv[1][2]);
-  const F2 tot = f2(totv[0], totv[1]);
-  F2 T = f2s(1.f), P = f2s(0.f);
-  const uint32_t* row = vmask + (size_t)warp * vm_words;
-  const int x0 = tx * TILE, y0 = ty * TILE;
-  SRec* wsm = wstage + warp * 32;
-  for (int c = 0; c < warp_na; c += 32) {
-    const uint32_t g0 = r.x + c;
-    const uint32_t sh = g0 & 31u;
-    unsigned bits = __ldg(row + (g0 >> 5)) >> sh;
-    if (sh) bits |= __ldg(row + (g0 >> 5) + 1) << (32u - sh);
-    const int nb = warp_na - c;
-    if (nb < 32) bits &= (1u << nb) - 1u;
-    if (!bits) continue;
-    // lane i stages the i-th visible entry of the chunk (all loads in flight at once)
-    const int m = __popc(bits);
-    const int kk = (int)__fns(bits, 0, lane + 1);  // position of the (lane+1)-th set bit
-    if (lane < m) {
-      const uint32_t gid = __ldg(vals + g0 + kk);
-      wsm[lane] = derive_srec(rec[gid], gid, x0, y0);
-    }
-    __syncwarp();
-    for (int q = 0; q < m; ++q) {
-      const int k = __ffs(bits) - 1;
-      bits &= bits - 1;
-      bwd_entry<true>(wsm[q], c + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
-    }
-    __syncwarp();
-  }
-}
-
 // ---------------------------------------------------------------------------
 // K6 backward blend (grad.backward tile_job + e_chain)
 
@@ -905,11 +830,6 @@ void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
 #define VG_RB(C, L) \
   k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
-  if (cut && vmask) {
-    if (loss) k_render_bwd_vm<1><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
-    else k_render_bwd_vm<0><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
-    return;
-  }
   if (cut) {
     if (loss) VG_RB(true, 1); else VG_RB(true, 0);
   } else {

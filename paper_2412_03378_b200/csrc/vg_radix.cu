@@ -45,9 +45,19 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, in
   for (int i = threadIdx.x; i < 4 * BINS; i += THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * THREADS;
-  for (int64_t i = (int64_t)blockIdx.x * THREADS + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = (uint32_t)keys[i];
-    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (BITS * p)) & (BINS - 1)], 1u);
+  const int64_t n_round = (n + stride - 1) / stride * stride;  // whole warps iterate together
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+  for (int64_t i = (int64_t)blockIdx.x * THREADS + threadIdx.x; i < n_round; i += stride) {
+    const bool valid = i < n;
+    const uint32_t k = valid ? (uint32_t)keys[i] : 0u;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    for (int p = 0; p < passes; ++p) {
+      // warp-aggregated: one shared atomic per distinct digit in the warp
+      // (the top byte of float depths is nearly constant)
+      const uint32_t d = (k >> (BITS * p)) & (BINS - 1);
+      const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu) & vm;
+      if (valid && (peers & lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * BINS; i += THREADS) {
