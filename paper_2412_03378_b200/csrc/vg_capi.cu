@@ -67,7 +67,7 @@ struct vg_context {
   bool prepared = false;
   bool have_fwd = false;
   bool pending = false;          // vg_prepare_async issued, finish outstanding
-  bool use_cub = false;          // VG_CUB_SORT=1: CUB onesweep instead of vg_radix (A/B)
+  bool use_cub = true;           // false with VG_RADIX=1: hand-written sort (A/B)
   uint32_t* perm_ptr = nullptr;  // depth order of the last prepare
   cudaEvent_t count_ready = nullptr;
   // event profiling (vg_profile)
@@ -137,8 +137,10 @@ int vg_create(vg_context** out, int32_t device) {
   vg_context* c = new vg_context();
   c->device = device;
   {
-    const char* e = getenv("VG_CUB_SORT");
-    c->use_cub = e && e[0] == '1';
+    // VG_RADIX=1 selects the hand-written onesweep sort (vg_radix.cu); CUB's
+    // onesweep is the default until the hand-written one is faster
+    const char* e = getenv("VG_RADIX");
+    c->use_cub = !(e && e[0] == '1');
   }
   // keep freed stream-ordered allocations cached in the device pool
   cudaMemPool_t pool;
