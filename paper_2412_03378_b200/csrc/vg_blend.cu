@@ -649,178 +649,6 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
 }
 
 // ---------------------------------------------------------------------------
-// K6, two-phase variant (alpha_cut > 0, driven by the forward's bitmask).
-// Per warp and group of up to 16 visible entries:
-//   phase 1 (pixel-parallel, list order): recompute alpha, advance T and the
-//     running suffix exactly as bwd_entry does, and write each pixel's
-//     h = dL/de * beta * peak and contrib = alpha T_before to a per-warp
-//     shared buffer;
-//   phase 2 (Gaussian-parallel): lane (q, half) owns entry q of the group and
-//     32 of the block's 64 pixels, recomputes the pixel geometry and
-//     accumulates the 13 per-Gaussian sums in registers; one shuffle joins
-//     the two halves and 16 lanes issue the atomics.
-// This replaces a 13-value warp transpose-reduction per entry with a
-// register accumulation (the algebra is pinhole_grad_terms').
-constexpr int GROUP = 16;
-constexpr int HC_STRIDE = 132;  // words per group slot: 32 lanes x (h0, c0, h1, c1) + pad
-
-template <int LOSS>
-__global__ void __launch_bounds__(NT) k_render_bwd2(const GRec* __restrict__ rec,
-                                                    const uint32_t* __restrict__ vals,
-                                                    const uint2* __restrict__ ranges,
-                                                    const uint32_t* __restrict__ order,
-                                                    BlendParams p, BwdIO io,
-                                                    const uint32_t* __restrict__ vmask,
-                                                    int vm_words) {
-  __shared__ SRec sm[BATCH];
-  extern __shared__ __align__(16) float hc_dyn[];  // (NT/32) * GROUP * HC_STRIDE floats
-  __shared__ float dcs[NT / 32][3][64];
-  __shared__ int kidx[NT / 32][GROUP];
-  __shared__ int s_maxna;
-  const int tile = order[blockIdx.x];
-  const int tx = tile % p.ntx, ty = tile / p.ntx;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const LaneGeo G = lane_geo(p, tx, ty);
-  const float lx = (float)G.lxi;
-  const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
-  const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
-  const uint2 r = ranges[tile];
-  float dcv[2][3], totv[2];
-  int nav[2];
-  if (threadIdx.x == 0) s_maxna = 0;
-  bwd_prologue<LOSS>(p, G, io, dcv, totv, nav, &s_maxna);
-  int warp_na = max(nav[0], nav[1]);
-  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
-  const uint32_t end = r.x + (uint32_t)s_maxna;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    dcs[warp][c][lane] = dcv[0][c];
-    dcs[warp][c][32 + lane] = dcv[1][c];
-  }
-  const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
-           dcb = f2(dcv[0][2], dcv[1][2]);
-  const F2 tot = f2(totv[0], totv[1]);
-  F2 T = f2s(1.f), P = f2s(0.f);
-  // phase-2 role of this lane: group slot q, pixel half hf (lo / hi pixels of lanes 0..31)
-  const int q2 = lane & 15, hf = lane >> 4;
-  const float lpx_base = (float)(8 * (warp & 1));
-  const float lpy_base = (float)(8 * (warp >> 1) + 4 * hf);
-  float* myhc = hc_dyn + warp * GROUP * HC_STRIDE;
-  int ng = 0;  // entries in the current group
-
-  auto flush_group = [&](int n) {
-    __syncwarp();
-    {
-      // every lane runs the loop (shuffles below need the full warp); slots
-      // beyond the group size read slot 0's record and discard their sums
-      const bool mine = q2 < n;
-      const SRec s = sm[kidx[warp][mine ? q2 : 0]];
-      float a[13];
-#pragma unroll
-      for (int i = 0; i < 13; ++i) a[i] = 0.f;
-      const float* row = myhc + q2 * HC_STRIDE + 2 * hf;
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        const float2 hcv = *reinterpret_cast<const float2*>(row + 4 * j);
-        const float h = mine ? hcv.x : 0.f, cn = mine ? hcv.y : 0.f;
-        const float plx = lpx_base + (float)(j & 7);
-        const float ply = lpy_base + (float)(j >> 3);
-        const float q1 = fmaf(s.b.x, plx, s.a.x);
-        const float qq2 = fmaf(s.b.y, plx, fmaf(s.b.z, ply, s.a.y));
-        const float wp = fmaf(s.c.x, plx, fmaf(s.c.y, ply, s.a.z));
-        const float X = fmaf(qq2, qq2, q1 * q1);
-        const float rs = rsqf(fmaf(wp, wp, X));
-        const float ri = rs * rs;
-        const float sD = s.c.z * ri, s2 = sD * sD, wp2 = wp * wp;
-        const float k1 = h * fmaf(s2, wp2, ri);
-        const float k2 = h * wp * fmaf(-s2, X, ri);
-        const float k1q1 = k1 * q1;
-        a[0] = fmaf(k1q1, q1, a[0]);
-        a[1] = fmaf(k1q1, qq2, a[1]);
-        a[2] = fmaf(k2, q1, a[2]);
-        a[3] = fmaf(k1 * qq2, qq2, a[3]);
-        a[4] = fmaf(k2, qq2, a[4]);
-        a[5] = fmaf(h, fmaf(s2, X * X, ri * wp2), a[5]);
-        const float hsD = h * sD, hsw = hsD * wp;
-        a[6] = fmaf(-hsw, q1, a[6]);
-        a[7] = fmaf(-hsw, qq2, a[7]);
-        a[8] = fmaf(hsD, X, a[8]);
-        a[9] += h;
-        const int pix = hf * 32 + j;
-        a[10] = fmaf(cn, dcs[warp][0][pix], a[10]);
-        a[11] = fmaf(cn, dcs[warp][1][pix], a[11]);
-        a[12] = fmaf(cn, dcs[warp][2][pix], a[12]);
-      }
-#pragma unroll
-      for (int i = 0; i < 13; ++i) a[i] += __shfl_xor_sync(FULL, a[i], 16);
-      if (hf == 0 && mine) {
-        float* o = io.acc + (size_t)__float_as_uint(s.c.w) * ACC_STRIDE;
-#pragma unroll
-        for (int i = 0; i < 13; ++i)
-          if (a[i] != 0.f) atomicAdd(o + i, a[i]);
-      }
-    }
-    __syncwarp();
-  };
-
-  for (uint32_t base = r.x; base < end; base += BATCH) {
-    __syncthreads();
-    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
-      const uint32_t i = base + sidx;
-      if (i < end) stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, false, p.ecut);
-    }
-    __syncthreads();
-    const int jb = (int)(base - r.x);
-    const int nb = min(min((int)BATCH, (int)(end - base)), warp_na - jb);
-    for (int c = 0; c < nb; c += 32) {
-      const uint32_t g = base + c;
-      const uint32_t* vrow = vmask + (size_t)warp * vm_words + (g >> 5);
-      const uint32_t sh = g & 31u;
-      unsigned bits = __ldg(vrow) >> sh;
-      if (sh) bits |= __ldg(vrow + 1) << (32u - sh);
-      if (nb - c < 32) bits &= (1u << (nb - c)) - 1u;
-      while (bits) {
-        const int k = c + __ffs(bits) - 1;
-        bits &= bits - 1;
-        // ---- phase 1 for entry k (same arithmetic as bwd_entry)
-        const SRec s = sm[k];
-        const int j = jb + k;
-        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
-        const bool act0 = j < nav[0], act1 = j < nav[1];
-        float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
-        float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-        const bool cut0 = om0 > p.omcut, cut1 = om1 > p.omcut;
-        om0 = cut0 ? 1.f : om0;
-        om1 = cut1 ? 1.f : om1;
-        const F2 om = f2(om0, om1);
-        const F2 contrib = mul2(sub2(f2s(1.f), om), T);
-        const F2 Tn = mul2(T, om);
-        const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
-        P = fma2(dot, contrib, P);
-        T = Tn;
-        const bool live0 = !cut0 && lo(e.ex) > p.cc;
-        const bool live1 = !cut1 && hi(e.ex) > p.cc;
-        const F2 de = sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f));
-        const F2 h = mul2(de, e.G);
-        const bool vis = om0 < 1.f || om1 < 1.f;
-        if (__any_sync(FULL, vis) && lane == 0) io.visible[__float_as_uint(s.c.w)] = 1;
-        *reinterpret_cast<float4*>(myhc + ng * HC_STRIDE + 4 * lane) =
-            make_float4(lo(h), lo(contrib), hi(h), hi(contrib));
-        if (lane == 0) kidx[warp][ng] = k;
-        if (++ng == GROUP) {
-          flush_group(GROUP);
-          ng = 0;
-        }
-      }
-    }
-    if (ng) {  // the group's records must be consumed before the next staging
-      flush_group(ng);
-      ng = 0;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // K8 tomography (tomo.tomo_forward / tomo_backward): order-independent sum
 // of e over every binned pair; no cut, clamp or early stop (tomo.py:43-47).
 
@@ -1002,21 +830,6 @@ void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
 #define VG_RB(C, L) \
   k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
-  if (cut && vmask) {
-    const int dyn = (NT / 32) * GROUP * HC_STRIDE * (int)sizeof(float);
-    // per device, once (attributes are per function and device)
-    static bool attr[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || !attr[dev]) {
-      cudaFuncSetAttribute(k_render_bwd2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-      cudaFuncSetAttribute(k_render_bwd2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-      if (dev >= 0 && dev < 64) attr[dev] = true;
-    }
-    if (loss) k_render_bwd2<1><<<n_tiles, NT, dyn, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
-    else k_render_bwd2<0><<<n_tiles, NT, dyn, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words);
-    return;
-  }
   if (cut) {
     if (loss) VG_RB(true, 1); else VG_RB(true, 0);
   } else {
