@@ -24,9 +24,9 @@ namespace radix {
 
 constexpr int BITS = 8;
 constexpr int BINS = 256;
-constexpr int THREADS = 256;
+constexpr int THREADS = 512;
 constexpr int WARPS = THREADS / 32;
-constexpr int ITEMS = 16;                     // per thread
+constexpr int ITEMS = 8;                      // per thread
 constexpr int TILE_ITEMS = THREADS * ITEMS;   // 4096
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* 
                                                   uint32_t* __restrict__ status,
                                                   uint32_t* __restrict__ tile_counter) {
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t wcnt[WARPS][BINS];  // per-warp digit counts -> exclusive offsets
+  __shared__ uint16_t wcnt[WARPS][BINS];  // per-warp digit counts -> exclusive offsets (< 4096)
   __shared__ uint32_t s_scan[BINS];       // tile-local exclusive offset per digit
   __shared__ uint32_t s_global[BINS];     // global output base of this tile per digit
   __shared__ K s_keys[TILE_ITEMS];
@@ -130,18 +130,18 @@ __global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* 
     const uint32_t before = valid ? wcnt[warp][d] : 0u;
     __syncwarp();
     rank[i] = before + __popc(peers & lt);
-    if (valid && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+    if (valid && (peers & lt) == 0) wcnt[warp][d] = (uint16_t)(before + __popc(peers));
     __syncwarp();
   }
   __syncthreads();
-  // per digit (thread d): exclusive prefix over warps, publish, look back
-  {
+  // per digit (thread d < 256): exclusive prefix over warps, publish, look back
+  if (threadIdx.x < BINS) {
     const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const uint32_t c = wcnt[w][d];
-      wcnt[w][d] = run;
+      wcnt[w][d] = (uint16_t)run;
       run += c;
     }
     uint32_t* st = status + (size_t)tile * BINS + d;
@@ -167,16 +167,17 @@ __global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* 
   // tile-local exclusive offsets per digit (Hillis-Steele scan of the totals)
   {
     const int d = threadIdx.x;
-    const uint32_t v = s_scan[d];
+    const bool on = d < BINS;
+    const uint32_t v = on ? s_scan[d] : 0u;
     for (int off = 1; off < BINS; off <<= 1) {
-      const uint32_t t = d >= off ? s_scan[d - off] : 0u;
+      const uint32_t t = (on && d >= off) ? s_scan[d - off] : 0u;
       __syncthreads();
-      s_scan[d] += t;
+      if (on) s_scan[d] += t;
       __syncthreads();
     }
-    const uint32_t incl = s_scan[d];
+    const uint32_t incl = on ? s_scan[d] : 0u;
     __syncthreads();
-    s_scan[d] = incl - v;
+    if (on) s_scan[d] = incl - v;
   }
   __syncthreads();
   // reorder the tile through shared memory by digit (stable), then write runs

@@ -339,3 +339,24 @@ def test_degenerate_inputs():
     for f in GRAD_FIELDS:
         check_field(getattr(g, f), getattr(rg, f), f"degenerate {f}")
     assert g.d_scales[0, 1] == 0.0
+
+
+@pytest.mark.parametrize("name", ["tiny", "mini_opaque", "large"])
+def test_handwritten_radix_sort_lists(name, monkeypatch):
+    """The hand-written onesweep sort (vg_radix.cu, VG_RADIX=1) produces the
+    same bit-exact tile lists as the oracle (depth sort of N keys + stable
+    tile sort of the pairs, many tiles of look-back on the large config)."""
+    monkeypatch.setenv("VG_RADIX", "1")
+    if name == "large":
+        from paper_2412_03378_b200 import configs
+        cfg = configs.large()
+        scene, cam = _f64_scene(cfg.scene), cfg.cameras[5]
+        flags = {"alpha_cut": O.ALPHA_CUT}
+    else:
+        scene, cam, d = load_case(name)
+        flags = case_flags(d)
+    prep = vg().prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    oprep = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"], key_dtype=np.float32)
+    prims, offs = prep.tile_lists_device()
+    assert np.array_equal(offs.cpu().numpy(), oprep.tile_start)
+    assert np.array_equal(prims.cpu().numpy(), oprep.pair_prim)
