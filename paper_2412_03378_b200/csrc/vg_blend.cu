@@ -375,10 +375,8 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
       const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
       unsigned bits = __ballot_sync(FULL, vb);
       unsigned seen = 0;  // entries of this chunk with a visible pixel in this warp's block
-      while (bits) {
-        const int k = c + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const SRec s = sm[k];
+      // composite one evaluated entry (front to back; T carries the order)
+      auto composite = [&](int k, const SRec& s, const Pair2& e) {
         if (STOP) {
           // active iff the transmittance in front is >= stop (raster.py:384-385);
           // n_act = 1 + index of the last active processed entry
@@ -388,7 +386,6 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
           na0 = a0 ? jb + k : na0;
           na1 = a1 ? jb + k : na1;
         }
-        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
         float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
         if (CUT) {
           const bool c0 = om0 > p.omcut, c1 = om1 > p.omcut;
@@ -410,6 +407,24 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
         if (STATS) {
           st_proc++;
           st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
+        }
+      };
+      // two visible entries per iteration: their (independent) alpha
+      // evaluations overlap before the short compositing chain
+      while (bits) {
+        const int k = c + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const SRec s = sm[k];
+        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        if (bits) {
+          const int kb = c + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const SRec sb = sm[kb];
+          const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
+          composite(k, s, e);
+          composite(kb, sb, eb);
+        } else {
+          composite(k, s, e);
         }
       }
       if (vmask && seen && lane == 0) {
@@ -492,11 +507,10 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
 // forward did, advance T and the running suffix, form dL/de for live pixels,
 // and flush the warp's 13 accumulator sums for this Gaussian.
 template <bool CUT>
-__device__ __forceinline__ void bwd_entry(const SRec& s, int j, float lx, F2 ly, F2 Lp,
+__device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, int j,
                                           const int (&nav)[2], F2 dcr, F2 dcg, F2 dcb, F2 tot,
                                           const BlendParams& p, F2& T, F2& P, int lane,
                                           const BwdIO& io) {
-  const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
   // inactive entries (j >= n_act) get a floor of 1: alpha = 0, no change
   const bool act0 = j < nav[0], act1 = j < nav[1];
   float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
@@ -639,10 +653,23 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
         const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
         bits = __ballot_sync(FULL, vb);
       }
+      // two visible entries per iteration: both alpha evaluations are
+      // issued before the replay chain of the first
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
-        bwd_entry<CUT>(sm[k], jb + k, lx, ly, Lp, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+        const SRec s = sm[k];
+        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        if (bits) {
+          const int kb = c + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const SRec sb = sm[kb];
+          const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
+          bwd_entry<CUT>(s, e, jb + k, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT>(sb, eb, jb + kb, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+        } else {
+          bwd_entry<CUT>(s, e, jb + k, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+        }
       }
     }
   }

@@ -24,9 +24,9 @@ namespace radix {
 
 constexpr int BITS = 8;
 constexpr int BINS = 256;
-constexpr int THREADS = 512;
+constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int ITEMS = 8;                      // per thread
+constexpr int ITEMS = 16;                     // per thread
 constexpr int TILE_ITEMS = THREADS * ITEMS;   // 4096
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;
