@@ -46,23 +46,23 @@ struct vg_context {
   // per-Gaussian
   Buf rec, depth, rect, count, offset, acc;
   // per-pair (double-buffered for the radix sort)
-  Buf keys0, keys1, vals0, vals1;
-  Buf ranges, n_act, scan_tmp, sort_tmp, total;
-  Buf tlen, tord, ord_tmp;  // heavy-first tile order
-  Buf dkey, perm, cnt_s, dsort_tmp;  // depth pre-sort of the Gaussians
+  Buf vals0;                         // per-tile Gaussian lists (depth order), P entries
+  Buf ranges, n_act, total;
+  Buf tord;                          // heavy-first tile launch order
+  Buf span1, span2;                  // span-binning scratch (vg_span.cu)
+  Buf dkey, perm, dsort_tmp;         // depth pre-sort of the Gaussians
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
   Buf cacc;                          // colour / SH gradient accumulators, SoA [3|48][N]
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
-  uint64_t* total_host = nullptr;
+  unsigned long long* total_host = nullptr;  // {pairs, step-2 span chunks}
   // state of the last prepare
   vg_scene scene{};
   CamK cam{};
   vg_options opt{};
   int64_t pairs = 0;
   int n_tiles = 0;
-  void* keys = nullptr;      // sorted tile ids (uint16, or uint32 beyond 65536 tiles)
   uint32_t* vals = nullptr;
   bool prepared = false;
   bool have_fwd = false;
@@ -148,7 +148,11 @@ int vg_create(vg_context** out, int32_t device) {
     uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
-  if (cudaMallocHost(&c->total_host, sizeof(uint64_t)) != cudaSuccess) {
+  if (span_configure() != cudaSuccess) {
+    delete c;
+    return fail(VG_ECUDA, "vg_create: kernel attribute setup failed");
+  }
+  if (cudaMallocHost(&c->total_host, 2 * sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return fail(VG_ENOMEM, "vg_create: pinned alloc failed");
   }
@@ -165,10 +169,10 @@ void vg_destroy(vg_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  Buf* all[] = {&c->rec, &c->depth, &c->rect, &c->count, &c->offset, &c->acc, &c->keys0,
-                &c->keys1, &c->vals0, &c->vals1, &c->ranges, &c->n_act, &c->scan_tmp,
-                &c->sort_tmp, &c->total, &c->tlen, &c->tord, &c->ord_tmp, &c->dkey,
-                &c->perm, &c->cnt_s, &c->dsort_tmp, &c->frame, &c->lacc, &c->cacc, &c->vmask};
+  Buf* all[] = {&c->rec,  &c->depth, &c->rect,  &c->count, &c->offset, &c->acc,
+                &c->vals0, &c->ranges, &c->n_act, &c->total, &c->tord, &c->span1,
+                &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
+                &c->cacc, &c->vmask};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -248,7 +252,9 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   const int64_t npix = (int64_t)k.width * k.height;
   VG_TRY(ensure(c->ranges, sizeof(uint2) * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->n_act, sizeof(int) * (size_t)npix, st));
-  VG_TRY(ensure(c->total, sizeof(uint64_t), st));
+  VG_TRY(ensure(c->total, 2 * sizeof(unsigned long long), st));
+  if (k.ntx > span_max_buckets() || k.nty > span_max_buckets())
+    return fail(VG_EINVAL, "image too large: at most 1024 tile rows and columns (16384 px)");
   VG_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->n_tiles, st));
   c->pairs = 0;
   if (n > 0) {
@@ -261,7 +267,6 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)n, st));
     VG_TRY(ensure(c->dkey, sizeof(uint32_t) * (size_t)n, st));
     VG_TRY(ensure(c->perm, sizeof(uint32_t) * 2 * (size_t)n, st));
-    VG_TRY(ensure(c->cnt_s, sizeof(uint32_t) * (size_t)n, st));
     if (grow_acc) VG_TRY(ensure(c->acc, accb, st, true));
     if (c->lacc.bytes < sizeof(float) * 12 * (size_t)n)
       VG_TRY(ensure(c->lacc, sizeof(float) * 12 * (size_t)n, st, true));
@@ -302,21 +307,16 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
       }
     }
     c->perm_ptr = perm;
-    size_t tmp = 0;
-    launch_gather_counts(n, perm, (const uint32_t*)c->count.p, (uint32_t*)c->cnt_s.p, st);
-    VG_LAUNCHED(c, 1);
-    VG_CUDA(scan_temp_bytes(n, &tmp));
-    VG_TRY(ensure(c->scan_tmp, tmp, st));
+    // step 1 of the span binning up to the pair count (vg_span.cu)
+    VG_TRY(ensure(c->span1, span_scratch1_bytes(n, k.nty), st));
     {
       ProfScope ps(c, VG_K_SCAN, st);
-      VG_CUDA(exclusive_scan(c->scan_tmp.p, c->scan_tmp.bytes, (const uint32_t*)c->cnt_s.p,
-                             (uint32_t*)c->offset.p, n, st));
+      VG_CUDA(span_rows_begin(n, perm, (const uint32_t*)c->count.p, (const int4*)c->rect.p, k.nty,
+                              c->span1.p, (unsigned long long*)c->total.p, st));
     }
-    VG_LAUNCHED(c, 1);
-    launch_total(n, (const uint32_t*)c->cnt_s.p, (const uint32_t*)c->offset.p,
-                 (uint64_t*)c->total.p, st);
-    VG_LAUNCHED(c, 1);
-    VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    VG_LAUNCHED(c, 3);
+    VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
     VG_CUDA(cudaEventRecord(c->count_ready, st));
   }
   c->pending = true;
@@ -332,80 +332,31 @@ int vg_prepare_finish(vg_context* c, void* stream) {
   const int64_t n = c->scene.n;
   const CamK& k = c->cam;
   c->pairs = 0;
+  int64_t chunks2 = 0;
   if (n > 0) {
-    // the only host synchronisation of the pipeline: the pair count sizes the sort
+    // the only host synchronisation of the pipeline: the pair count sizes the lists
     VG_CUDA(cudaEventSynchronize(c->count_ready));
-    uint64_t P = *c->total_host;
-    if (P > 0x3fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^30");
+    const unsigned long long P = c->total_host[0];
+    if (P > 0x7fffffffull) return fail(VG_EINVAL, "tile-pair count exceeds 2^31");
     c->pairs = (int64_t)P;
+    chunks2 = (int64_t)c->total_host[1];
   }
   const int64_t P = c->pairs;
-  if (P > 0) {
-    const bool wide = c->n_tiles > 65536;
-    const size_t kb = wide ? sizeof(uint32_t) : sizeof(uint16_t);
-    VG_TRY(ensure(c->keys0, kb * (size_t)P, st));
-    VG_TRY(ensure(c->keys1, kb * (size_t)P, st));
-    VG_TRY(ensure(c->vals0, sizeof(uint32_t) * (size_t)P, st));
-    VG_TRY(ensure(c->vals1, sizeof(uint32_t) * (size_t)P, st));
-    {
-      ProfScope ps(c, VG_K_DUPLICATE, st);
-      launch_duplicate_sorted(n, c->perm_ptr, (const uint32_t*)c->offset.p,
-                              (const uint32_t*)c->cnt_s.p, (const int4*)c->rect.p, k.ntx,
-                              c->keys0.p, wide, (uint32_t*)c->vals0.p, st);
-    }
-    VG_LAUNCHED(c, 1);
-    int tile_bits = 1;
-    while ((1 << tile_bits) < c->n_tiles) ++tile_bits;
-    int which = 0;
-    {
-      ProfScope ps(c, VG_K_SORT, st);
-      if (c->use_cub) {
-        size_t tmp = 0;
-        VG_CUDA(tile_sort_temp_bytes(P, tile_bits, wide, &tmp));
-        VG_TRY(ensure(c->sort_tmp, tmp, st));
-        VG_CUDA(tile_sort(c->sort_tmp.p, c->sort_tmp.bytes, c->keys0.p, c->keys1.p,
-                          (uint32_t*)c->vals0.p, (uint32_t*)c->vals1.p, P, tile_bits, wide, &which,
-                          st));
-        c->launches += sort_launches(tile_bits);
-      } else {
-        VG_TRY(ensure(c->sort_tmp, radix_temp_bytes(P, tile_bits), st));
-        int nl = 0;
-        if (wide)
-          VG_CUDA(radix_sort_u32(c->sort_tmp.p, c->sort_tmp.bytes, (uint32_t*)c->keys0.p,
-                                 (uint32_t*)c->keys1.p, (uint32_t*)c->vals0.p,
-                                 (uint32_t*)c->vals1.p, P, tile_bits, &which, &nl, st));
-        else
-          VG_CUDA(radix_sort_u16(c->sort_tmp.p, c->sort_tmp.bytes, (uint16_t*)c->keys0.p,
-                                 (uint16_t*)c->keys1.p, (uint32_t*)c->vals0.p,
-                                 (uint32_t*)c->vals1.p, P, tile_bits, &which, &nl, st));
-        c->launches += nl;
-      }
-    }
-    c->keys = which ? c->keys1.p : c->keys0.p;
-    c->vals = which ? (uint32_t*)c->vals1.p : (uint32_t*)c->vals0.p;
-    {
-      ProfScope ps(c, VG_K_RANGES, st);
-      launch_tile_ranges(P, c->keys, wide, (uint2*)c->ranges.p, st);
-    }
-    VG_LAUNCHED(c, 1);
-  } else {
-    c->keys = nullptr;
-    c->vals = nullptr;
-  }
+  const int nt = c->n_tiles;
+  VG_TRY(ensure(c->tord, sizeof(uint32_t) * (size_t)nt, st));
+  VG_TRY(ensure(c->span2, span_scratch2_bytes(chunks2, k.ntx, nt), st));
+  if (P > 0) VG_TRY(ensure(c->vals0, sizeof(uint32_t) * (size_t)P, st));
   {
-    // tile launch order, heaviest list first
-    const int nt = c->n_tiles;
-    VG_TRY(ensure(c->tlen, sizeof(uint32_t) * 2 * (size_t)nt, st));
-    VG_TRY(ensure(c->tord, sizeof(uint32_t) * 2 * (size_t)nt, st));
-    size_t tmp = 0;
-    VG_CUDA(tile_order_temp_bytes(nt, &tmp));
-    VG_TRY(ensure(c->ord_tmp, tmp, st));
-    uint32_t* len = (uint32_t*)c->tlen.p;
-    uint32_t* ids = (uint32_t*)c->tord.p;
-    VG_CUDA(tile_order(c->ord_tmp.p, c->ord_tmp.bytes, (const uint2*)c->ranges.p, len, len + nt,
-                       ids + nt, ids, nt, st));
-    c->launches += 2;
+    // step 2: row spans -> per-tile lists, tile ranges, heavy-tiles-first order
+    ProfScope ps(c, VG_K_DUPLICATE, st);
+    int nl = 0;
+    VG_CUDA(span_finish(n, c->perm_ptr, (const uint32_t*)c->count.p, (const int4*)c->rect.p,
+                        k.ntx, k.nty, c->span1.p, P > 0 ? chunks2 : 0, c->span2.p,
+                        (uint2*)c->ranges.p, (uint32_t*)c->tord.p, (uint32_t*)c->vals0.p, &nl,
+                        st));
+    VG_LAUNCHED(c, nl);
   }
+  c->vals = P > 0 ? (uint32_t*)c->vals0.p : nullptr;
   c->prepared = true;
   return VG_OK;
 }

@@ -61,26 +61,11 @@ void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const f
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const vg_grads& g, cudaStream_t st);
 
-// radix sort / scan (vg_sort.cu)
-cudaError_t scan_temp_bytes(int64_t n, size_t* bytes);
-cudaError_t exclusive_scan(void* tmp, size_t tmp_bytes, const uint32_t* in, uint32_t* out,
-                           int64_t n, cudaStream_t st);
-int sort_launches(int end_bit);
+// depth sort of the Gaussians (CUB onesweep, vg_sort.cu)
 cudaError_t depth_sort_temp_bytes(int64_t n, size_t* bytes);
 cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out,
                        const uint32_t* ids_in, uint32_t* ids_out, int64_t n, cudaStream_t st);
-cudaError_t tile_sort_temp_bytes(int64_t n, int end_bit, bool wide, size_t* bytes);
-cudaError_t tile_sort(void* tmp, size_t tmp_bytes, void* k0, void* k1, uint32_t* v0, uint32_t* v1,
-                      int64_t n, int end_bit, bool wide, int* which, cudaStream_t st);
-// binning kernels over the depth order (vg_binning.cu)
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
-void launch_gather_counts(int64_t n, const uint32_t* perm, const uint32_t* count, uint32_t* out,
-                          cudaStream_t st);
-// tile keys are uint16 when n_tiles <= 65536 (wide = false), else uint32
-void launch_duplicate_sorted(int64_t n, const uint32_t* perm, const uint32_t* offset,
-                             const uint32_t* count_sorted, const int4* rect, int ntx, void* keys,
-                             bool wide, uint32_t* vals, cudaStream_t st);
-void launch_tile_ranges(int64_t P, const void* keys, bool wide, uint2* ranges, cudaStream_t st);
 // hand-written onesweep radix sort (vg_radix.cu); result buffer in *which
 size_t radix_temp_bytes(int64_t n, int key_bits);
 cudaError_t radix_sort_u32(void* tmp, size_t tmp_bytes, uint32_t* k0, uint32_t* k1, uint32_t* v0,
@@ -89,10 +74,18 @@ cudaError_t radix_sort_u32(void* tmp, size_t tmp_bytes, uint32_t* k0, uint32_t* 
 cudaError_t radix_sort_u16(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
                            uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
                            cudaStream_t st);
-// heavy-tiles-first order: tile ids sorted by descending list length
-cudaError_t tile_order_temp_bytes(int n_tiles, size_t* bytes);
-cudaError_t tile_order(void* tmp, size_t tmp_bytes, const uint2* ranges, uint32_t* len_in,
-                       uint32_t* len_out, uint32_t* ids_in, uint32_t* ids_out, int n_tiles,
-                       cudaStream_t st);
+// span binning (vg_span.cu): per-tile lists in depth order without a pair sort.
+// begin (before the host sync): step-1 counts; info = {pairs, step-2 chunks}.
+int span_max_buckets();
+cudaError_t span_configure();
+size_t span_scratch1_bytes(int64_t n, int nty);
+cudaError_t span_rows_begin(int64_t n, const uint32_t* perm, const uint32_t* count,
+                            const int4* rect, int nty, void* scratch1,
+                            unsigned long long* info, cudaStream_t st);
+size_t span_scratch2_bytes(int64_t chunks2, int ntx, int n_tiles);
+cudaError_t span_finish(int64_t n, const uint32_t* perm, const uint32_t* count, const int4* rect,
+                        int ntx, int nty, const void* scratch1, int64_t chunks2, void* scratch2,
+                        uint2* ranges, uint32_t* order, uint32_t* vals, int* launches,
+                        cudaStream_t st);
 
 }  // namespace vg

@@ -35,7 +35,8 @@ constexpr uint32_t VALUE_MASK = (1u << 30) - 1;
 inline size_t temp_bytes(int64_t n, int key_bits) {
   const int passes = (key_bits + BITS - 1) / BITS;
   const int64_t tiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
-  return sizeof(uint32_t) * (2 * (size_t)passes * BINS + 8 + (size_t)(tiles > 0 ? tiles : 1) * BINS);
+  return sizeof(uint32_t) * (2 * (size_t)passes * BINS + 8 +
+                             (size_t)passes * (size_t)(tiles > 0 ? tiles : 1) * BINS);
 }
 
 template <typename K>
@@ -90,16 +91,17 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
 }
 
 template <typename K>
-__global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* __restrict__ kout,
-                                                  const uint32_t* __restrict__ vin,
-                                                  uint32_t* __restrict__ vout, int64_t n, int shift,
-                                                  const uint32_t* __restrict__ bucket_base,
-                                                  uint32_t* __restrict__ status,
-                                                  uint32_t* __restrict__ tile_counter) {
+__global__ void __launch_bounds__(THREADS, 3) k_pass(const K* __restrict__ kin, K* __restrict__ kout,
+                                                     const uint32_t* __restrict__ vin,
+                                                     uint32_t* __restrict__ vout, int64_t n, int shift,
+                                                     const uint32_t* __restrict__ bucket_base,
+                                                     uint32_t* __restrict__ status,
+                                                     uint32_t* __restrict__ tile_counter, int nbits) {
   __shared__ uint32_t s_tile;
-  __shared__ uint16_t wcnt[WARPS][BINS];  // per-warp digit counts -> exclusive offsets (< 4096)
+  __shared__ uint32_t wcnt[WARPS][BINS];  // per-warp digit counts -> exclusive offsets
   __shared__ uint32_t s_scan[BINS];       // tile-local exclusive offset per digit
   __shared__ uint32_t s_global[BINS];     // global output base of this tile per digit
+  __shared__ uint32_t s_wsum[WARPS];
   __shared__ K s_keys[TILE_ITEMS];
   __shared__ uint32_t s_vals[TILE_ITEMS];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -109,39 +111,47 @@ __global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* 
   const int64_t tbase = (int64_t)tile * TILE_ITEMS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  K key[ITEMS];
-  uint32_t val[ITEMS];
+  const int64_t wbase = tbase + warp * (32 * ITEMS) + lane;
+  uint32_t dig[ITEMS];
   uint32_t rank[ITEMS];
-  // warp-striped load: warp w owns items [w*512, w*512+512) of the tile
+  // warp-striped load: warp w owns items [w*32*ITEMS, (w+1)*32*ITEMS) of the tile
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = tbase + warp * (32 * ITEMS) + i * 32 + lane;
-    key[i] = idx < n ? kin[idx] : (K)0;
-    val[i] = idx < n ? vin[idx] : 0u;
+    const int64_t idx = wbase + i * 32;
+    dig[i] = idx < n ? (((uint32_t)kin[idx] >> shift) & (BINS - 1)) : 0xffffffffu;
   }
-  // stable ranks within the warp, in (round, lane) order
+  // Stable ranks within the warp in (round, lane) order.  The lanes sharing
+  // a digit are found with one ballot per digit bit (multisplit); the leader
+  // of each group adds the group size to the warp's counter with a shared
+  // atomic (atomics of one warp to one address apply in issue order, so
+  // rounds need no barrier) and broadcasts the old value to its peers.
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = tbase + warp * (32 * ITEMS) + i * 32 + lane;
-    const bool valid = idx < n;
-    const uint32_t d = ((uint32_t)key[i] >> shift) & (BINS - 1);
-    const unsigned vm = __ballot_sync(0xffffffffu, valid);
-    const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu) & vm;
-    const uint32_t before = valid ? wcnt[warp][d] : 0u;
-    __syncwarp();
-    rank[i] = before + __popc(peers & lt);
-    if (valid && (peers & lt) == 0) wcnt[warp][d] = (uint16_t)(before + __popc(peers));
-    __syncwarp();
+    const bool valid = dig[i] != 0xffffffffu;
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
+    if (!valid) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) {
+      if (b < nbits) {
+        const bool bit = (dig[i] >> b) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+      }
+    }
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) old = atomicAdd(&wcnt[warp][dig[i]], (uint32_t)__popc(peers));
+    rank[i] = __popc(peers & lt) + __shfl_sync(0xffffffffu, old, leader);
   }
   __syncthreads();
   // per digit (thread d < 256): exclusive prefix over warps, publish, look back
+  uint32_t run = 0;
   if (threadIdx.x < BINS) {
     const int d = threadIdx.x;
-    uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
       const uint32_t c = wcnt[w][d];
-      wcnt[w][d] = (uint16_t)run;
+      wcnt[w][d] = run;
       run += c;
     }
     uint32_t* st = status + (size_t)tile * BINS + d;
@@ -150,46 +160,56 @@ __global__ void __launch_bounds__(THREADS) k_pass(const K* __restrict__ kin, K* 
       st_volatile(st, FLAG_INC | run);
     } else {
       st_volatile(st, FLAG_AGG | run);
+      // walk back over the predecessors, four status words per round trip
       int64_t t = (int64_t)tile - 1;
-      while (true) {
-        const uint32_t v = ld_volatile(status + (size_t)t * BINS + d);
-        if ((v & ~VALUE_MASK) == 0u) continue;  // predecessor not published yet
-        excl += v & VALUE_MASK;
-        if (v & FLAG_INC) break;
-        --t;
+      bool found = false;
+      while (!found) {
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[j] = t - j >= 0 ? ld_volatile(status + (size_t)(t - j) * BINS + d) : FLAG_INC;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (found) break;
+          if ((v[j] & ~VALUE_MASK) == 0u) break;  // not published yet: re-poll from here
+          excl += v[j] & VALUE_MASK;
+          --t;
+          if (v[j] & FLAG_INC) found = true;
+        }
       }
       st_volatile(st, FLAG_INC | (excl + run));
     }
     s_global[d] = bucket_base[d] + excl;
-    s_scan[d] = run;
   }
-  __syncthreads();
-  // tile-local exclusive offsets per digit (Hillis-Steele scan of the totals)
+  // tile-local exclusive offsets per digit: warp scans + one pass over warp sums
   {
-    const int d = threadIdx.x;
-    const bool on = d < BINS;
-    const uint32_t v = on ? s_scan[d] : 0u;
-    for (int off = 1; off < BINS; off <<= 1) {
-      const uint32_t t = (on && d >= off) ? s_scan[d - off] : 0u;
-      __syncthreads();
-      if (on) s_scan[d] += t;
-      __syncthreads();
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    const uint32_t incl = on ? s_scan[d] : 0u;
+    if (lane == 31) s_wsum[warp] = x;
     __syncthreads();
-    if (on) s_scan[d] = incl - v;
+    uint32_t add = 0;
+#pragma unroll
+    for (int w = 0; w < BINS / 32; ++w) add += (w < warp) ? s_wsum[w] : 0u;
+    if (threadIdx.x < BINS) s_scan[threadIdx.x] = add + x - run;
   }
   __syncthreads();
-  // reorder the tile through shared memory by digit (stable), then write runs
+  // reorder the tile through shared memory by digit (stable): keys from the
+  // digits' source registers, values straight from global
   const int tile_n = (int)min((int64_t)TILE_ITEMS, n - tbase);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = tbase + warp * (32 * ITEMS) + i * 32 + lane;
+    if (dig[i] != 0xffffffffu) rank[i] += s_scan[dig[i]] + wcnt[warp][dig[i]];
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = wbase + i * 32;
     if (idx < n) {
-      const uint32_t d = ((uint32_t)key[i] >> shift) & (BINS - 1);
-      const uint32_t pos = s_scan[d] + wcnt[warp][d] + rank[i];
-      s_keys[pos] = key[i];
-      s_vals[pos] = val[i];
+      s_keys[rank[i]] = kin[idx];
+      s_vals[rank[i]] = vin[idx];
     }
   }
   __syncthreads();
@@ -214,7 +234,9 @@ cudaError_t sort_pairs(void* tmp, size_t tmp_bytes, K* k0, K* k1, uint32_t* v0, 
   uint32_t* base = hist + passes * BINS;
   uint32_t* counters = base + passes * BINS;
   uint32_t* status = counters + 8;
-  cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(uint32_t) * (2 * (size_t)passes * BINS + 8), st);
+  // histograms, tile counters and every pass's look-back status in one memset
+  cudaError_t e = cudaMemsetAsync(
+      tmp, 0, sizeof(uint32_t) * (2 * (size_t)passes * BINS + 8 + (size_t)passes * tiles * BINS), st);
   if (e != cudaSuccess) return e;
   int hist_blocks = (int)((n + THREADS * 16 - 1) / (THREADS * 16));
   if (hist_blocks > 1184) hist_blocks = 1184;
@@ -226,10 +248,10 @@ cudaError_t sort_pairs(void* tmp, size_t tmp_bytes, K* k0, K* k1, uint32_t* v0, 
   uint32_t* vin = v0;
   uint32_t* vout = v1;
   for (int p = 0; p < passes; ++p) {
-    e = cudaMemsetAsync(status, 0, sizeof(uint32_t) * (size_t)tiles * BINS, st);
-    if (e != cudaSuccess) return e;
     k_pass<K><<<(unsigned)tiles, THREADS, 0, st>>>(kin, kout, vin, vout, n, BITS * p,
-                                                   base + p * BINS, status, counters + p);
+                                                   base + p * BINS,
+                                                   status + (size_t)p * tiles * BINS, counters + p,
+                                                   min(BITS, key_bits - BITS * p));
     *launches += 1;
     K* tk = kin; kin = kout; kout = tk;
     uint32_t* tv = vin; vin = vout; vout = tv;

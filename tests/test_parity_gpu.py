@@ -286,9 +286,9 @@ def test_full_size_tomography_parallel_view():
         check_field(getattr(g, f), getattr(rg, f), f"tomo {f}")
 
 
-def test_more_than_65536_tiles_uses_wide_keys():
-    """4400x4000 = 68750 tiles: 32-bit tile keys; lists and sampled pixels
-    still match."""
+def test_more_than_65536_tiles():
+    """4400x4000 = 68750 tiles (275 tile columns, 250 rows in the span
+    binning): lists and sampled pixels still match."""
     from paper_2412_03378_b200 import configs
     from paper_2412_03378_b200.camera import look_at
     cfg = configs.medium(n=4000, size=64, n_views=1)
@@ -343,9 +343,9 @@ def test_degenerate_inputs():
 
 @pytest.mark.parametrize("name", ["tiny", "mini_opaque", "large"])
 def test_handwritten_radix_sort_lists(name, monkeypatch):
-    """The hand-written onesweep sort (vg_radix.cu, VG_RADIX=1) produces the
-    same bit-exact tile lists as the oracle (depth sort of N keys + stable
-    tile sort of the pairs, many tiles of look-back on the large config)."""
+    """The hand-written onesweep depth sort (vg_radix.cu, VG_RADIX=1) feeds
+    the span binning the same order: bit-exact tile lists (many tiles of
+    look-back on the large config)."""
     monkeypatch.setenv("VG_RADIX", "1")
     if name == "large":
         from paper_2412_03378_b200 import configs
