@@ -44,10 +44,10 @@ struct vg_context {
   int device = 0;
   int64_t launches = 0;
   // per-Gaussian
-  Buf rec, depth, rect, count, offset, acc;
+  Buf rec, depth, rect, offset, acc;
   // per-pair (double-buffered for the radix sort)
   Buf vals0;                         // per-tile Gaussian lists (depth order), P entries
-  Buf ranges, n_act, total;
+  Buf ranges, n_act;
   Buf tord;                          // heavy-first tile launch order
   Buf span1, span2;                  // span-binning scratch (vg_span.cu)
   Buf dkey, perm, dsort_tmp;         // depth pre-sort of the Gaussians
@@ -67,7 +67,6 @@ struct vg_context {
   bool prepared = false;
   bool have_fwd = false;
   bool pending = false;          // vg_prepare_async issued, finish outstanding
-  bool use_cub = true;           // false with VG_RADIX=1: hand-written sort (A/B)
   uint32_t* perm_ptr = nullptr;  // depth order of the last prepare
   cudaEvent_t count_ready = nullptr;
   // event profiling (vg_profile)
@@ -136,12 +135,6 @@ int vg_create(vg_context** out, int32_t device) {
   VG_CUDA(cudaSetDevice(device));
   vg_context* c = new vg_context();
   c->device = device;
-  {
-    // VG_RADIX=1 selects the hand-written onesweep sort (vg_radix.cu); CUB's
-    // onesweep is the default until the hand-written one is faster
-    const char* e = getenv("VG_RADIX");
-    c->use_cub = !(e && e[0] == '1');
-  }
   // keep freed stream-ordered allocations cached in the device pool
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -169,8 +162,8 @@ void vg_destroy(vg_context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  Buf* all[] = {&c->rec,  &c->depth, &c->rect,  &c->count, &c->offset, &c->acc,
-                &c->vals0, &c->ranges, &c->n_act, &c->total, &c->tord, &c->span1,
+  Buf* all[] = {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
+                &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask};
   for (Buf* b : all)
@@ -252,7 +245,6 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   const int64_t npix = (int64_t)k.width * k.height;
   VG_TRY(ensure(c->ranges, sizeof(uint2) * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->n_act, sizeof(int) * (size_t)npix, st));
-  VG_TRY(ensure(c->total, 2 * sizeof(unsigned long long), st));
   if (k.ntx > span_max_buckets() || k.nty > span_max_buckets())
     return fail(VG_EINVAL, "image too large: at most 1024 tile rows and columns (16384 px)");
   VG_CUDA(cudaMemsetAsync(c->ranges.p, 0, sizeof(uint2) * (size_t)c->n_tiles, st));
@@ -262,8 +254,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     bool grow_acc = c->acc.bytes < accb;
     VG_TRY(ensure(c->rec, sizeof(GRec) * (size_t)n, st));
     VG_TRY(ensure(c->depth, sizeof(float) * (size_t)n, st));
-    VG_TRY(ensure(c->rect, sizeof(int4) * (size_t)n, st));
-    VG_TRY(ensure(c->count, sizeof(uint32_t) * (size_t)n, st));
+    VG_TRY(ensure(c->rect, sizeof(ushort4) * (size_t)n, st));
     VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)n, st));
     VG_TRY(ensure(c->dkey, sizeof(uint32_t) * (size_t)n, st));
     VG_TRY(ensure(c->perm, sizeof(uint32_t) * 2 * (size_t)n, st));
@@ -278,7 +269,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
-                        (int4*)c->rect.p, (uint32_t*)c->count.p, (float*)c->frame.p, st);
+                        (ushort4*)c->rect.p, (float*)c->frame.p, st);
     }
     VG_LAUNCHED(c, 1);
     // Gaussians in (float32 depth, index) order: hand-written radix sort of
@@ -290,32 +281,23 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     uint32_t* perm = ids1;
     {
       ProfScope ps(c, VG_K_SORT, st);
-      if (c->use_cub) {
-        size_t tmp = 0;
-        VG_CUDA(depth_sort_temp_bytes(n, &tmp));
-        VG_TRY(ensure(c->dsort_tmp, tmp, st));
-        VG_CUDA(depth_sort(c->dsort_tmp.p, c->dsort_tmp.bytes, (const uint32_t*)c->depth.p,
-                           (uint32_t*)c->dkey.p, ids0, ids1, n, st));
-        c->launches += 5;
-      } else {
-        VG_TRY(ensure(c->dsort_tmp, radix_temp_bytes(n, 32), st));
-        int which = 0, nl = 0;
-        VG_CUDA(radix_sort_u32(c->dsort_tmp.p, c->dsort_tmp.bytes, (uint32_t*)c->depth.p,
-                               (uint32_t*)c->dkey.p, ids0, ids1, n, 32, &which, &nl, st));
-        c->launches += nl;
-        perm = which ? ids1 : ids0;
-      }
+      VG_TRY(ensure(c->dsort_tmp, radix_temp_bytes(n, 32), st));
+      int which = 0, nl = 0;
+      VG_CUDA(radix_sort_u32(c->dsort_tmp.p, c->dsort_tmp.bytes, (uint32_t*)c->depth.p,
+                             (uint32_t*)c->dkey.p, ids0, ids1, n, 32, &which, &nl, st));
+      c->launches += nl;
+      perm = which ? ids1 : ids0;
     }
     c->perm_ptr = perm;
     // step 1 of the span binning up to the pair count (vg_span.cu)
     VG_TRY(ensure(c->span1, span_scratch1_bytes(n, k.nty), st));
     {
       ProfScope ps(c, VG_K_SCAN, st);
-      VG_CUDA(span_rows_begin(n, perm, (const uint32_t*)c->count.p, (const int4*)c->rect.p, k.nty,
-                              c->span1.p, (unsigned long long*)c->total.p, st));
+      int nl = 0;
+      VG_CUDA(span_rows_begin(n, perm, (const ushort4*)c->rect.p, k.nty, c->span1.p, &nl, st));
+      VG_LAUNCHED(c, nl);
     }
-    VG_LAUNCHED(c, 3);
-    VG_CUDA(cudaMemcpyAsync(c->total_host, c->total.p, 2 * sizeof(unsigned long long),
+    VG_CUDA(cudaMemcpyAsync(c->total_host, span_info(c->span1.p), 2 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, st));
     VG_CUDA(cudaEventRecord(c->count_ready, st));
   }
@@ -350,10 +332,9 @@ int vg_prepare_finish(vg_context* c, void* stream) {
     // step 2: row spans -> per-tile lists, tile ranges, heavy-tiles-first order
     ProfScope ps(c, VG_K_DUPLICATE, st);
     int nl = 0;
-    VG_CUDA(span_finish(n, c->perm_ptr, (const uint32_t*)c->count.p, (const int4*)c->rect.p,
-                        k.ntx, k.nty, c->span1.p, P > 0 ? chunks2 : 0, c->span2.p,
-                        (uint2*)c->ranges.p, (uint32_t*)c->tord.p, (uint32_t*)c->vals0.p, &nl,
-                        st));
+    VG_CUDA(span_finish(n, c->perm_ptr, (const ushort4*)c->rect.p, k.ntx, k.nty, c->span1.p,
+                        P > 0 ? chunks2 : 0, c->span2.p, (uint2*)c->ranges.p,
+                        (uint32_t*)c->tord.p, (uint32_t*)c->vals0.p, &nl, st));
     VG_LAUNCHED(c, nl);
   }
   c->vals = P > 0 ? (uint32_t*)c->vals0.p : nullptr;

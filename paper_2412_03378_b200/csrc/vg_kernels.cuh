@@ -32,9 +32,7 @@ struct BwdIO {
 };
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st);
-void launch_total(int64_t n, const uint32_t* count, const uint32_t* offset, uint64_t* total,
-                  cudaStream_t st);
+                       float* depth, ushort4* rect, float* frame, cudaStream_t st);
 // vmask (optional): per-warp bit rows of vm_words words marking the list
 // entries where the forward saw a visible pixel (the backward's work list).
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
@@ -61,10 +59,6 @@ void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const f
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const vg_grads& g, cudaStream_t st);
 
-// depth sort of the Gaussians (CUB onesweep, vg_sort.cu)
-cudaError_t depth_sort_temp_bytes(int64_t n, size_t* bytes);
-cudaError_t depth_sort(void* tmp, size_t tmp_bytes, const uint32_t* keys_in, uint32_t* keys_out,
-                       const uint32_t* ids_in, uint32_t* ids_out, int64_t n, cudaStream_t st);
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
 // hand-written onesweep radix sort (vg_radix.cu); result buffer in *which
 size_t radix_temp_bytes(int64_t n, int key_bits);
@@ -75,17 +69,16 @@ cudaError_t radix_sort_u16(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* 
                            uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
                            cudaStream_t st);
 // span binning (vg_span.cu): per-tile lists in depth order without a pair sort.
-// begin (before the host sync): step-1 counts; info = {pairs, step-2 chunks}.
+// begin (before the host sync): step-1 counts; span_info(scratch1) = {pairs, step-2 chunks}.
 int span_max_buckets();
 cudaError_t span_configure();
 size_t span_scratch1_bytes(int64_t n, int nty);
-cudaError_t span_rows_begin(int64_t n, const uint32_t* perm, const uint32_t* count,
-                            const int4* rect, int nty, void* scratch1,
-                            unsigned long long* info, cudaStream_t st);
+cudaError_t span_rows_begin(int64_t n, const uint32_t* perm, const ushort4* rect, int nty,
+                            void* scratch1, int* launches, cudaStream_t st);
+const unsigned long long* span_info(const void* scratch1);
 size_t span_scratch2_bytes(int64_t chunks2, int ntx, int n_tiles);
-cudaError_t span_finish(int64_t n, const uint32_t* perm, const uint32_t* count, const int4* rect,
-                        int ntx, int nty, const void* scratch1, int64_t chunks2, void* scratch2,
-                        uint2* ranges, uint32_t* order, uint32_t* vals, int* launches,
-                        cudaStream_t st);
+cudaError_t span_finish(int64_t n, const uint32_t* perm, const ushort4* rect, int ntx, int nty,
+                        void* scratch1, int64_t chunks2, void* scratch2, uint2* ranges,
+                        uint32_t* order, uint32_t* vals, int* launches, cudaStream_t st);
 
 }  // namespace vg

@@ -14,8 +14,7 @@ namespace vg {
 struct PrepOut {
   GRec* rec;
   float* depth;        // sort key (float32 view depth)
-  int4* rect;          // tile rectangle x0, y0, x1, y1 (inclusive)
-  uint32_t* count;     // tiles overlapped (0 = not binned)
+  ushort4* rect;       // tile rectangle x0, y0, x1, y1 (inclusive); x1 < x0: not binned
   float* frame;        // e1, e2, e3 in whitened-local coordinates (12 floats)
 };
 
@@ -31,7 +30,7 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   Frame f;
   bool ok = make_frame(c, means + 3 * i, scales + 3 * i, rots + 4 * i, f);
   uint32_t cnt = 0;
-  int4 rect = make_int4(0, 0, -1, -1);
+  ushort4 rect = make_ushort4(1, 0, 0, 0);
   double kappa = kappa_of((double)thetas[i], f.s, nullptr, nullptr);
   if (ok) {
     // --- EWA screen covariance (raster.py:175-209) or orthographic projection
@@ -85,11 +84,11 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
       double fx1 = fmin(fmax(floor((u + r) / TILE), 0.0), (double)(c.ntx - 1));
       double fy0 = fmin(fmax(floor((v - r) / TILE), 0.0), (double)(c.nty - 1));
       double fy1 = fmin(fmax(floor((v + r) / TILE), 0.0), (double)(c.nty - 1));
-      rect = make_int4((int)fx0, (int)fy0, (int)fx1, (int)fy1);
-      cnt = (uint32_t)((rect.z - rect.x + 1) * (rect.w - rect.y + 1));
+      rect = make_ushort4((unsigned short)fx0, (unsigned short)fy0, (unsigned short)fx1,
+                          (unsigned short)fy1);
+      cnt = (uint32_t)(rect.z - rect.x + 1) * (uint32_t)(rect.w - rect.y + 1);
     }
   }
-  o.count[i] = cnt;
   o.rect[i] = rect;
   o.depth[i] = (float)f.v[2];
   if (!cnt) return;
@@ -141,9 +140,9 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
 }
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, int4* rect, uint32_t* count, float* frame, cudaStream_t st) {
+                       float* depth, ushort4* rect, float* frame, cudaStream_t st) {
   if (n <= 0) return;
-  PrepOut o{rec, depth, rect, count, frame};
+  PrepOut o{rec, depth, rect, frame};
   int blocks = (int)((n + 255) / 256);
   k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
                                        s.sh, c, bin_cut, o);

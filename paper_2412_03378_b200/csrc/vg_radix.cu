@@ -26,7 +26,10 @@ constexpr int BITS = 8;
 constexpr int BINS = 256;
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr int ITEMS = 16;                     // per thread
+#ifndef VG_RADIX_ITEMS
+#define VG_RADIX_ITEMS 16
+#endif
+constexpr int ITEMS = VG_RADIX_ITEMS;          // per thread
 constexpr int TILE_ITEMS = THREADS * ITEMS;   // 4096
 constexpr uint32_t FLAG_AGG = 1u << 30;
 constexpr uint32_t FLAG_INC = 2u << 30;

@@ -54,17 +54,21 @@ class ViewShardedStep:
     """One training step of the analytic rasterizer over a camera set, on
     this rank's share of the views.
 
-    Two device contexts (engine.Engine) alternate between views: view v+1's
-    binning front half (projection, depth sort, pair-count scan) is enqueued
-    before view v's blend kernels, so the one host wait of the pipeline (the
-    pair count that sizes the sort) never leaves the GPU idle.  Both contexts
-    defer the float64 parameter chain, which runs once per step per context
-    (vg_finalize_grads adds both into the same flat buffer)."""
+    Two device contexts (engine.Engine) alternate between views, and the
+    binning of view v+1 (projection, depth sort, span binning) runs on a
+    high-priority side stream while view v's blend kernels run on the main
+    stream: the binning kernels are latency-bound and fill the issue slots
+    the compute-bound blend kernels leave free, and the one host wait of the
+    pipeline (the pair count that sizes the lists) happens while the GPU is
+    busy.  Both contexts defer the float64 parameter chain, which runs once
+    per step per context (vg_finalize_grads adds both into the same flat
+    buffer)."""
 
     def __init__(self, engine, dscene, cameras, targets, *, world=1, rank=0, tomography=False,
                  parallel=False, extent=1.6, group=None, pipeline=True):
         import torch
         from .engine import Engine
+        self.torch = torch
         self.eng = engine
         self.engines = [engine]
         if pipeline:
@@ -80,16 +84,35 @@ class ViewShardedStep:
         self.grads = engine.new_grads(dscene)
         self.loss = torch.zeros((), dtype=torch.float64, device=engine.device)
         self.ready = None
+        dev = engine.device
+        # binning stream: high priority so its short CTAs interleave with the blend kernels
+        import os
+        prio = int(os.environ.get("VG_SIDE_PRIORITY", "-1"))
+        self.side = torch.cuda.Stream(device=dev, priority=prio) if pipeline else None
+        self.ev_binned = [torch.cuda.Event() for _ in self.engines]
+        self.ev_free = [torch.cuda.Event() for _ in self.engines]
 
-    def _begin(self, eng, v):
+    def _bin(self, i, v):
+        """Bin view v on context i (side stream when pipelining)."""
+        eng = self.engines[i]
         kw = dict(tomo=True, parallel=self.parallel, extent=self.extent) if self.tomo else {}
-        eng.prepare_async(self.ds, self.cams[v], **kw)
+        if self.side is None:
+            eng.prepare(self.ds, self.cams[v], **kw)
+            return
+        with self.torch.cuda.stream(self.side):
+            eng.prepare_async(self.ds, self.cams[v], **kw)
+            eng.prepare_finish()                    # host waits for the pair count only
+            self.ev_binned[i].record(self.side)
 
-    def _blend(self, eng, v):
+    def _blend(self, i, v):
         from ._lib import VG_DEFER
+        eng = self.engines[i]
+        main = self.torch.cuda.current_stream(eng.device)
+        if self.side is not None:
+            main.wait_event(self.ev_binned[i])
         if self.ready is not None and v in self.ready:
             # the target of this view is still streaming in on a copy stream
-            eng.torch.cuda.current_stream(eng.device).wait_event(self.ready[v])
+            main.wait_event(self.ready[v])
         if self.tomo:
             img = eng.tomo_forward()
             eng.tomo_backward_l2(img, self.targets[v], self.grads, accumulate=VG_DEFER,
@@ -98,6 +121,8 @@ class ViewShardedStep:
             color, tfin, _ = eng.forward()
             eng.backward_l2(color, tfin, self.targets[v], self.grads, accumulate=VG_DEFER,
                             loss=self.loss)
+        if self.side is not None:
+            self.ev_free[i].record(main)            # context i may be re-binned after this
 
     def _run_views(self):
         views = self.views
@@ -105,21 +130,20 @@ class ViewShardedStep:
         self._used = set()
         if not views:
             return
-        engs = self.engines
-        self._used = {0} | ({1} if len(views) > 1 and len(engs) > 1 else set())
-        self._begin(engs[0], views[0])
-        engs[0].prepare_finish()
+        ne = len(self.engines)
+        self._used = set(range(min(ne, len(views))))
+        if self.side is not None:
+            # the scene (and zeroed buffers) come from the main stream
+            self.side.wait_stream(self.torch.cuda.current_stream(self.eng.device))
+        self._bin(0, views[0])
         for j, v in enumerate(views):
-            cur = engs[j % len(engs)]
-            nxt = engs[(j + 1) % len(engs)]
-            last = j + 1 >= len(views)
-            if not last and nxt is not cur:
-                self._begin(nxt, views[j + 1])       # enqueued before this view's blend
-            self._blend(cur, v)
-            if not last:
-                if nxt is cur:
-                    self._begin(nxt, views[j + 1])
-                nxt.prepare_finish()                 # its count is already on the host
+            cur = j % ne
+            self._blend(cur, v)                     # enqueued before the host waits below
+            if j + 1 < len(views):
+                nxt = (j + 1) % ne
+                if self.side is not None and j >= 1:
+                    self.side.wait_event(self.ev_free[nxt])   # its previous view is done
+                self._bin(nxt, views[j + 1])
 
     def _finish(self):
         for i in sorted(getattr(self, "_used", ())):

@@ -342,11 +342,10 @@ def test_degenerate_inputs():
 
 
 @pytest.mark.parametrize("name", ["tiny", "mini_opaque", "large"])
-def test_handwritten_radix_sort_lists(name, monkeypatch):
-    """The hand-written onesweep depth sort (vg_radix.cu, VG_RADIX=1) feeds
-    the span binning the same order: bit-exact tile lists (many tiles of
-    look-back on the large config)."""
-    monkeypatch.setenv("VG_RADIX", "1")
+def test_depth_sort_and_span_lists(name):
+    """The hand-written onesweep depth sort (vg_radix.cu) and the span
+    binning (vg_span.cu) give bit-exact tile lists and tile starts (many
+    tiles of look-back, 68 x 120 tiles on the large config)."""
     if name == "large":
         from paper_2412_03378_b200 import configs
         cfg = configs.large()
