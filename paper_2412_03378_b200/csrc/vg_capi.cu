@@ -52,7 +52,9 @@ struct vg_context {
   Buf span1, span2;                  // span-binning scratch (vg_span.cu)
   Buf dkey, perm, dsort_tmp;         // depth pre-sort of the Gaussians
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
-  Buf cacc;                          // colour / SH gradient accumulators, SoA [3|48][N]
+  Buf cacc;                          // RGB gradient accumulators, SoA [3][N]
+  Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
+  int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
@@ -165,7 +167,7 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
-                &c->cacc, &c->vmask};
+                &c->cacc, &c->vmask, &c->dcol, &c->centers};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -236,6 +238,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   cudaStream_t st = (cudaStream_t)stream;
   VG_CUDA(cudaSetDevice(c->device));
   const int64_t n = s->n;
+  if (n != c->scene.n) c->sh_views = 0;  // pending SH slabs belong to another scene
   c->scene = *s;
   c->cam = k;
   c->opt = *opt;
@@ -263,7 +266,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
       VG_TRY(ensure(c->lacc, sizeof(float) * 12 * (size_t)n, st, true));
     VG_TRY(ensure(c->frame, sizeof(float) * 12 * (size_t)n, st));
     {
-      const size_t cb = sizeof(float) * (s->sh ? 48 : 3) * (size_t)n;
+      const size_t cb = sizeof(float) * 3 * (size_t)n;
       if (c->cacc.bytes < cb) VG_TRY(ensure(c->cacc, cb, st, true));
     }
     {
@@ -492,23 +495,54 @@ static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
 // After a backward blend: rotate this view's accumulators into the
 // view-independent ones (and add colour / SH gradients), then -- unless the
 // caller defers -- run the float64 parameter chain.
+// Grow a buffer to at least `bytes`, keeping its contents (stream ordered).
+static int grow_keep(Buf& b, size_t bytes, cudaStream_t st) {
+  if (b.bytes >= bytes && b.p) return VG_OK;
+  size_t want = bytes * 2 + 256;
+  void* p = nullptr;
+  VG_CUDA(cudaMallocAsync(&p, want, st));
+  if (b.p) {
+    VG_CUDA(cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, st));
+    VG_CUDA(cudaFreeAsync(b.p, st));
+  }
+  b.p = p;
+  b.bytes = want;
+  return VG_OK;
+}
+
+static int run_param_chain(vg_context* c, const vg_grads& g, cudaStream_t st) {
+  int k = 0;
+  {
+    ProfScope ps(c, VG_K_FINALIZE, st);
+    k = launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p,
+                               (const float*)c->dcol.p, (const double*)c->centers.p, c->sh_views,
+                               g, st);
+  }
+  c->sh_views = 0;
+  VG_LAUNCHED(c, k);
+  return VG_OK;
+}
+
 static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
   const int64_t n = c->scene.n;
   if (n <= 0) return VG_OK;
+  float* dcol = nullptr;
+  double* center = nullptr;
+  if (c->scene.sh) {
+    const int v = c->sh_views;
+    VG_TRY(grow_keep(c->dcol, sizeof(float) * 3 * (size_t)n * (size_t)(v + 1), st));
+    VG_TRY(grow_keep(c->centers, sizeof(double) * 3 * (size_t)(v + 1), st));
+    dcol = (float*)c->dcol.p + (size_t)v * 3 * (size_t)n;
+    center = (double*)c->centers.p + 3 * v;
+    c->sh_views = v + 1;
+  }
   {
     ProfScope ps(c, VG_K_FINALIZE, st);
     launch_view_accumulate(n, c->scene, c->cam, (const float*)c->frame.p, (float*)c->acc.p,
-                           (float*)c->lacc.p, (float*)c->cacc.p, st);
+                           (float*)c->lacc.p, (float*)c->cacc.p, dcol, center, st);
   }
   VG_LAUNCHED(c, 1);
-  if (g->accumulate != VG_DEFER) {
-    int k = 0;
-    {
-      ProfScope ps(c, VG_K_FINALIZE, st);
-      k = launch_finalize_params(n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p, *g, st);
-    }
-    VG_LAUNCHED(c, k);
-  }
+  if (g->accumulate != VG_DEFER) VG_TRY(run_param_chain(c, *g, st));
   return VG_OK;
 }
 
@@ -518,14 +552,7 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   vg_grads gg = *g;
   gg.accumulate = g->accumulate == VG_OVERWRITE ? VG_OVERWRITE : VG_ADD;
   cudaStream_t st = (cudaStream_t)stream;
-  if (c->scene.n > 0) {
-    int k = 0;
-    {
-      ProfScope ps(c, VG_K_FINALIZE, st);
-      k = launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p, gg, st);
-    }
-    VG_LAUNCHED(c, k);
-  }
+  if (c->scene.n > 0) VG_TRY(run_param_chain(c, gg, st));
   return VG_OK;
 }
 

@@ -10,8 +10,12 @@
 //   with rho = W r (closest-approach offset, whitened) and w^ = W d / |W d|.
 //   The e-frame (stored by preprocess) is view dependent; rotating A and B
 //   into the Gaussian's whitened-LOCAL frame makes them view independent, so
-//   they are summed over views in a per-context accumulator.  Colour / SH
-//   gradients are linear and view specific and go straight to the outputs.
+//   they are summed over views in a per-context accumulator.  RGB colour
+//   gradients are summed the same way.  With SH colour the pull-back onto the
+//   16 x 3 coefficients depends on the view direction, so each view only
+//   stores its 3-float dL/dRGB (a slab per view) and k_sh_pull folds all the
+//   views of the step in one pass (48 register accumulators per Gaussian)
+//   instead of a 384-byte read-modify-write per Gaussian and view.
 //
 // (b) k_finalize_params, once per step (float64): because
 //   g_expo = -1/2 dL/de e = -1/2 kappa sqrt(2 pi) h, the envelope form of
@@ -34,7 +38,9 @@ struct ViewAccIn {
   const float* frame;    // n * 12: e1, e2, e3 (whitened-local), pad
   float* acc;            // n * 16 per-view accumulators (zeroed here)
   float* lacc;           // n * 12 view-independent accumulators
-  float* cacc;           // [3 or 48][n] colour / SH gradient accumulators (SoA: coalesced)
+  float* cacc;           // [3][n] RGB gradient accumulators (SoA: coalesced)
+  float* dcol;           // SH scenes: this view's dL/dRGB slab [3][n]
+  double* center;        // SH scenes: this view's camera centre (written by thread 0)
 };
 
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
@@ -51,6 +57,17 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   bool any = false;
 #pragma unroll
   for (int k = 0; k < 13; ++k) any |= raw[k] != 0.f;
+  const int64_t n = in.n;
+  if (in.dcol) {
+    if (i == 0) {
+      in.center[0] = c.center[0];
+      in.center[1] = c.center[1];
+      in.center[2] = c.center[2];
+    }
+    in.dcol[i] = raw[10];
+    in.dcol[n + i] = raw[11];
+    in.dcol[2 * n + i] = raw[12];
+  }
   if (!any) return;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   a4[0] = z; a4[1] = z; a4[2] = z; a4[3] = z;
@@ -75,30 +92,55 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   l1.x += Al[4]; l1.y += Al[5]; l1.z += Bl[0]; l1.w += Bl[1];
   l2.x += Bl[2]; l2.y += raw[9];
   l4[0] = l0; l4[1] = l1; l4[2] = l2;
-  // colour: dL/dRGB of this view, or its SH pull-back (DC band basis = 1)
-  const float dc[3] = {raw[10], raw[11], raw[12]};
-  if (dc[0] == 0.f && dc[1] == 0.f && dc[2] == 0.f) return;
-  const int64_t n = in.n;
-  if (!in.sh) {
-    in.cacc[i] += dc[0];
-    in.cacc[n + i] += dc[1];
-    in.cacc[2 * n + i] += dc[2];
-    return;
-  }
-  double d[3] = {in.means[3 * i] - c.center[0], in.means[3 * i + 1] - c.center[1],
-                 in.means[3 * i + 2] - c.center[2]};
-  const double dn = sqrt(dot3(d, d));
-  d[0] /= dn; d[1] /= dn; d[2] /= dn;
-  double b[16];
-  sh_basis(d, b);
+  // colour: dL/dRGB of this view (SH scenes: deferred to k_sh_pull)
+  if (in.dcol) return;
+  if (raw[10] != 0.f) in.cacc[i] += raw[10];
+  if (raw[11] != 0.f) in.cacc[n + i] += raw[11];
+  if (raw[12] != 0.f) in.cacc[2 * n + i] += raw[12];
+}
+
+// SH pull-back of the step's views: d_sh[i][l][ch] (+)= sum_v b_l(d_v) dRGB_v[ch]
+// with d_v = normalize(mean_i - centre_v) and the real SH basis of
+// vg_common.cuh (DC band basis = 1).  One thread per Gaussian, 48 register
+// accumulators, the per-view slabs read coalesced.
+__global__ void __launch_bounds__(128) k_sh_pull(int64_t n, const float* __restrict__ means,
+                                                 const float* __restrict__ dcol,
+                                                 const double* __restrict__ centers, int nviews,
+                                                 float* __restrict__ d_sh, int add) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc[48];
 #pragma unroll
-  for (int l = 0; l < 16; ++l) {
-    const float bl = (float)b[l];
+  for (int k = 0; k < 48; ++k) acc[k] = 0.f;
+  const double m[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+  bool any = false;
+  for (int v = 0; v < nviews; ++v) {
+    const float* sl = dcol + (size_t)v * 3 * n;
+    const float dc[3] = {sl[i], sl[n + i], sl[2 * n + i]};
+    if (dc[0] == 0.f && dc[1] == 0.f && dc[2] == 0.f) continue;
+    any = true;
+    double d[3] = {m[0] - centers[3 * v], m[1] - centers[3 * v + 1], m[2] - centers[3 * v + 2]};
+    const double dn = sqrt(dot3(d, d));
+    d[0] /= dn; d[1] /= dn; d[2] /= dn;
+    double b[16];
+    sh_basis(d, b);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float* o = in.cacc + (int64_t)(3 * l + ch) * n + i;
-      *o = fmaf(bl, dc[ch], *o);
+    for (int l = 0; l < 16; ++l) {
+      const float bl = (float)b[l];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) acc[3 * l + ch] = fmaf(bl, dc[ch], acc[3 * l + ch]);
     }
+  }
+  if (!any && add) return;
+  float4* o = reinterpret_cast<float4*>(d_sh + 48 * i);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    float4 v = make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+    if (add) {
+      const float4 u = o[k];
+      v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
+    }
+    o[k] = v;
   }
 }
 
@@ -221,13 +263,15 @@ __global__ void __launch_bounds__(128) k_finalize_params(FinalIn in, vg_grads g)
 }
 
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
-                            float* acc, float* lacc, float* cacc, cudaStream_t st) {
+                            float* acc, float* lacc, float* cacc, float* dcol, double* center,
+                            cudaStream_t st) {
   if (n <= 0) return;
-  ViewAccIn in{n, s.means, s.sh, frame, acc, lacc, cacc};
+  ViewAccIn in{n, s.means, s.sh, frame, acc, lacc, cacc, dcol, center};
   k_view_accumulate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, c);
 }
 
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
+                           const float* dcol, const double* centers, int sh_views,
                            const vg_grads& g, cudaStream_t st) {
   if (n <= 0) return 0;
   FinalIn in{n, s.scales, s.rotations, s.thetas, lacc};
@@ -235,7 +279,9 @@ int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cac
   const unsigned blocks = (unsigned)((n + 31) / 32);
   const int add = g.accumulate != 0;
   if (s.sh) {
-    k_color_out<48><<<blocks, 256, 0, st>>>(n, cacc, g.d_sh, add);
+    if (g.d_sh)
+      k_sh_pull<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, s.means, dcol, centers, sh_views,
+                                                            g.d_sh, add);
     // d_colors (dL/d evaluated RGB) is not tracked separately for SH scenes
     if (g.d_colors && !add) cudaMemsetAsync(g.d_colors, 0, sizeof(float) * 3 * (size_t)n, st);
   } else {

@@ -53,10 +53,13 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
                      const float* d_image,
                      const float* image, const float* target, float loss_scale, double* loss_sum,
                      float* acc, uint8_t* visible, cudaStream_t st);
+// SH scenes: dcol / center receive this view's dL/dRGB slab [3][n] and camera centre
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
-                            float* acc, float* lacc, float* cacc, cudaStream_t st);
-// returns the number of kernels launched
+                            float* acc, float* lacc, float* cacc, float* dcol, double* center,
+                            cudaStream_t st);
+// returns the number of kernels launched; SH scenes fold the sh_views slabs of dcol
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
+                           const float* dcol, const double* centers, int sh_views,
                            const vg_grads& g, cudaStream_t st);
 
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
