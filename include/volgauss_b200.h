@@ -149,7 +149,10 @@ int vg_pair_count(vg_context* ctx, int64_t* out_pairs);
 int vg_tile_lists(vg_context* ctx, int32_t* prims, int32_t* offsets, void* stream);
 
 /* raster.render (raster.py:410-439), analytic mode: color (H,W,3),
- * final_transmittance (H,W), n_contrib (H,W). */
+ * final_transmittance (H,W), n_contrib (H,W).  n_contrib may be NULL: the
+ * per-pixel counts (n_contrib and the active-entry counts of vg_n_active) are
+ * then not computed -- the training-step forward; the backward does not need
+ * them. */
 int vg_render_forward(vg_context* ctx, float* color, float* final_t, int32_t* n_contrib,
                       void* stream);
 

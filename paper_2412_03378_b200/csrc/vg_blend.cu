@@ -331,7 +331,10 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
 
 __device__ unsigned long long g_vg_stats[4];  // debug: processed / visible warp-entries, list entries
 
-template <bool STOP, bool CUT, bool STATS = false>
+// COUNTS: also produce n_contrib and n_active (the render API and the
+// roofline statistics); the training step's forward skips them -- the
+// backward re-derives activity from its own transmittance replay.
+template <bool STOP, bool CUT, bool STATS = false, bool COUNTS = true>
 __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
@@ -383,17 +386,21 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
           const bool a0 = lo(T) >= p.stop, a1 = hi(T) >= p.stop;
           fl0 = a0 ? p.cc : 1.f;
           fl1 = a1 ? p.cc : 1.f;
-          na0 = a0 ? jb + k : na0;
-          na1 = a1 ? jb + k : na1;
+          if (COUNTS) {
+            na0 = a0 ? jb + k : na0;
+            na1 = a1 ? jb + k : na1;
+          }
         }
         float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
         if (CUT) {
           const bool c0 = om0 > p.omcut, c1 = om1 > p.omcut;
           om0 = c0 ? 1.f : om0;
           om1 = c1 ? 1.f : om1;
-          nc0 += c0 ? 0 : 1;
-          nc1 += c1 ? 0 : 1;
-        } else {
+          if (COUNTS) {
+            nc0 += c0 ? 0 : 1;
+            nc1 += c1 ? 0 : 1;
+          }
+        } else if (COUNTS) {
           nc0 += om0 < 1.f;
           nc1 += om1 < 1.f;
         }
@@ -454,8 +461,10 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
     color[3 * pix + 1] = fmaf(t0, p.bg[1], lo(Cg));
     color[3 * pix + 2] = fmaf(t0, p.bg[2], lo(Cb));
     final_t[pix] = t0;
-    n_contrib[pix] = nc0;
-    n_act[pix] = na0;
+    if (COUNTS) {
+      n_contrib[pix] = nc0;
+      n_act[pix] = na0;
+    }
   }
   if (G.in1) {
     const int pix = G.row1 * p.width + G.col;
@@ -463,8 +472,10 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
     color[3 * pix + 1] = fmaf(t1, p.bg[1], hi(Cg));
     color[3 * pix + 2] = fmaf(t1, p.bg[2], hi(Cb));
     final_t[pix] = t1;
-    n_contrib[pix] = nc1;
-    n_act[pix] = na1;
+    if (COUNTS) {
+      n_contrib[pix] = nc1;
+      n_act[pix] = na1;
+    }
   }
 }
 
@@ -507,12 +518,12 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
 // forward did, advance T and the running suffix, form dL/de for live pixels,
 // and flush the warp's 13 accumulator sums for this Gaussian.
 template <bool CUT>
-__device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, int j,
-                                          const int (&nav)[2], F2 dcr, F2 dcg, F2 dcb, F2 tot,
-                                          const BlendParams& p, F2& T, F2& P, int lane,
-                                          const BwdIO& io) {
-  // inactive entries (j >= n_act) get a floor of 1: alpha = 0, no change
-  const bool act0 = j < nav[0], act1 = j < nav[1];
+__device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in0, bool in1,
+                                          F2 dcr, F2 dcg, F2 dcb, F2 tot, const BlendParams& p,
+                                          F2& T, F2& P, int lane, const BwdIO& io) {
+  // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
+  // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
+  const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
   float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
   float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
   // cut: skipped below alpha_cut (raster.py:363-365) or inactive
@@ -554,21 +565,18 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, int j,
 // L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
 template <int LOSS>
 __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo& G, const BwdIO& io,
-                                             float (&dcv)[2][3], float (&totv)[2], int (&nav)[2],
-                                             int* s_maxna) {
+                                             float (&dcv)[2][3], float (&totv)[2]) {
   float Tfv[2] = {1.f, 1.f};
   double lossv = 0.0;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     dcv[q][0] = dcv[q][1] = dcv[q][2] = 0.f;
     totv[q] = 0.f;
-    nav[q] = 0;
     const bool in = q ? G.in1 : G.in0;
     if (!in) continue;
     const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
     const float cc0 = io.color[3 * pix], cc1 = io.color[3 * pix + 1], cc2 = io.color[3 * pix + 2];
     Tfv[q] = io.final_t[pix];
-    nav[q] = io.n_act[pix];
     float dT = 0.f;
     if (LOSS == 0) {
       dcv[q][0] = io.d_color[3 * pix];
@@ -586,8 +594,6 @@ __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo
     totv[q] = fmaf(dcv[q][0], cc0, fmaf(dcv[q][1], cc1, fmaf(dcv[q][2], cc2, dT * Tfv[q])));
   }
   __syncthreads();
-  const int my_na = max(nav[0], nav[1]);
-  if (my_na && s_maxna) atomicMax(s_maxna, my_na);
   block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
               dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
               LOSS ? io.loss_sum : nullptr);
@@ -607,7 +613,6 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
                                                    int vm_words) {
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
-  __shared__ int s_maxna;
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -617,29 +622,26 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
   const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
   float dcv[2][3], totv[2];
-  int nav[2];
-  if (threadIdx.x == 0) s_maxna = 0;
-  bwd_prologue<LOSS>(p, G, io, dcv, totv, nav, &s_maxna);
-  int warp_na = max(nav[0], nav[1]);
-  for (int o = 16; o; o >>= 1) warp_na = max(warp_na, __shfl_xor_sync(FULL, warp_na, o));
-  const uint32_t end = r.x + (uint32_t)s_maxna;
+  bwd_prologue<LOSS>(p, G, io, dcv, totv);
   const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
            dcb = f2(dcv[0][2], dcv[1][2]);
   const F2 tot = f2(totv[0], totv[1]);
-  F2 T = f2s(1.f), P = f2s(0.f);
-  for (uint32_t base = r.x; base < end; base += BATCH) {
-    __syncthreads();
+  // the replay follows the forward exactly: same entries, same order, same
+  // transmittance (so the same activity and the same early exits)
+  F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f), P = f2s(0.f);
+  bool done = !(G.in0 || G.in1);
+  for (uint32_t base = r.x; base < r.y; base += BATCH) {
+    if (__syncthreads_count(done) == NT) break;
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
-      if (i < end) {
+      if (i < r.y) {
         const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
         if (!vmask) smask[sidx] = (uint8_t)m;
       }
     }
     __syncthreads();
-    const int jb = (int)(base - r.x);
-    const int nb = min(min((int)BATCH, (int)(end - base)), warp_na - jb);
-    for (int c = 0; c < nb; c += 32) {
+    const int nb = min((uint32_t)BATCH, r.y - base);
+    for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
       unsigned bits;
       if (vmask) {
         // exact: the entries where the forward saw a visible pixel in this block
@@ -665,12 +667,13 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
           bits &= bits - 1;
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
-          bwd_entry<CUT>(s, e, jb + k, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
-          bwd_entry<CUT>(sb, eb, jb + kb, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
         } else {
-          bwd_entry<CUT>(s, e, jb + k, nav, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
         }
       }
+      done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);
     }
   }
 }
@@ -842,9 +845,18 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
                        int vm_words, cudaStream_t st) {
+  // n_contrib == NULL: the training-step forward (no counts)
 #define VG_RF(S, C)                                                                             \
-  k_render_fwd<S, C><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color, final_t,       \
-                                             n_contrib, n_act, vmask, vm_words)
+  do {                                                                                          \
+    if (n_contrib)                                                                              \
+      k_render_fwd<S, C, false, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color, \
+                                                               final_t, n_contrib, n_act, vmask, \
+                                                               vm_words);                       \
+    else                                                                                        \
+      k_render_fwd<S, C, false, false><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p,      \
+                                                                color, final_t, nullptr, nullptr, \
+                                                                vmask, vm_words);                \
+  } while (0)
   if (stop && cut) VG_RF(true, true);
   else if (stop) VG_RF(true, false);
   else if (cut) VG_RF(false, true);

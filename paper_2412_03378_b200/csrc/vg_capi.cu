@@ -68,6 +68,7 @@ struct vg_context {
   uint32_t* vals = nullptr;
   bool prepared = false;
   bool have_fwd = false;
+  bool have_counts = false;      // the last forward produced n_contrib / n_active
   bool pending = false;          // vg_prepare_async issued, finish outstanding
   uint32_t* perm_ptr = nullptr;  // depth order of the last prepare
   cudaEvent_t count_ready = nullptr;
@@ -431,7 +432,7 @@ static BlendParams blend_params(const vg_context* c) {
 
 int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_contrib,
                       void* stream) {
-  if (!c || !color || !final_t || !n_contrib) return fail(VG_EINVAL, "vg_render_forward: NULL argument");
+  if (!c || !color || !final_t) return fail(VG_EINVAL, "vg_render_forward: NULL argument");
   if (!c->prepared) return fail(VG_EINVAL, "vg_render_forward: call vg_prepare first");
   if (c->cam.projection != VG_PINHOLE) return fail(VG_EINVAL, "render needs a pinhole camera");
   cudaStream_t st = (cudaStream_t)stream;
@@ -458,6 +459,7 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   }
   VG_LAUNCHED(c, 1);
   c->have_fwd = true;
+  c->have_counts = n_contrib != nullptr;
   return VG_OK;
 }
 
@@ -474,7 +476,8 @@ int vg_debug_forward_stats(vg_context* c, float* color, float* final_t, int32_t*
 
 int vg_n_active(vg_context* c, int32_t* out, void* stream) {
   if (!c || !out) return fail(VG_EINVAL, "vg_n_active: NULL argument");
-  if (!c->have_fwd) return fail(VG_EINVAL, "vg_n_active: no forward on this context");
+  if (!c->have_fwd || !c->have_counts)
+    return fail(VG_EINVAL, "vg_n_active: no counting forward (n_contrib != NULL) on this context");
   size_t bytes = sizeof(int32_t) * (size_t)c->cam.width * (size_t)c->cam.height;
   VG_CUDA(cudaMemcpyAsync(out, c->n_act.p, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return VG_OK;
@@ -568,7 +571,6 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
   BwdIO io;
   io.color = color;
   io.final_t = final_t;
-  io.n_act = (const int*)c->n_act.p;
   io.d_color = d_color;
   io.d_t = d_t;
   io.target = target;

@@ -20,7 +20,6 @@ struct BlendParams {
 struct BwdIO {
   const float* color;
   const float* final_t;
-  const int* n_act;
   const float* d_color;     // explicit upstream gradient (LOSS == 0)
   const float* d_t;         // optional dL/dT_final (LOSS == 0)
   const float* target;      // fused L2 (LOSS == 1)

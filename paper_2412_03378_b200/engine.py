@@ -73,12 +73,14 @@ class Engine:
     def prepare_finish(self):
         _lib.check(self.lib.vg_prepare_finish(self.ctx.handle, self.stream()), "vg_prepare_finish")
 
-    def forward(self, slot=0):
+    def forward(self, slot=0, counts=True):
+        """Forward blend -> (color, final_T, n_contrib).  counts=False skips
+        the per-pixel counts (n_contrib is then None): the training step."""
         H, W = int(self.cam.height), int(self.cam.width)
         t = self.torch
         color = self._buf(("color", slot), (H, W, 3), t.float32)
         tfin = self._buf(("T", slot), (H, W), t.float32)
-        ncon = self._buf(("nc", slot), (H, W), t.int32)
+        ncon = self._buf(("nc", slot), (H, W), t.int32) if counts else None
         _lib.check(self.lib.vg_render_forward(self.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),
                                               _lib.ptr(ncon), self.stream()), "vg_render_forward")
         return color, tfin, ncon

@@ -88,7 +88,8 @@ class ViewShardedStep:
         # binning stream: high priority so its short CTAs interleave with the blend kernels
         import os
         prio = int(os.environ.get("VG_SIDE_PRIORITY", "-1"))
-        self.side = torch.cuda.Stream(device=dev, priority=prio) if pipeline else None
+        overlap = pipeline and os.environ.get("VG_OVERLAP", "1") != "0"  # "0": serial A/B timing
+        self.side = torch.cuda.Stream(device=dev, priority=prio) if overlap else None
         self.ev_binned = [torch.cuda.Event() for _ in self.engines]
         self.ev_free = [torch.cuda.Event() for _ in self.engines]
 
@@ -118,7 +119,7 @@ class ViewShardedStep:
             eng.tomo_backward_l2(img, self.targets[v], self.grads, accumulate=VG_DEFER,
                                  loss=self.loss)
         else:
-            color, tfin, _ = eng.forward()
+            color, tfin, _ = eng.forward(counts=False)
             eng.backward_l2(color, tfin, self.targets[v], self.grads, accumulate=VG_DEFER,
                             loss=self.loss)
         if self.side is not None:
