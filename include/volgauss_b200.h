@@ -213,6 +213,84 @@ int64_t vg_launch_count(vg_context* ctx);
 int vg_profile(vg_context* ctx, int32_t enable);
 int vg_profile_read(vg_context* ctx, double* ms, int64_t* counts);
 
+/* ---------------------------------------------------------------------------
+ * Training-step caller: optim.Trainer.step + GradAccum
+ * (optim.py:119-206) and the device half of densify_and_prune
+ * (optim.py:218-317).  Scene arrays are updated in place. */
+
+/* Trainer state on the device (float32).  moments: per primitive 14 Adam
+ * first moments then 14 second moments, in the order position (3), scale (3),
+ * rotation (4), colour (3, of the pre-softplus colour), density (1). */
+typedef struct {
+  float* means;
+  float* scales;
+  float* rotations;
+  float* thetas;
+  float* colors;
+  float* color_raw;    /* N*3 pre-softplus colours (optim.py:128) */
+  float* moments;      /* N*28 */
+  float* accum_norm;   /* optional GradAccum (optim.py:194-206): N */
+  float* accum_count;  /* N */
+  int64_t n;
+} vg_train_state;
+
+/* optim.Adam (optim.py:84-107) hyper-parameters for one step; lr in group
+ * order position (already scheduled: optim.py:140-144), scale, rotation,
+ * colour, density; t = the step count after this step (>= 1). */
+typedef struct {
+  double lr[5];
+  double beta1, beta2, eps;
+  int64_t t;
+} vg_adam_hparams;
+
+/* One Trainer.step (optim.py:146-175) fused with GradAccum.update: Adam on
+ * every group, then means -= u, scales floored at 1e-7, quaternions
+ * renormalised, colours through softplus, thetas clipped to [0, 1].  The
+ * gradients are a vg_grads (d_means, d_scales, d_rotations, d_thetas,
+ * d_colors and visible are read).  bad: device int32[5], set to the first
+ * primitive whose update is non-finite per group (INT32_MAX if none) -- the
+ * caller raises DivergenceError (optim.py:159-164) after reading it. */
+int vg_adam_step(vg_train_state* state, const vg_grads* grads, const vg_adam_hparams* hp,
+                 int32_t* bad, void* stream);
+
+/* densify_and_prune inputs (optim.TrainConfig fields, optim.py:24-53). */
+typedef struct {
+  int64_t n;
+  const float* means;
+  const float* scales;
+  const float* rotations;
+  const float* thetas;
+  const float* colors;
+  const float* color_raw;
+  const float* moments;
+  const float* accum_norm;
+  const float* accum_count;
+  double extent;
+  double split_grad_threshold, clone_grad_threshold, prune_theta_min;
+  double prune_scale_fraction, high_kappa_split_fraction;
+  int64_t max_primitives;
+} vg_densify_args;
+
+/* Scratch for vg_densify_plan / vg_densify_apply (device bytes). */
+size_t vg_densify_scratch_bytes(int64_t n);
+
+/* Split / clone / prune decisions with the primitive budget
+ * (optim.py:224-240, 292-297).  counts: device uint32[4] = {growing before
+ * the budget, kept, splits, clones}; the per-primitive decisions stay in
+ * scratch for vg_densify_apply. */
+int vg_densify_plan(const vg_densify_args* args, void* scratch, uint32_t* counts, void* stream);
+
+/* Write the densified state into `out` (sized kept + 2*(splits + clones)):
+ * kept rows in order, then two children per split parent (means offset by
+ * R diag(s) xi, scales / 1.6), then two per clone parent; children halve
+ * kappa (theta clamped at the ceiling), copy rotation and colour, and start
+ * with zero Adam moments.  counts_host: the counts of vg_densify_plan;
+ * xi: device float64[splits*6], the standard normals the reference draws
+ * per split parent (rng.standard_normal((2, 3)), optim.py:282). */
+int vg_densify_apply(const vg_densify_args* args, const void* scratch,
+                     const uint32_t* counts_host, const double* xi, vg_train_state* out,
+                     void* stream);
+
 /* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and
  * MUFU ex2 ops/s over all SMs of `device`. */
 int vg_probe_peaks(int32_t device, double* fp32_per_s, double* mufu_per_s);

@@ -46,6 +46,28 @@ class VgGrads(C.Structure):
                 ("accumulate", C.c_int32), ("_pad", C.c_int32)]
 
 
+class VgTrainState(C.Structure):
+    _fields_ = [("means", C.c_void_p), ("scales", C.c_void_p), ("rotations", C.c_void_p),
+                ("thetas", C.c_void_p), ("colors", C.c_void_p), ("color_raw", C.c_void_p),
+                ("moments", C.c_void_p), ("accum_norm", C.c_void_p), ("accum_count", C.c_void_p),
+                ("n", C.c_int64)]
+
+
+class VgAdamHparams(C.Structure):
+    _fields_ = [("lr", C.c_double * 5), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("t", C.c_int64)]
+
+
+class VgDensifyArgs(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("scales", C.c_void_p),
+                ("rotations", C.c_void_p), ("thetas", C.c_void_p), ("colors", C.c_void_p),
+                ("color_raw", C.c_void_p), ("moments", C.c_void_p), ("accum_norm", C.c_void_p),
+                ("accum_count", C.c_void_p), ("extent", C.c_double),
+                ("split_grad_threshold", C.c_double), ("clone_grad_threshold", C.c_double),
+                ("prune_theta_min", C.c_double), ("prune_scale_fraction", C.c_double),
+                ("high_kappa_split_fraction", C.c_double), ("max_primitives", C.c_int64)]
+
+
 EXPORTS = {
     "vg_abi_version": (C.c_int, []),
     "vg_last_error": (C.c_char_p, []),
@@ -74,6 +96,12 @@ EXPORTS = {
     "vg_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "vg_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "vg_probe_peaks": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "vg_adam_step": (C.c_int, [C.POINTER(VgTrainState), C.POINTER(VgGrads), C.POINTER(VgAdamHparams),
+                               C.c_void_p, C.c_void_p]),
+    "vg_densify_scratch_bytes": (C.c_size_t, [C.c_int64]),
+    "vg_densify_plan": (C.c_int, [C.POINTER(VgDensifyArgs), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vg_densify_apply": (C.c_int, [C.POINTER(VgDensifyArgs), C.c_void_p, C.POINTER(C.c_uint32),
+                                   C.c_void_p, C.POINTER(VgTrainState), C.c_void_p]),
 }
 
 KERNEL_KINDS = ("preprocess", "scan", "duplicate", "sort", "ranges", "render_fwd", "render_bwd",

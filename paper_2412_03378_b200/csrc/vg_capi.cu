@@ -21,6 +21,10 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+namespace vg {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace vg
+
 #define VG_CUDA(call)                                                                      \
   do {                                                                                     \
     cudaError_t _e = (call);                                                               \

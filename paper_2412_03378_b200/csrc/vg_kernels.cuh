@@ -5,6 +5,9 @@
 
 namespace vg {
 
+// record the thread-local message of vg_last_error (vg_capi.cu); returns code
+int set_error(int code, const char* msg);
+
 struct BlendParams {
   int width, height, ntx;
   float cx, cy, fx, fy;

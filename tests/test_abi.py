@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "volgauss_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|int64_t|const char\*)\s+(vg_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|int64_t|size_t|const char\*)\s+(vg_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_boundary():
