@@ -72,7 +72,13 @@ typedef struct {
   double alpha_clamp;  /* raster.ALPHA_CLAMP */
   double bin_cut;      /* alpha_cut used for bin radii: raster.prepare's
                           alpha_cut, or tomo.TOMO_BIN_CUT (tomo.py:28) */
+  int32_t sort_by;     /* VG_SORT_DEPTH (default) or VG_SORT_GAMMA (raster.py:291-312) */
+  int32_t _pad2;
 } vg_options;
+
+/* per-tile list order (raster.prepare's sort_by) */
+#define VG_SORT_DEPTH 0 /* (tile, float32 view depth, index) */
+#define VG_SORT_GAMMA 1 /* stable re-sort by gamma along each tile's central ray */
 
 /* raster.Scene (raster.py:38-97) as device float32 SoA */
 typedef struct {
@@ -120,9 +126,11 @@ void vg_destroy(vg_context* ctx);
 
 /* raster.prepare (raster.py:263-296) / bin_tiles (raster.py:315-319):
  * per-Gaussian projection, bounding radius and tile rectangle
- * (_project_all/_bounding_radii, raster.py:154-209), blend records,
- * tile-pair duplication, 64-bit (tile, depth) radix sort and per-tile ranges
- * (_build_grid, raster.py:222-260).  The scene pointers must stay valid
+ * (_project_all/_bounding_radii, raster.py:154-209), blend records, the
+ * depth radix sort of the Gaussians and the span binning into per-tile lists
+ * in (tile, depth, index) order with their ranges (_build_grid,
+ * raster.py:222-260); with opt->sort_by == VG_SORT_GAMMA each list is then
+ * re-sorted by gamma (_resort_by_gamma, raster.py:299-312).  The scene pointers must stay valid
  * until the matching backward has run. */
 int vg_prepare(vg_context* ctx, const vg_scene* scene, const vg_camera* cam,
                const vg_options* opt, void* stream);

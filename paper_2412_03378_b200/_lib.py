@@ -30,7 +30,8 @@ class VgCamera(C.Structure):
 
 class VgOptions(C.Structure):
     _fields_ = [("tile_size", C.c_int32), ("_pad", C.c_int32), ("early_stop", C.c_double),
-                ("alpha_cut", C.c_double), ("alpha_clamp", C.c_double), ("bin_cut", C.c_double)]
+                ("alpha_cut", C.c_double), ("alpha_clamp", C.c_double), ("bin_cut", C.c_double),
+                ("sort_by", C.c_int32), ("_pad2", C.c_int32)]
 
 
 class VgScene(C.Structure):
@@ -223,8 +224,12 @@ def make_camera(cam, projection=VG_PINHOLE, extent=0.0):
     return c
 
 
-def make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut):
+VG_SORT_DEPTH, VG_SORT_GAMMA = 0, 1
+
+
+def make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth"):
     o = VgOptions()
+    o.sort_by = VG_SORT_GAMMA if sort_by == "gamma" else VG_SORT_DEPTH
     o.tile_size = int(tile_size)
     o.early_stop = -1.0 if early_stop is None else float(early_stop)
     o.alpha_cut = float(alpha_cut)

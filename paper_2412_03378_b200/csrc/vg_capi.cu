@@ -57,6 +57,7 @@ struct vg_context {
   Buf dkey, perm, dsort_tmp;         // depth pre-sort of the Gaussians
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
   Buf cacc;                          // RGB gradient accumulators, SoA [3][N]
+  Buf gm, gscratch;                  // sort_by="gamma": per-Gaussian M, M delta; merge scratch
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
@@ -172,7 +173,7 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
-                &c->cacc, &c->vmask, &c->dcol, &c->centers};
+                &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -234,6 +235,10 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
                      const vg_options* opt, void* stream) {
   if (!c || !s || !opt) return fail(VG_EINVAL, "vg_prepare: NULL argument");
   if (opt->tile_size != TILE) return fail(VG_EINVAL, "only tile_size=16 is supported");
+  if (opt->sort_by != VG_SORT_DEPTH && opt->sort_by != VG_SORT_GAMMA)
+    return fail(VG_EINVAL, "unknown sort key");
+  if (opt->sort_by == VG_SORT_GAMMA && cam && cam->projection != VG_PINHOLE)
+    return fail(VG_EINVAL, "sort_by gamma needs a pinhole camera");
   if (s->n < 0) return fail(VG_EINVAL, "negative primitive count");
   if (s->n > 0x7fffffff) return fail(VG_EINVAL, "too many primitives (> 2^31-1)");
   if (s->n > 0 && (!s->means || !s->scales || !s->rotations || !s->thetas))
@@ -274,10 +279,15 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
       const size_t cb = sizeof(float) * 3 * (size_t)n;
       if (c->cacc.bytes < cb) VG_TRY(ensure(c->cacc, cb, st, true));
     }
+    double* gm = nullptr;
+    if (opt->sort_by == VG_SORT_GAMMA) {
+      VG_TRY(ensure(c->gm, sizeof(double) * 9 * (size_t)n, st));
+      gm = (double*)c->gm.p;
+    }
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
-                        (ushort4*)c->rect.p, (float*)c->frame.p, st);
+                        (ushort4*)c->rect.p, (float*)c->frame.p, gm, st);
     }
     VG_LAUNCHED(c, 1);
     // Gaussians in (float32 depth, index) order: hand-written radix sort of
@@ -346,6 +356,13 @@ int vg_prepare_finish(vg_context* c, void* stream) {
     VG_LAUNCHED(c, nl);
   }
   c->vals = P > 0 ? (uint32_t*)c->vals0.p : nullptr;
+  if (c->opt.sort_by == VG_SORT_GAMMA && P > 1) {
+    VG_TRY(ensure(c->gscratch, gamma_scratch_bytes(P), st));
+    ProfScope ps(c, VG_K_SORT, st);
+    launch_gamma_sort(nt, (const uint2*)c->ranges.p, c->vals, (const double*)c->gm.p, P,
+                      c->gscratch.p, k, st);
+    VG_LAUNCHED(c, 1);
+  }
   c->prepared = true;
   return VG_OK;
 }

@@ -33,8 +33,13 @@ struct BwdIO {
   float* d_background;
 };
 
+// gm (nullable): per binned Gaussian M and M (mean - centre) in float64, for sort_by="gamma"
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, ushort4* rect, float* frame, cudaStream_t st);
+                       float* depth, ushort4* rect, float* frame, double* gm, cudaStream_t st);
+// sort_by="gamma" re-sort of every tile list (vg_gamma.cu)
+size_t gamma_scratch_bytes(int64_t pairs);
+void launch_gamma_sort(int n_tiles, const uint2* ranges, uint32_t* vals, const double* gm,
+                       int64_t pairs, void* scratch, const CamK& cam, cudaStream_t st);
 // vmask (optional): per-warp bit rows of vm_words words marking the list
 // entries where the forward saw a visible pixel (the backward's work list).
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,

@@ -15,6 +15,7 @@ struct PrepOut {
   GRec* rec;
   float* depth;        // sort key (float32 view depth)
   ushort4* rect;       // tile rectangle x0, y0, x1, y1 (inclusive); x1 < x0: not binned
+  double* gm;          // sort_by="gamma" only: M (xx, xy, xz, yy, yz, zz) and M (mean - centre)
   float* frame;        // e1, e2, e3 in whitened-local coordinates (12 floats)
 };
 
@@ -92,6 +93,22 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   o.rect[i] = rect;
   o.depth[i] = (float)f.v[2];
   if (!cnt) return;
+  if (o.gm) {
+    // core.precision_matrices (core.py:111-119) and raster.prepare's
+    // minv_delta (raster.py:276-280), for the gamma re-sort
+    double M[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += f.R[a * 3 + k] * (1.0 / (f.s[k] * f.s[k])) * f.R[b * 3 + k];
+        M[a * 3 + b] = acc;
+      }
+    const double dl[3] = {(double)means[3 * i] - c.center[0], (double)means[3 * i + 1] - c.center[1],
+                          (double)means[3 * i + 2] - c.center[2]};
+    double* q = o.gm + 9 * i;
+    q[0] = M[0]; q[1] = M[1]; q[2] = M[2]; q[3] = M[4]; q[4] = M[5]; q[5] = M[8];
+    for (int a = 0; a < 3; ++a) q[6 + a] = M[a * 3] * dl[0] + M[a * 3 + 1] * dl[1] + M[a * 3 + 2] * dl[2];
+  }
   // --- blend record
   GRec g;
   g.u = f.pu;
@@ -140,9 +157,9 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
 }
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, ushort4* rect, float* frame, cudaStream_t st) {
+                       float* depth, ushort4* rect, float* frame, double* gm, cudaStream_t st) {
   if (n <= 0) return;
-  PrepOut o{rec, depth, rect, frame};
+  PrepOut o{rec, depth, rect, gm, frame};
   int blocks = (int)((n + 255) / 256);
   k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
                                        s.sh, c, bin_cut, o);

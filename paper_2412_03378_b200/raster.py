@@ -8,10 +8,11 @@ Same names, signatures, flag defaults and error behaviour as the reference:
 Array types: a scene whose arrays are numpy (e.g. a reference
 `volgauss.Scene`) gets numpy float64 outputs, exactly like the reference; a
 scene whose arrays are CUDA torch tensors gets CUDA torch outputs with no host
-round trip.  Unsupported reference options raise: tile_size != 16,
-mode='splat' (the EWA comparator, out of scope) and sort_by='gamma' (next
-round) raise NotImplementedError; unknown modes / sort keys raise ValueError
-as in raster.py:268-269, 293-294.
+round trip.  sort_by='gamma' re-sorts every tile list by gamma along the
+tile's central ray on the device (raster.py:299-312).  Unsupported reference
+options raise NotImplementedError: tile_size != 16 and mode='splat' (the EWA
+comparator, out of scope); unknown modes / sort keys raise ValueError as in
+raster.py:268-269, 293-294.
 """
 
 from __future__ import annotations
@@ -129,8 +130,6 @@ def _check_mode(mode, sort_by, tile_size):
         raise NotImplementedError("mode='splat' (EWA comparator) is outside this build's hot path")
     if sort_by not in ("depth", "gamma"):
         raise ValueError(f"unknown sort key {sort_by!r}")
-    if sort_by == "gamma":
-        raise NotImplementedError("sort_by='gamma' is not implemented yet")
     if int(tile_size) != TILE_SIZE:
         raise NotImplementedError("only tile_size=16 is supported")
 
@@ -244,8 +243,8 @@ class Prep:
         return z.cpu().numpy()
 
 
-def _options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut):
-    return _lib.make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut)
+def _options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth"):
+    return _lib.make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by)
 
 
 def _stream(dev):
@@ -262,7 +261,7 @@ def prepare(scene, camera, mode="analytic", tile_size=TILE_SIZE, sort_by="depth"
     dscene = scene if isinstance(scene, DeviceScene) else DeviceScene(scene)
     ctx = _ctx if _ctx is not None else _lib.Context(dscene.device.index)
     bin_cut = alpha_cut if _bin_cut is None else _bin_cut
-    opt = _options(tile_size, EARLY_STOP_T, alpha_cut, ALPHA_CLAMP, bin_cut)
+    opt = _options(tile_size, EARLY_STOP_T, alpha_cut, ALPHA_CLAMP, bin_cut, sort_by)
     cam = _lib.make_camera(camera, _projection, _extent)
     s = dscene.struct()
     import ctypes
