@@ -73,7 +73,8 @@ typedef struct {
   double bin_cut;      /* alpha_cut used for bin radii: raster.prepare's
                           alpha_cut, or tomo.TOMO_BIN_CUT (tomo.py:28) */
   int32_t sort_by;     /* VG_SORT_DEPTH (default) or VG_SORT_GAMMA (raster.py:291-312) */
-  int32_t _pad2;
+  int32_t deterministic; /* != 0: bitwise-reproducible backward (fixed-order reductions,
+                            like the reference's tile-order sum, grad.py:188-204) */
 } vg_options;
 
 /* per-tile list order (raster.prepare's sort_by) */

@@ -31,7 +31,7 @@ class VgCamera(C.Structure):
 class VgOptions(C.Structure):
     _fields_ = [("tile_size", C.c_int32), ("_pad", C.c_int32), ("early_stop", C.c_double),
                 ("alpha_cut", C.c_double), ("alpha_clamp", C.c_double), ("bin_cut", C.c_double),
-                ("sort_by", C.c_int32), ("_pad2", C.c_int32)]
+                ("sort_by", C.c_int32), ("deterministic", C.c_int32)]
 
 
 class VgScene(C.Structure):
@@ -227,8 +227,10 @@ def make_camera(cam, projection=VG_PINHOLE, extent=0.0):
 VG_SORT_DEPTH, VG_SORT_GAMMA = 0, 1
 
 
-def make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth"):
+def make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth",
+                 deterministic=False):
     o = VgOptions()
+    o.deterministic = 1 if deterministic else 0
     o.sort_by = VG_SORT_GAMMA if sort_by == "gamma" else VG_SORT_DEPTH
     o.tile_size = int(tile_size)
     o.early_stop = -1.0 if early_stop is None else float(early_stop)

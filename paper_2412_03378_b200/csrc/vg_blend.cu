@@ -272,6 +272,14 @@ __device__ __forceinline__ void flush_acc(float (&v)[16], int lane, uint32_t gid
   if (!(lane & 1) && idx < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + idx, s);
 }
 
+// Deterministic mode: the warp's 13 sums go to the (entry, warp) slot (no
+// atomics); vg_det.cu reduces the slots per Gaussian in a fixed order.
+__device__ __forceinline__ void flush_det(float (&v)[16], int lane, float* slot) {
+  float s = transpose_reduce16(v, lane);
+  int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  if (!(lane & 1) && idx < 13 && s != 0.f) slot[idx] = s;
+}
+
 // Warp reduction of 13 per-lane values through a shared-memory transpose:
 // each lane stores its 16-float row (4 x STS.128, row stride 20 floats), then
 // lane l sums column (l & 15) over the 16 rows of its half-warp (half 1 walks
@@ -301,7 +309,7 @@ __device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, f
 
 // Block sum of 3 floats + 1 double into global (d_background, loss).
 __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double l, float* out3,
-                                            double* outl) {
+                                            double* outl, bool store = false) {
   __shared__ float r3[NT / 32][3];
   __shared__ double rl[NT / 32];
   for (int o = 16; o; o >>= 1) {
@@ -317,12 +325,17 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
     float s0 = 0, s1 = 0, s2 = 0;
     double sl = 0;
     for (int i = 0; i < NT / 32; ++i) { s0 += r3[i][0]; s1 += r3[i][1]; s2 += r3[i][2]; sl += rl[i]; }
-    if (out3) {
-      if (s0 != 0.f) atomicAdd(out3 + 0, s0);
-      if (s1 != 0.f) atomicAdd(out3 + 1, s1);
-      if (s2 != 0.f) atomicAdd(out3 + 2, s2);
+    if (store) {  // deterministic mode: this tile's partial, reduced in tile order later
+      if (out3) { out3[0] = s0; out3[1] = s1; out3[2] = s2; }
+      if (outl) *outl = sl;
+    } else {
+      if (out3) {
+        if (s0 != 0.f) atomicAdd(out3 + 0, s0);
+        if (s1 != 0.f) atomicAdd(out3 + 1, s1);
+        if (s2 != 0.f) atomicAdd(out3 + 2, s2);
+      }
+      if (outl && sl != 0.0) atomicAdd(outl, sl);
     }
-    if (outl && sl != 0.0) atomicAdd(outl, sl);
   }
 }
 
@@ -517,10 +530,10 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
 // staged and the warp-independent kernels): recompute alpha exactly as the
 // forward did, advance T and the running suffix, form dL/de for live pixels,
 // and flush the warp's 13 accumulator sums for this Gaussian.
-template <bool CUT>
+template <bool CUT, bool DET>
 __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in0, bool in1,
                                           F2 dcr, F2 dcg, F2 dcb, F2 tot, const BlendParams& p,
-                                          F2& T, F2& P, int lane, const BwdIO& io) {
+                                          F2& T, F2& P, int lane, const BwdIO& io, uint32_t pos) {
   // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
   // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
@@ -558,14 +571,17 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
   v[13] = v[14] = v[15] = 0.f;
   const uint32_t gid = __float_as_uint(s.c.w);
   if (lane == 0 && any_vis) io.visible[gid] = 1;
-  flush_acc(v, lane, gid, io.acc);
+  if (DET)
+    flush_det(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE);
+  else
+    flush_acc(v, lane, gid, io.acc);
 }
 
 // Per-pixel prologue of the backward: upstream gradient (explicit or fused
 // L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
-template <int LOSS>
+template <int LOSS, bool DET>
 __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo& G, const BwdIO& io,
-                                             float (&dcv)[2][3], float (&totv)[2]) {
+                                             float (&dcv)[2][3], float (&totv)[2], int tile) {
   float Tfv[2] = {1.f, 1.f};
   double lossv = 0.0;
 #pragma unroll
@@ -594,16 +610,21 @@ __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo
     totv[q] = fmaf(dcv[q][0], cc0, fmaf(dcv[q][1], cc1, fmaf(dcv[q][2], cc2, dT * Tfv[q])));
   }
   __syncthreads();
-  block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
-              dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
-              LOSS ? io.loss_sum : nullptr);
+  if (DET)
+    block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
+                dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.det_bg + 3 * tile,
+                LOSS ? io.det_loss + tile : nullptr, true);
+  else
+    block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
+                dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
+                LOSS ? io.loss_sum : nullptr);
   __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
 // K6 backward blend (grad.backward tile_job + e_chain)
 
-template <bool CUT, int LOSS>
+template <bool CUT, int LOSS, bool DET = false>
 __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
@@ -622,7 +643,7 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
   const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
   const uint2 r = ranges[tile];
   float dcv[2][3], totv[2];
-  bwd_prologue<LOSS>(p, G, io, dcv, totv);
+  bwd_prologue<LOSS, DET>(p, G, io, dcv, totv, tile);
   const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
            dcb = f2(dcv[0][2], dcv[1][2]);
   const F2 tot = f2(totv[0], totv[1]);
@@ -667,10 +688,11 @@ __global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
           bits &= bits - 1;
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
-          bwd_entry<CUT>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
-          bwd_entry<CUT>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k);
+          bwd_entry<CUT, DET>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
+                              base + kb);
         } else {
-          bwd_entry<CUT>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io);
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k);
         }
       }
       done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);
@@ -867,12 +889,19 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
-#define VG_RB(C, L) \
-  k_render_bwd<C, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
-  if (cut) {
-    if (loss) VG_RB(true, 1); else VG_RB(true, 0);
+  const bool det = io.det_part != nullptr;
+#define VG_RB(C, L, D) \
+  k_render_bwd<C, L, D><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
+  if (det) {
+    if (cut) {
+      if (loss) VG_RB(true, 1, true); else VG_RB(true, 0, true);
+    } else {
+      if (loss) VG_RB(false, 1, true); else VG_RB(false, 0, true);
+    }
+  } else if (cut) {
+    if (loss) VG_RB(true, 1, false); else VG_RB(true, 0, false);
   } else {
-    if (loss) VG_RB(false, 1); else VG_RB(false, 0);
+    if (loss) VG_RB(false, 1, false); else VG_RB(false, 0, false);
   }
 #undef VG_RB
 }

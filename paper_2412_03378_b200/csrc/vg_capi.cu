@@ -58,6 +58,8 @@ struct vg_context {
   Buf frame, lacc;                   // per-view e-frames; view-independent grad accumulators
   Buf cacc;                          // RGB gradient accumulators, SoA [3][N]
   Buf gm, gscratch;                  // sort_by="gamma": per-Gaussian M, M delta; merge scratch
+  Buf det_part, det_cnt, det_off, det_slot, det_bg, det_loss, det_scan;  // deterministic mode
+  bool det_ready = false;            // det_slot maps the lists of the last prepare
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
@@ -173,7 +175,8 @@ void vg_destroy(vg_context* c) {
   Buf* all[] = {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
-                &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch};
+                &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
+                &c->det_bg, &c->det_loss, &c->det_scan};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -255,6 +258,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   c->n_tiles = k.ntx * k.nty;
   c->prepared = false;
   c->have_fwd = false;
+  c->det_ready = false;
   const int64_t npix = (int64_t)k.width * k.height;
   VG_TRY(ensure(c->ranges, sizeof(uint2) * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->n_act, sizeof(int) * (size_t)npix, st));
@@ -379,6 +383,7 @@ int vg_set_options(vg_context* c, const vg_options* opt) {
   c->opt.early_stop = opt->early_stop;
   c->opt.alpha_cut = opt->alpha_cut;
   c->opt.alpha_clamp = opt->alpha_clamp;
+  c->opt.deterministic = opt->deterministic;
   return VG_OK;
 }
 
@@ -605,6 +610,27 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)(c->scene.n > 0 ? c->scene.n : 1), st));
     io.visible = (uint8_t*)c->offset.p;
   }
+  const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
+  if (det) {
+    const int64_t n = c->scene.n, P = c->pairs;
+    if (!c->det_ready) {
+      VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
+      VG_TRY(ensure(c->det_off, sizeof(uint32_t) * ((size_t)n + 1), st));
+      VG_TRY(ensure(c->det_slot, sizeof(uint32_t) * (size_t)P, st));
+      VG_TRY(ensure(c->det_scan, scan_u32_scratch_bytes(n) + 16, st));
+      VG_CUDA(det_prepare(n, (const ushort4*)c->rect.p, (const uint2*)c->ranges.p, c->vals,
+                          c->n_tiles, c->cam.ntx, (uint32_t*)c->det_cnt.p, (uint32_t*)c->det_off.p,
+                          (uint32_t*)c->det_slot.p, c->det_scan.p, (uint32_t*)c->det_off.p + n, st));
+      c->det_ready = true;
+    }
+    VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
+    VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+    VG_TRY(ensure(c->det_bg, sizeof(float) * 3 * (size_t)c->n_tiles, st));
+    VG_TRY(ensure(c->det_loss, sizeof(double) * (size_t)c->n_tiles, st));
+    io.det_part = (float*)c->det_part.p;
+    io.det_bg = (float*)c->det_bg.p;
+    io.det_loss = (double*)c->det_loss.p;
+  }
   if (c->scene.n > 0) {
     {
       ProfScope ps(c, VG_K_RENDER_BWD, st);
@@ -614,6 +640,14 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                         vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st);
     }
     VG_LAUNCHED(c, 1);
+    if (det) {
+      VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
+                         (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
+                         (float*)c->acc.p, c->n_tiles, (const float*)c->det_bg.p,
+                         target ? (const double*)c->det_loss.p : nullptr, g->d_background,
+                         loss_sum, st));
+      VG_LAUNCHED(c, 2);
+    }
     VG_TRY(finish_view(c, g, st));
   } else {
     // empty scene: d_background = sum of d_color (grad.py:126-128) -- the

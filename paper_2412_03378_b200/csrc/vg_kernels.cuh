@@ -31,11 +31,27 @@ struct BwdIO {
   float* acc;               // per-Gaussian accumulators, 16 floats each
   uint8_t* visible;
   float* d_background;
+  // deterministic mode (vg_det.cu): per (entry, warp) slots and per-tile partials
+  float* det_part = nullptr;
+  float* det_bg = nullptr;
+  double* det_loss = nullptr;
 };
 
 // gm (nullable): per binned Gaussian M and M (mean - centre) in float64, for sort_by="gamma"
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
                        float* depth, ushort4* rect, float* frame, double* gm, cudaStream_t st);
+// deterministic-gradient mode (vg_det.cu)
+cudaError_t scan_u32(const uint32_t* in, uint32_t* out, void* scratch, uint32_t* total, int64_t n,
+                     cudaStream_t st);
+size_t scan_u32_scratch_bytes(int64_t n);
+size_t det_part_bytes(int64_t pairs);
+cudaError_t det_prepare(int64_t n, const ushort4* rect, const uint2* ranges, const uint32_t* vals,
+                        int n_tiles, int ntx, uint32_t* cnt, uint32_t* off, uint32_t* slot,
+                        void* scan_scratch, uint32_t* total, cudaStream_t st);
+cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, const uint32_t* slot,
+                       const float* part, float* acc, int n_tiles, const float* bg_part,
+                       const double* loss_part, float* d_background, double* loss_sum,
+                       cudaStream_t st);
 // sort_by="gamma" re-sort of every tile list (vg_gamma.cu)
 size_t gamma_scratch_bytes(int64_t pairs);
 void launch_gamma_sort(int n_tiles, const uint2* ranges, uint32_t* vals, const double* gm,

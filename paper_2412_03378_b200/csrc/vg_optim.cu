@@ -326,6 +326,13 @@ cudaError_t exclusive_scan(const T* in, T* out, T* scratch, T* total, int64_t n,
 }
 
 }  // namespace optim
+
+cudaError_t scan_u32(const uint32_t* in, uint32_t* out, void* scratch, uint32_t* total, int64_t n,
+                     cudaStream_t st) {
+  return optim::exclusive_scan<uint32_t>(in, out, (uint32_t*)scratch, total, n, st);
+}
+size_t scan_u32_scratch_bytes(int64_t n) { return sizeof(uint32_t) * (size_t)((n + 1023) / 1024 + 1); }
+
 }  // namespace vg
 
 using namespace vg;

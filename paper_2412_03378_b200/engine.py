@@ -21,12 +21,14 @@ from .tomo import TOMO_BIN_CUT
 
 class Engine:
     def __init__(self, device=None, early_stop=EARLY_STOP_T, alpha_cut=ALPHA_CUT,
-                 alpha_clamp=ALPHA_CLAMP):
+                 alpha_clamp=ALPHA_CLAMP, deterministic=False, sort_by="depth"):
         torch = _lib._require_cuda()
         self.torch = torch
         self.ctx = _lib.Context(device)
         self.device = torch.device("cuda", self.ctx.device)
         self.flags = (early_stop, alpha_cut, alpha_clamp)
+        self.deterministic = deterministic   # fixed-order gradient sums (vg_det.cu)
+        self.sort_by = sort_by
         self.lib = _lib.load()
         self._bufs = {}
         self.cam = None
@@ -61,7 +63,8 @@ class Engine:
         """First half of prepare (no host wait); see vg_prepare_async."""
         es, ac, cl = self.flags
         bin_cut = TOMO_BIN_CUT if tomo else ac
-        opt = _lib.make_options(TILE_SIZE, es, ac, cl, bin_cut)
+        opt = _lib.make_options(TILE_SIZE, es, ac, cl, bin_cut, sort_by=self.sort_by,
+                                deterministic=self.deterministic)
         c = _lib.make_camera(cam, _lib.VG_PARALLEL if parallel else _lib.VG_PINHOLE,
                              extent if parallel else 0.0)
         s = ds.struct()

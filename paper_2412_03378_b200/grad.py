@@ -146,10 +146,13 @@ def _dev_image(a, shape, dev):
 
 def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
              tile_size=TILE_SIZE, sort_by="depth", early_stop=EARLY_STOP_T, alpha_cut=ALPHA_CUT,
-             alpha_clamp=ALPHA_CLAMP, threads=None, prep=None) -> SceneGrads:
+             alpha_clamp=ALPHA_CLAMP, threads=None, prep=None, deterministic=True) -> SceneGrads:
     """grad.backward (grad.py:107-213), analytic mode.  Flags must match the
     forward render they differentiate.  Raises ValueError on a non-finite
-    upstream gradient (grad.py:121-125)."""
+    upstream gradient (grad.py:121-125).  deterministic=True (the default,
+    like the reference's thread-count-invariant result, grad.py:188-204)
+    reduces with fixed-order sums instead of float atomics: bitwise
+    reproducible; False is the faster training-loop path."""
     _check_mode(mode, sort_by, tile_size)
     _finite_or_raise(d_color, d_transmittance)
     if prep is None:
@@ -164,6 +167,9 @@ def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
     dt = _dev_image(d_transmittance, (H, W), dev) if d_transmittance is not None else None
     bufs = GradBuffers(dscene.n, dev, with_sh=dscene.sh is not None)
     g = bufs.struct(accumulate=False)
+    opt = _lib.make_options(TILE_SIZE, early_stop, alpha_cut, alpha_clamp, prep.alpha_cut,
+                            deterministic=deterministic)
+    _lib.check(_lib.load().vg_set_options(prep.ctx.handle, ctypes.byref(opt)), "vg_set_options")
     _lib.check(_lib.load().vg_render_backward(prep.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),
                                               _lib.ptr(dc), _lib.ptr(dt), ctypes.byref(g),
                                               _stream(dev)), "vg_render_backward")

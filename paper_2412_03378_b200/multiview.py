@@ -72,7 +72,8 @@ class ViewShardedStep:
         self.eng = engine
         self.engines = [engine]
         if pipeline:
-            self.engines.append(Engine(engine.ctx.device, *engine.flags))
+            self.engines.append(Engine(engine.ctx.device, *engine.flags,
+                                       deterministic=engine.deterministic, sort_by=engine.sort_by))
         self.ds = dscene
         self.cams = cameras
         self.targets = targets

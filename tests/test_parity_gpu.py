@@ -473,3 +473,42 @@ def test_gamma_sort_long_lists_merge_path():
     assert np.diff(offs).max() > 2 * 2048
     mism = np.flatnonzero(prims != oprep.pair_prim)
     assert mism.size <= 1e-4 * prims.size, mism.size
+
+
+@pytest.mark.parametrize("name", ["mini_opaque", "tiny"])
+def test_deterministic_backward_is_bitwise_reproducible(name):
+    """deterministic=True (default of the drop-in backward): fixed-order sums
+    (vg_det.cu), so repeated calls are bitwise identical -- the reference's
+    thread-count invariance (grad.py:188-204) -- and agree with the
+    atomic path within the parity tolerance."""
+    scene, cam, d = load_case(name)
+    rng = np.random.default_rng(3)
+    dc = rng.uniform(-1, 1, (cam.height, cam.width, 3))
+    a = vg().backward(scene, cam, dc)
+    b = vg().backward(scene, cam, dc)
+    fast = vg().backward(scene, cam, dc, deterministic=False)
+    for f in GRAD_FIELDS + ["d_background"]:
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        np.testing.assert_allclose(getattr(a, f), getattr(fast, f), rtol=1e-4,
+                                   atol=1e-5 * max(1.0, float(np.abs(getattr(fast, f)).max())))
+    assert np.array_equal(a.visible, fast.visible)
+
+
+def test_deterministic_multiview_step_is_bitwise_reproducible():
+    """The engine's multi-view step with deterministic=True: two runs give
+    bitwise-identical flat gradient buffers and loss."""
+    import torch
+    from paper_2412_03378_b200 import configs
+    from paper_2412_03378_b200.engine import Engine
+    from paper_2412_03378_b200.multiview import ViewShardedStep
+    cfg = configs.large(n=20000, width=160, height=96, n_views=4)
+    eng = Engine(deterministic=True)
+    ds = eng.upload(cfg.scene)
+    targets = {v: torch.from_numpy(cfg.target(v, (96, 160, 3))).cuda() for v in range(4)}
+    step = ViewShardedStep(eng, ds, cfg.cameras, targets)
+    l1 = float(step())
+    g1 = step.grads.flat.clone()
+    l2 = float(step())
+    g2 = step.grads.flat.clone()
+    assert l1 == l2
+    assert torch.equal(g1, g2)
