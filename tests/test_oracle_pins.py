@@ -159,3 +159,32 @@ def test_gamma_sort_matches_reference(name):
     gr = O.backward(scene, cam, g[f"{name}_dcolor"], prep=prep)
     for f in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_background"):
         close(getattr(gr, f), g[f"{name}_{f}"], rtol=1e-8, atol=1e-11)
+
+
+@pytest.mark.parametrize("name", ["tiny", "ragged"])
+def test_splat_mode_matches_reference(name):
+    """mode='splat' (the EWA comparator, raster.py:353-361, grad.py:170-177,
+    262-302): bin radii, tile lists, image, n_contrib and every gradient
+    (golden: tests/golden/make_golden_splat.py)."""
+    import os
+    from types import SimpleNamespace
+    from oracle import splat_oracle as SO
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "splat.npz"))
+    scene, cam, d = load_case(name)
+    scene = SimpleNamespace(means=scene.means, scales=scene.scales, rotations=scene.rotations,
+                            thetas=scene.thetas, colors=scene.colors, background=scene.background,
+                            splat_opacities=g[f"{name}_opac"])
+    prep = SO.prepare(scene, cam)
+    close(prep.radius, g[f"{name}_radius"], rtol=1e-13)
+    off = g[f"{name}_offsets"]
+    for t in range(len(off) - 1):
+        assert np.array_equal(prep.tile_ids(t), g[f"{name}_prims"][off[t]:off[t + 1]]), t
+    out = SO.render(scene, cam, prep=prep)
+    close(out.color, g[f"{name}_color"], rtol=1e-10, atol=1e-13)
+    close(out.final_transmittance, g[f"{name}_T"], rtol=1e-10, atol=1e-13)
+    assert np.array_equal(out.n_contrib, g[f"{name}_ncontrib"])
+    gr = SO.backward(scene, cam, g[f"{name}_dcolor"], prep=prep)
+    for f in ("d_means", "d_scales", "d_rotations", "d_colors", "d_background", "d_splat_opacities"):
+        close(getattr(gr, f), g[f"{name}_{f}"], rtol=1e-8, atol=1e-11)
+    assert np.array_equal(gr.visible, g[f"{name}_visible"])
+    assert not np.any(g[f"{name}_d_thetas"])
