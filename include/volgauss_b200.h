@@ -75,7 +75,13 @@ typedef struct {
   int32_t sort_by;     /* VG_SORT_DEPTH (default) or VG_SORT_GAMMA (raster.py:291-312) */
   int32_t deterministic; /* != 0: bitwise-reproducible backward (fixed-order reductions,
                             like the reference's tile-order sum, grad.py:188-204) */
+  int32_t mode;        /* VG_MODE_ANALYTIC (default) or VG_MODE_SPLAT (the EWA comparator) */
+  int32_t _pad3;
 } vg_options;
+
+/* render mode (raster.prepare's mode, raster.py:268-269) */
+#define VG_MODE_ANALYTIC 0 /* analytic transmittance (the paper's method) */
+#define VG_MODE_SPLAT 1    /* EWA splatting: opacity * exp(-maha/2) (raster.py:353-361) */
 
 /* per-tile list order (raster.prepare's sort_by) */
 #define VG_SORT_DEPTH 0 /* (tile, float32 view depth, index) */
@@ -92,6 +98,7 @@ typedef struct {
                            are evaluated per view from sh (DC band = RGB) */
   int64_t n;
   double background[3];
+  const float* splat_opacities; /* N, mode="splat" only (raster.Scene.splat_opacities) */
 } vg_scene;
 
 /* grad.SceneGrads (grad.py:41-69) as device pointers.  Any pointer may be
@@ -117,6 +124,7 @@ typedef struct {
   uint8_t* visible;    /* N   (OR-accumulated) */
   int32_t accumulate;  /* VG_OVERWRITE, VG_ADD or VG_DEFER */
   int32_t _pad;
+  float* d_splat_opacities; /* N, mode="splat" (zero in analytic mode) */
 } vg_grads;
 
 /* lifecycle */

@@ -31,20 +31,21 @@ class VgCamera(C.Structure):
 class VgOptions(C.Structure):
     _fields_ = [("tile_size", C.c_int32), ("_pad", C.c_int32), ("early_stop", C.c_double),
                 ("alpha_cut", C.c_double), ("alpha_clamp", C.c_double), ("bin_cut", C.c_double),
-                ("sort_by", C.c_int32), ("deterministic", C.c_int32)]
+                ("sort_by", C.c_int32), ("deterministic", C.c_int32), ("mode", C.c_int32),
+                ("_pad3", C.c_int32)]
 
 
 class VgScene(C.Structure):
     _fields_ = [("means", C.c_void_p), ("scales", C.c_void_p), ("rotations", C.c_void_p),
                 ("thetas", C.c_void_p), ("colors", C.c_void_p), ("sh", C.c_void_p),
-                ("n", C.c_int64), ("background", C.c_double * 3)]
+                ("n", C.c_int64), ("background", C.c_double * 3), ("splat_opacities", C.c_void_p)]
 
 
 class VgGrads(C.Structure):
     _fields_ = [("d_means", C.c_void_p), ("d_scales", C.c_void_p), ("d_rotations", C.c_void_p),
                 ("d_thetas", C.c_void_p), ("d_colors", C.c_void_p), ("d_kappas", C.c_void_p),
                 ("d_sh", C.c_void_p), ("d_background", C.c_void_p), ("visible", C.c_void_p),
-                ("accumulate", C.c_int32), ("_pad", C.c_int32)]
+                ("accumulate", C.c_int32), ("_pad", C.c_int32), ("d_splat_opacities", C.c_void_p)]
 
 
 class VgTrainState(C.Structure):
@@ -227,9 +228,13 @@ def make_camera(cam, projection=VG_PINHOLE, extent=0.0):
 VG_SORT_DEPTH, VG_SORT_GAMMA = 0, 1
 
 
+VG_MODE_ANALYTIC, VG_MODE_SPLAT = 0, 1
+
+
 def make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth",
-                 deterministic=False):
+                 deterministic=False, mode="analytic"):
     o = VgOptions()
+    o.mode = VG_MODE_SPLAT if mode == "splat" else VG_MODE_ANALYTIC
     o.deterministic = 1 if deterministic else 0
     o.sort_by = VG_SORT_GAMMA if sort_by == "gamma" else VG_SORT_DEPTH
     o.tile_size = int(tile_size)

@@ -31,15 +31,9 @@
 // Per-Gaussian accumulators (13 floats, whitened e-frame, see vg_finalize.cu)
 // are summed over the lane's two pixels, warp-reduced with a transpose-reduce
 // (16 shuffles) and added with one 13-lane red.global.add per warp.
-#include "vg_kernels.cuh"
+#include "vg_blend.cuh"
 
 namespace vg {
-
-constexpr unsigned FULL = 0xffffffffu;
-constexpr float C_HALF_LOG2E = 0.72134752044448170f;  // 0.5 * log2(e)
-constexpr int ACC_STRIDE = 16;                         // floats per Gaussian accumulator
-constexpr int NT = 128;                                // threads per tile CTA
-constexpr int BATCH = 256;                             // staged records per batch
 
 struct __align__(16) SRec {
   float4 a;  // c1, c2, c3, cD2
@@ -47,55 +41,6 @@ struct __align__(16) SRec {
   float4 c;  // n1, n2, D|beta, gid (bits)
   float4 d;  // r, g, b, 0
 };
-
-// ---------------------------------------------------------------------------
-// packed FP32x2 helpers (sm_100a FFMA2 / FMUL2 / FADD2)
-
-struct F2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ F2 f2(float a, float b) {
-  F2 r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r.v) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ F2 f2s(float a) { return f2(a, a); }
-__device__ __forceinline__ float lo(F2 x) { return __uint_as_float((unsigned)(x.v & 0xffffffffull)); }
-__device__ __forceinline__ float hi(F2 x) { return __uint_as_float((unsigned)(x.v >> 32)); }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-  F2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-  return d;
-}
-__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
-  F2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
-  return d;
-}
-__device__ __forceinline__ F2 add2(F2 a, F2 b) {
-  F2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
-  return d;
-}
-__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
-  F2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
-  return d;
-}
-__device__ __forceinline__ F2 ex2_2(F2 x) { return f2(ex2f(lo(x)), ex2f(hi(x))); }
-__device__ __forceinline__ F2 rsq_2(F2 x) { return f2(rsqf(lo(x)), rsqf(hi(x))); }
-__device__ __forceinline__ F2 neg2(F2 x) { return f2(-lo(x), -hi(x)); }
-__device__ __forceinline__ F2 sel2(bool p0, bool p1, F2 a, F2 b) {
-  return f2(p0 ? lo(a) : lo(b), p1 ? hi(a) : hi(b));
-}
-
-// ---------------------------------------------------------------------------
-// staging + culling
-
-__device__ __forceinline__ float d0(float lo_, float hi_) {
-  // distance of the interval [lo_, hi_] from 0
-  return fmaxf(fmaxf(lo_, -hi_), 0.f);
-}
 
 // Stage one record for the tile at pixel origin (x0, y0); return the 4-bit
 // mask of 8x8 warp blocks the Gaussian may reach with alpha >= cut.
@@ -212,131 +157,6 @@ __device__ __forceinline__ float pixel_lp(const BlendParams& p, int col, int row
   float X = ((float)col + 0.5f - p.cx) / p.fx;
   float Y = ((float)row + 0.5f - p.cy) / p.fy;
   return 0.5f * lg2f(fmaf(X, X, fmaf(Y, Y, 1.f)));
-}
-
-// Lane geometry: warp w owns the 8x8 block (8(w&1), 8(w>>1)); lane l owns
-// column 8(w&1) + (l&7) and rows 8(w>>1) + (l>>3) and +4.
-struct LaneGeo {
-  int lxi, ly0, col, row0, row1;
-  bool in0, in1;
-};
-__device__ __forceinline__ LaneGeo lane_geo(const BlendParams& p, int tx, int ty) {
-  LaneGeo g;
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  g.lxi = 8 * (w & 1) + (l & 7);
-  g.ly0 = 8 * (w >> 1) + (l >> 3);
-  g.col = tx * TILE + g.lxi;
-  g.row0 = ty * TILE + g.ly0;
-  g.row1 = g.row0 + 4;
-  g.in0 = g.col < p.width && g.row0 < p.height;
-  g.in1 = g.col < p.width && g.row1 < p.height;
-  return g;
-}
-
-// Reduce 16 per-lane values over the warp; lane l ends with the warp total of
-// value index ((l>>4&1)*8 + (l>>3&1)*4 + (l>>2&1)*2 + (l>>1&1)).
-__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    bool h = lane & 16;
-    float send = h ? v[i] : v[i + 8];
-    float keep = h ? v[i + 8] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    bool h = lane & 8;
-    float send = h ? v[i] : v[i + 4];
-    float keep = h ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    bool h = lane & 4;
-    float send = h ? v[i] : v[i + 2];
-    float keep = h ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 4);
-  }
-  {
-    bool h = lane & 2;
-    float send = h ? v[0] : v[1];
-    float keep = h ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(FULL, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(FULL, v[0], 1);
-}
-
-__device__ __forceinline__ void flush_acc(float (&v)[16], int lane, uint32_t gid, float* acc) {
-  float s = transpose_reduce16(v, lane);
-  int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-  if (!(lane & 1) && idx < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + idx, s);
-}
-
-// Deterministic mode: the warp's 13 sums go to the (entry, warp) slot (no
-// atomics); vg_det.cu reduces the slots per Gaussian in a fixed order.
-__device__ __forceinline__ void flush_det(float (&v)[16], int lane, float* slot) {
-  float s = transpose_reduce16(v, lane);
-  int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-  if (!(lane & 1) && idx < 13 && s != 0.f) slot[idx] = s;
-}
-
-// Warp reduction of 13 per-lane values through a shared-memory transpose:
-// each lane stores its 16-float row (4 x STS.128, row stride 20 floats), then
-// lane l sums column (l & 15) over the 16 rows of its half-warp (half 1 walks
-// its rows rotated by 4 so the two halves hit disjoint banks), and one
-// shuffle joins the halves; lanes 0..12 add the result to global memory.
-// ~39 instructions instead of ~61 for the shuffle/select butterfly.
-constexpr int RED_STRIDE = 20;
-__device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, float* red,
-                                               uint32_t gid, float* acc) {
-  float4* row = reinterpret_cast<float4*>(red + lane * RED_STRIDE);
-  row[0] = make_float4(v[0], v[1], v[2], v[3]);
-  row[1] = make_float4(v[4], v[5], v[6], v[7]);
-  row[2] = make_float4(v[8], v[9], v[10], v[11]);
-  row[3] = make_float4(v[12], 0.f, 0.f, 0.f);
-  __syncwarp();
-  const int col = lane & 15, half = lane >> 4;
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int r = half * 16 + ((k + 4 * half) & 15);
-    s += red[r * RED_STRIDE + col];
-  }
-  __syncwarp();
-  s += __shfl_xor_sync(FULL, s, 16);
-  if (lane < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + lane, s);
-}
-
-// Block sum of 3 floats + 1 double into global (d_background, loss).
-__device__ __forceinline__ void block_flush(float a0, float a1, float a2, double l, float* out3,
-                                            double* outl, bool store = false) {
-  __shared__ float r3[NT / 32][3];
-  __shared__ double rl[NT / 32];
-  for (int o = 16; o; o >>= 1) {
-    a0 += __shfl_xor_sync(FULL, a0, o);
-    a1 += __shfl_xor_sync(FULL, a1, o);
-    a2 += __shfl_xor_sync(FULL, a2, o);
-    l += __shfl_xor_sync(FULL, l, o);
-  }
-  int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) { r3[w][0] = a0; r3[w][1] = a1; r3[w][2] = a2; rl[w] = l; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float s0 = 0, s1 = 0, s2 = 0;
-    double sl = 0;
-    for (int i = 0; i < NT / 32; ++i) { s0 += r3[i][0]; s1 += r3[i][1]; s2 += r3[i][2]; sl += rl[i]; }
-    if (store) {  // deterministic mode: this tile's partial, reduced in tile order later
-      if (out3) { out3[0] = s0; out3[1] = s1; out3[2] = s2; }
-      if (outl) *outl = sl;
-    } else {
-      if (out3) {
-        if (s0 != 0.f) atomicAdd(out3 + 0, s0);
-        if (s1 != 0.f) atomicAdd(out3 + 1, s1);
-        if (s2 != 0.f) atomicAdd(out3 + 2, s2);
-      }
-      if (outl && sl != 0.0) atomicAdd(outl, sl);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -499,7 +319,6 @@ __global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
 //   A11 = q1^2 k1, A12 = q1 k1 q2, A22 = k1 q2^2, A13 = q1 k2, A23 = k2 q2,
 //   A33 = h (s^2 X^2 + w_par^2 / |w|^2),  k1 = h (s^2 w_par^2 + 1/|w|^2),
 //   k2 = h w_par (1/|w|^2 - s^2 X); q1 is shared by the lane's two pixels.
-__device__ __forceinline__ float hsum(F2 x) { return lo(x) + hi(x); }
 
 __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s, F2 h,
                                                    float (&v)[16]) {
@@ -575,50 +394,6 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
     flush_det(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE);
   else
     flush_acc(v, lane, gid, io.acc);
-}
-
-// Per-pixel prologue of the backward: upstream gradient (explicit or fused
-// L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
-template <int LOSS, bool DET>
-__device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo& G, const BwdIO& io,
-                                             float (&dcv)[2][3], float (&totv)[2], int tile) {
-  float Tfv[2] = {1.f, 1.f};
-  double lossv = 0.0;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    dcv[q][0] = dcv[q][1] = dcv[q][2] = 0.f;
-    totv[q] = 0.f;
-    const bool in = q ? G.in1 : G.in0;
-    if (!in) continue;
-    const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
-    const float cc0 = io.color[3 * pix], cc1 = io.color[3 * pix + 1], cc2 = io.color[3 * pix + 2];
-    Tfv[q] = io.final_t[pix];
-    float dT = 0.f;
-    if (LOSS == 0) {
-      dcv[q][0] = io.d_color[3 * pix];
-      dcv[q][1] = io.d_color[3 * pix + 1];
-      dcv[q][2] = io.d_color[3 * pix + 2];
-      if (io.d_t) dT = io.d_t[pix];
-    } else {
-      const float r0 = cc0 - io.target[3 * pix], r1 = cc1 - io.target[3 * pix + 1],
-                  r2 = cc2 - io.target[3 * pix + 2];
-      lossv += (double)r0 * r0 + (double)r1 * r1 + (double)r2 * r2;
-      dcv[q][0] = io.loss_scale * r0;
-      dcv[q][1] = io.loss_scale * r1;
-      dcv[q][2] = io.loss_scale * r2;
-    }
-    totv[q] = fmaf(dcv[q][0], cc0, fmaf(dcv[q][1], cc1, fmaf(dcv[q][2], cc2, dT * Tfv[q])));
-  }
-  __syncthreads();
-  if (DET)
-    block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
-                dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.det_bg + 3 * tile,
-                LOSS ? io.det_loss + tile : nullptr, true);
-  else
-    block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],
-                dcv[0][2] * Tfv[0] + dcv[1][2] * Tfv[1], lossv, io.d_background,
-                LOSS ? io.loss_sum : nullptr);
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------

@@ -240,6 +240,12 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   if (opt->tile_size != TILE) return fail(VG_EINVAL, "only tile_size=16 is supported");
   if (opt->sort_by != VG_SORT_DEPTH && opt->sort_by != VG_SORT_GAMMA)
     return fail(VG_EINVAL, "unknown sort key");
+  if (opt->mode != VG_MODE_ANALYTIC && opt->mode != VG_MODE_SPLAT)
+    return fail(VG_EINVAL, "unknown mode");
+  if (opt->mode == VG_MODE_SPLAT && s && s->n > 0 && !s->splat_opacities)
+    return fail(VG_EINVAL, "mode splat needs scene.splat_opacities");
+  if (opt->mode == VG_MODE_SPLAT && cam && cam->projection != VG_PINHOLE)
+    return fail(VG_EINVAL, "mode splat needs a pinhole camera");
   if (opt->sort_by == VG_SORT_GAMMA && cam && cam->projection != VG_PINHOLE)
     return fail(VG_EINVAL, "sort_by gamma needs a pinhole camera");
   if (s->n < 0) return fail(VG_EINVAL, "negative primitive count");
@@ -291,7 +297,8 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     {
       ProfScope ps(c, VG_K_PREPROCESS, st);
       launch_preprocess(n, *s, k, opt->bin_cut, (GRec*)c->rec.p, (float*)c->depth.p,
-                        (ushort4*)c->rect.p, (float*)c->frame.p, gm, st);
+                        (ushort4*)c->rect.p, (float*)c->frame.p, gm, opt->mode == VG_MODE_SPLAT,
+                        st);
     }
     VG_LAUNCHED(c, 1);
     // Gaussians in (float32 depth, index) order: hand-written radix sort of
@@ -466,7 +473,7 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   // with alpha_cut > 0, "live => not cut => visible": the forward records
   // which (entry, warp block) pairs had a visible pixel and the backward
   // walks exactly those
-  const bool use_vm = c->opt.alpha_cut > 0 && c->pairs > 0;
+  const bool use_vm = c->opt.alpha_cut > 0 && c->pairs > 0 && c->opt.mode != VG_MODE_SPLAT;
   uint32_t* vm = nullptr;
   if (use_vm) {
     c->vm_words = (int)((c->pairs + 31) / 32) + 1;
@@ -478,10 +485,15 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   c->vmask_valid = use_vm;
   {
     ProfScope ps(c, VG_K_RENDER_FWD, st);
-    launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
-                      (const uint32_t*)c->tord.p, p,
-                      c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
-                      (int*)c->n_act.p, vm, c->vm_words, st);
+    if (c->opt.mode == VG_MODE_SPLAT)
+      launch_splat_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                       (const uint32_t*)c->tord.p, p, color, final_t, n_contrib,
+                       n_contrib ? (int*)c->n_act.p : nullptr, st);
+    else
+      launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                        (const uint32_t*)c->tord.p, p,
+                        c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
+                        (int*)c->n_act.p, vm, c->vm_words, st);
   }
   VG_LAUNCHED(c, 1);
   c->have_fwd = true;
@@ -545,7 +557,7 @@ static int run_param_chain(vg_context* c, const vg_grads& g, cudaStream_t st) {
     ProfScope ps(c, VG_K_FINALIZE, st);
     k = launch_finalize_params(c->scene.n, c->scene, (float*)c->lacc.p, (float*)c->cacc.p,
                                (const float*)c->dcol.p, (const double*)c->centers.p, c->sh_views,
-                               g, st);
+                               g, c->opt.mode == VG_MODE_SPLAT, st);
   }
   c->sh_views = 0;
   VG_LAUNCHED(c, k);
@@ -568,7 +580,8 @@ static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
   {
     ProfScope ps(c, VG_K_FINALIZE, st);
     launch_view_accumulate(n, c->scene, c->cam, (const float*)c->frame.p, (float*)c->acc.p,
-                           (float*)c->lacc.p, (float*)c->cacc.p, dcol, center, st);
+                           (float*)c->lacc.p, (float*)c->cacc.p, dcol, center,
+                           c->opt.mode == VG_MODE_SPLAT, st);
   }
   VG_LAUNCHED(c, 1);
   if (g->accumulate != VG_DEFER) VG_TRY(run_param_chain(c, *g, st));
@@ -635,9 +648,13 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     {
       ProfScope ps(c, VG_K_RENDER_BWD, st);
       const bool vm = c->vmask_valid && c->opt.alpha_cut > 0;
-      launch_render_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
-                        (const uint32_t*)c->tord.p, p, c->opt.alpha_cut > 0, target ? 1 : 0, io,
-                        vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st);
+      if (c->opt.mode == VG_MODE_SPLAT)
+        launch_splat_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                         (const uint32_t*)c->tord.p, p, target ? 1 : 0, io, st);
+      else
+        launch_render_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                          (const uint32_t*)c->tord.p, p, c->opt.alpha_cut > 0, target ? 1 : 0, io,
+                          vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st);
     }
     VG_LAUNCHED(c, 1);
     if (det) {
@@ -674,6 +691,7 @@ int vg_render_backward_l2(vg_context* c, const float* color, const float* final_
 int vg_tomo_forward(vg_context* c, float* image, float* intensity, void* stream) {
   if (!c || !image) return fail(VG_EINVAL, "vg_tomo_forward: NULL argument");
   if (!c->prepared) return fail(VG_EINVAL, "vg_tomo_forward: call vg_prepare first");
+  if (c->opt.mode != VG_MODE_ANALYTIC) return fail(VG_EINVAL, "tomography is analytic-mode only");
   cudaStream_t st = (cudaStream_t)stream;
   BlendParams p = blend_params(c);
   {
@@ -688,6 +706,7 @@ int vg_tomo_forward(vg_context* c, float* image, float* intensity, void* stream)
 static int tomo_bwd_common(vg_context* c, const float* d_image, const float* image,
                            const float* target, double* loss_sum, vg_grads* g, void* stream) {
   if (!c->prepared) return fail(VG_EINVAL, "vg_tomo_backward: call vg_prepare first");
+  if (c->opt.mode != VG_MODE_ANALYTIC) return fail(VG_EINVAL, "tomography is analytic-mode only");
   cudaStream_t st = (cudaStream_t)stream;
   VG_TRY(prep_grads(c, g, st));
   BlendParams p = blend_params(c);

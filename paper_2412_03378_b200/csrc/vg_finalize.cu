@@ -34,6 +34,8 @@ namespace vg {
 struct ViewAccIn {
   int64_t n;
   const float* means;
+  const float* scales;  // splat mode: the EWA projection is re-derived per view
+  const float* rots;
   const float* sh;       // optional SH-3 coefficients (selects the SH pull-back)
   const float* frame;    // n * 12: e1, e2, e3 (whitened-local), pad
   float* acc;            // n * 16 per-view accumulators (zeroed here)
@@ -41,6 +43,14 @@ struct ViewAccIn {
   float* cacc;           // [3][n] RGB gradient accumulators (SoA: coalesced)
   float* dcol;           // SH scenes: this view's dL/dRGB slab [3][n]
   double* center;        // SH scenes: this view's camera centre (written by thread 0)
+};
+
+struct FinalIn {
+  int64_t n;
+  const float* scales;
+  const float* rots;
+  const float* thetas;
+  float* lacc;  // n * 12 (zeroed here)
 };
 
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
@@ -97,6 +107,195 @@ __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   if (raw[10] != 0.f) in.cacc[i] += raw[10];
   if (raw[11] != 0.f) in.cacc[n + i] += raw[11];
   if (raw[12] != 0.f) in.cacc[2 * n + i] += raw[12];
+}
+
+// mode="splat" (the EWA comparator): the view's accumulators (slot 0
+// dL/dopacity, 1..3 dL/dconic (xx, xy, yy), 4..5 dL/dmean2d; colour 10..12)
+// are pulled through this view's EWA projection (grad.py:262-302,
+// _splat_projection_backward) into view-independent world-space terms:
+// lacc 0..5 dL/dSigma (xx, xy, xz, yy, yz, zz), 6..8 dL/dmean, 9 dL/dopacity.
+__global__ void __launch_bounds__(128) k_view_accumulate_splat(ViewAccIn in, CamK c) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= in.n) return;
+  float4* a4 = reinterpret_cast<float4*>(in.acc + 16 * i);
+  const float4 x0 = a4[0], x1 = a4[1], x2 = a4[2], x3 = a4[3];
+  const float raw[13] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w, x2.x, x2.y, x2.z, x2.w, x3.x};
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 13; ++k) any |= raw[k] != 0.f;
+  const int64_t n = in.n;
+  if (in.dcol) {
+    if (i == 0) { in.center[0] = c.center[0]; in.center[1] = c.center[1]; in.center[2] = c.center[2]; }
+    in.dcol[i] = raw[10];
+    in.dcol[n + i] = raw[11];
+    in.dcol[2 * n + i] = raw[12];
+  }
+  if (!any) return;
+  const float4 zf = make_float4(0.f, 0.f, 0.f, 0.f);
+  a4[0] = zf; a4[1] = zf; a4[2] = zf; a4[3] = zf;
+  if (raw[0] != 0.f || raw[1] != 0.f || raw[2] != 0.f || raw[3] != 0.f || raw[4] != 0.f ||
+      raw[5] != 0.f) {
+    // re-derive this view's projection exactly as preprocess did
+    double R[9];
+    quat_rotmat(in.rots + 4 * i, R, nullptr);
+    double s[3];
+    for (int k = 0; k < 3; ++k) s[k] = fmax((double)in.scales[3 * i + k], SCALE_FLOOR);
+    double Sig[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += R[a * 3 + k] * (s[k] * s[k]) * R[b * 3 + k];
+        Sig[a * 3 + b] = acc;
+      }
+    const double m3[3] = {in.means[3 * i], in.means[3 * i + 1], in.means[3 * i + 2]};
+    double v[3];
+    for (int j = 0; j < 3; ++j)
+      v[j] = c.R[j * 3 + 0] * m3[0] + c.R[j * 3 + 1] * m3[1] + c.R[j * 3 + 2] * m3[2] + c.t[j];
+    const double z = v[2], x = v[0], y = v[1];
+    const double limx = 1.3 * (0.5 * c.width / c.fx), limy = 1.3 * (0.5 * c.height / c.fy);
+    const double rx = fmin(fmax(x / z, -limx), limx), ry = fmin(fmax(y / z, -limy), limy);
+    const bool ox = !(fabs(x / z) > limx), oy = !(fabs(y / z) > limy);
+    const double J[6] = {c.fx / z, 0.0, -c.fx * rx / z, 0.0, c.fy / z, -c.fy * ry / z};
+    double U[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b)
+        U[a * 3 + b] = J[a * 3] * c.R[b] + J[a * 3 + 1] * c.R[3 + b] + J[a * 3 + 2] * c.R[6 + b];
+    double cov[4];
+    for (int a = 0; a < 2; ++a)
+      for (int l = 0; l < 2; ++l) {
+        double acc = 0.0;
+        for (int j = 0; j < 3; ++j)
+          for (int k = 0; k < 3; ++k) acc += U[a * 3 + j] * Sig[j * 3 + k] * U[l * 3 + k];
+        cov[a * 2 + l] = acc;
+      }
+    cov[0] += DILATION;
+    cov[3] += DILATION;
+    const double det = cov[0] * cov[3] - cov[1] * cov[2];
+    const double L[4] = {cov[3] / det, -cov[1] / det, -cov[2] / det, cov[0] / det};
+    const double gl[4] = {raw[1], raw[2], raw[2], raw[3]};
+    // g_cov = -L gl L
+    double t[4], gc[4];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) t[a * 2 + b] = gl[a * 2] * L[b] + gl[a * 2 + 1] * L[2 + b];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) gc[a * 2 + b] = -(L[a * 2] * t[b] + L[a * 2 + 1] * t[2 + b]);
+    // dSigma = U^T g_cov U
+    double dS[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int p = 0; p < 2; ++p)
+          for (int q = 0; q < 2; ++q) acc += U[p * 3 + a] * gc[p * 2 + q] * U[q * 3 + b];
+        dS[a * 3 + b] = acc;
+      }
+    // d_u = (g_cov + g_cov^T) U Sigma ; d_j = d_u R_c^T
+    double US[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b)
+        US[a * 3 + b] = U[a * 3] * Sig[b] + U[a * 3 + 1] * Sig[3 + b] + U[a * 3 + 2] * Sig[6 + b];
+    double du[6];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b)
+        du[a * 3 + b] = (gc[a * 2] + gc[a]) * US[b] + (gc[a * 2 + 1] + gc[2 + a]) * US[3 + b];
+    double dj[6];
+    for (int a = 0; a < 2; ++a)
+      for (int k = 0; k < 3; ++k)
+        dj[a * 3 + k] = du[a * 3] * c.R[k * 3] + du[a * 3 + 1] * c.R[k * 3 + 1] + du[a * 3 + 2] * c.R[k * 3 + 2];
+    const double fx = c.fx, fy = c.fy, z2 = z * z, z3 = z2 * z;
+    const double dup = raw[4], dvp = raw[5];
+    double dv[3];
+    dv[0] = dj[2] * (-fx / z2) * (ox ? 1.0 : 0.0) + dup * fx / z;
+    dv[1] = dj[5] * (-fy / z2) * (oy ? 1.0 : 0.0) + dvp * fy / z;
+    dv[2] = dj[0] * (-fx / z2) + dj[4] * (-fy / z2) +
+            dj[2] * (fx * rx / z2 + (fx * x / z3) * (ox ? 1.0 : 0.0)) +
+            dj[5] * (fy * ry / z2 + (fy * y / z3) * (oy ? 1.0 : 0.0)) + dup * (-fx * x / z2) +
+            dvp * (-fy * y / z2);
+    float4* l4 = reinterpret_cast<float4*>(in.lacc + 12 * i);
+    float4 l0 = l4[0], l1 = l4[1], l2 = l4[2];
+    l0.x += (float)dS[0]; l0.y += (float)dS[1]; l0.z += (float)dS[2]; l0.w += (float)dS[4];
+    l1.x += (float)dS[5]; l1.y += (float)dS[8];
+    // dL/dmean (world) = dv R_c
+    l1.z += (float)(dv[0] * c.R[0] + dv[1] * c.R[3] + dv[2] * c.R[6]);
+    l1.w += (float)(dv[0] * c.R[1] + dv[1] * c.R[4] + dv[2] * c.R[7]);
+    l2.x += (float)(dv[0] * c.R[2] + dv[1] * c.R[5] + dv[2] * c.R[8]);
+    l2.y += raw[0];
+    l4[0] = l0; l4[1] = l1; l4[2] = l2;
+  }
+  if (in.dcol) return;
+  if (raw[10] != 0.f) in.cacc[i] += raw[10];
+  if (raw[11] != 0.f) in.cacc[n + i] += raw[11];
+  if (raw[12] != 0.f) in.cacc[2 * n + i] += raw[12];
+}
+
+// mode="splat" parameter chain (grad.py:93-104 _factored_grads with
+// F = Sigma = R diag(s^2) R^T, then _quat_grads): dL/dSigma -> scales,
+// rotations; dL/dmean and dL/dopacity pass through; thetas / kappas get 0.
+__global__ void __launch_bounds__(128) k_finalize_splat(FinalIn in, vg_grads g) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= in.n) return;
+  float4* l4 = reinterpret_cast<float4*>(in.lacc + 12 * i);
+  const float4 l0 = l4[0], l1 = l4[1], l2 = l4[2];
+  const float raw[10] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w, l2.x, l2.y};
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) any |= raw[k] != 0.f;
+  const bool add = g.accumulate != 0;
+  if (!any && add) return;
+  if (any) {
+    const float4 zf = make_float4(0.f, 0.f, 0.f, 0.f);
+    l4[0] = zf; l4[1] = zf; l4[2] = zf;
+  }
+  double ds[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0};
+  if (any) {
+    double R[9], qh[4];
+    quat_rotmat(in.rots + 4 * i, R, qh);
+    const float* sc = in.scales + 3 * i;
+    double s[3];
+    for (int k = 0; k < 3; ++k) s[k] = fmax((double)sc[k], SCALE_FLOOR);
+    const double G[9] = {raw[0], raw[1], raw[2], raw[1], raw[3], raw[4], raw[2], raw[4], raw[5]};
+    // d_scale = diag(R^T G R) * 2 s (live scales only)
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0.0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) acc += R[a * 3 + k] * G[a * 3 + b] * R[b * 3 + k];
+      ds[k] = ((double)sc[k] >= SCALE_FLOOR) ? acc * 2.0 * s[k] : 0.0;
+    }
+    // dL/dR = (G + G^T) R diag(s^2)
+    double dR[9];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += 2.0 * G[a * 3 + k] * R[k * 3 + b];
+        dR[a * 3 + b] = acc * s[b] * s[b];
+      }
+    const double w = qh[0], x = qh[1], y = qh[2], z = qh[3];
+    const double J[4][9] = {{0, -z, y, z, 0, -x, -y, x, 0},
+                            {0, y, z, y, -2 * x, -w, z, w, -2 * x},
+                            {-2 * y, x, w, x, 0, z, -w, z, -2 * y},
+                            {-2 * z, -w, x, w, -2 * z, y, x, y, 0}};
+    double dqh[4];
+    for (int k = 0; k < 4; ++k) {
+      double acc = 0;
+      for (int e = 0; e < 9; ++e) acc += dR[e] * 2.0 * J[k][e];
+      dqh[k] = acc;
+    }
+    const float* qf = in.rots + 4 * i;
+    const double qn = sqrt((double)qf[0] * qf[0] + (double)qf[1] * qf[1] + (double)qf[2] * qf[2] +
+                           (double)qf[3] * qf[3]);
+    const double rad = qh[0] * dqh[0] + qh[1] * dqh[1] + qh[2] * dqh[2] + qh[3] * dqh[3];
+    for (int k = 0; k < 4; ++k) dq[k] = (dqh[k] - qh[k] * rad) / qn;
+  }
+#define VG_PUT(ptr, idx, val) \
+  do { if (ptr) { float _v = (float)(val); if (add) ptr[idx] += _v; else ptr[idx] = _v; } } while (0)
+  for (int k = 0; k < 3; ++k) {
+    VG_PUT(g.d_means, 3 * i + k, raw[6 + k]);
+    VG_PUT(g.d_scales, 3 * i + k, ds[k]);
+  }
+  for (int k = 0; k < 4; ++k) VG_PUT(g.d_rotations, 4 * i + k, dq[k]);
+  VG_PUT(g.d_thetas, i, 0.0);
+  VG_PUT(g.d_kappas, i, 0.0);
+  VG_PUT(g.d_splat_opacities, i, raw[9]);
+#undef VG_PUT
 }
 
 // SH pull-back of the step's views: d_sh[i][l][ch] (+)= sum_v b_l(d_v) dRGB_v[ch]
@@ -174,13 +373,7 @@ __global__ void __launch_bounds__(256) k_color_out(int64_t n, float* cacc, float
   }
 }
 
-struct FinalIn {
-  int64_t n;
-  const float* scales;
-  const float* rots;
-  const float* thetas;
-  float* lacc;  // n * 12 (zeroed here)
-};
+
 
 __global__ void __launch_bounds__(128) k_finalize_params(FinalIn in, vg_grads g) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -264,18 +457,27 @@ __global__ void __launch_bounds__(128) k_finalize_params(FinalIn in, vg_grads g)
 
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,
-                            cudaStream_t st) {
+                            bool splat, cudaStream_t st) {
   if (n <= 0) return;
-  ViewAccIn in{n, s.means, s.sh, frame, acc, lacc, cacc, dcol, center};
+  ViewAccIn in{n, s.means, s.scales, s.rotations, s.sh, frame, acc, lacc, cacc, dcol, center};
+  if (splat) {
+    k_view_accumulate_splat<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, c);
+    return;
+  }
   k_view_accumulate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, c);
 }
 
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const float* dcol, const double* centers, int sh_views,
-                           const vg_grads& g, cudaStream_t st) {
+                           const vg_grads& g, bool splat, cudaStream_t st) {
   if (n <= 0) return 0;
   FinalIn in{n, s.scales, s.rotations, s.thetas, lacc};
-  k_finalize_params<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, g);
+  if (splat)
+    k_finalize_splat<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, g);
+  else
+    k_finalize_params<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, g);
+  if (!splat && g.d_splat_opacities && g.accumulate == 0)
+    cudaMemsetAsync(g.d_splat_opacities, 0, sizeof(float) * (size_t)n, st);
   const unsigned blocks = (unsigned)((n + 31) / 32);
   const int add = g.accumulate != 0;
   if (s.sh) {

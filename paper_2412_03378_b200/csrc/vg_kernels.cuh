@@ -38,8 +38,17 @@ struct BwdIO {
 };
 
 // gm (nullable): per binned Gaussian M and M (mean - centre) in float64, for sort_by="gamma"
+// splat: mode="splat" records (conic, opacity) and 3-sigma radii
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, ushort4* rect, float* frame, double* gm, cudaStream_t st);
+                       float* depth, ushort4* rect, float* frame, double* gm, bool splat,
+                       cudaStream_t st);
+// mode="splat" tile kernels (vg_splat.cu)
+void launch_splat_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                      const uint32_t* order, const BlendParams& p, float* color, float* final_t,
+                      int* n_contrib, int* n_act, cudaStream_t st);
+void launch_splat_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                      const uint32_t* order, const BlendParams& p, int loss, const BwdIO& io,
+                      cudaStream_t st);
 // deterministic-gradient mode (vg_det.cu)
 cudaError_t scan_u32(const uint32_t* in, uint32_t* out, void* scratch, uint32_t* total, int64_t n,
                      cudaStream_t st);
@@ -79,11 +88,11 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
 // SH scenes: dcol / center receive this view's dL/dRGB slab [3][n] and camera centre
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,
-                            cudaStream_t st);
+                            bool splat, cudaStream_t st);
 // returns the number of kernels launched; SH scenes fold the sh_views slabs of dcol
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const float* dcol, const double* centers, int sh_views,
-                           const vg_grads& g, cudaStream_t st);
+                           const vg_grads& g, bool splat, cudaStream_t st);
 
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
 // hand-written onesweep radix sort (vg_radix.cu); result buffer in *which

@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
                                                     const float* __restrict__ rots,
                                                     const float* __restrict__ thetas,
                                                     const float* __restrict__ colors,
-                                                    const float* __restrict__ sh, CamK c,
+                                                    const float* __restrict__ sh,
+                                                    const float* __restrict__ opac, CamK c,
                                                     double bin_cut, PrepOut o) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -32,6 +33,7 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   bool ok = make_frame(c, means + 3 * i, scales + 3 * i, rots + 4 * i, f);
   uint32_t cnt = 0;
   ushort4 rect = make_ushort4(1, 0, 0, 0);
+  double conic[3] = {0.0, 0.0, 0.0}, lam_max = 1.0;
   double kappa = kappa_of((double)thetas[i], f.s, nullptr, nullptr);
   if (ok) {
     // --- EWA screen covariance (raster.py:175-209) or orthographic projection
@@ -71,11 +73,16 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
     double half_tr = 0.5 * (cov[0] + cov[3]);
     double det = cov[0] * cov[3] - cov[1] * cov[2];
     double lam = half_tr + sqrt(fmax(half_tr * half_tr - det, 0.0));
+    lam_max = lam;
+    conic[0] = cov[3] / det;
+    conic[1] = -cov[1] / det;
+    conic[2] = cov[0] / det;
     double smax = fmax(fmax(f.s[0], f.s[1]), f.s[2]);
     double amp = SQRT_2PI * kappa * smax;
     double cut = fmax(bin_cut, 1e-12);
     double need = sqrt(2.0 * log(fmax(1.05 * amp / cut, 1.0)));
-    double mult = fmax(BASE_SIGMA, need + 0.5);
+    // splat alphas are bounded by the opacity <= 1: 3 sigma (raster.py:154-172)
+    double mult = opac ? BASE_SIGMA : fmax(BASE_SIGMA, need + 0.5);
     double r = mult * sqrt(lam);
     // --- tile rectangle (raster.py:233-244)
     double u = f.pu, v = f.pv;
@@ -93,6 +100,33 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
   o.rect[i] = rect;
   o.depth[i] = (float)f.v[2];
   if (!cnt) return;
+  if (opac) {
+    // splat record (vg_splat.cu): the conic (raster._inv2x2, raster.py:212-219),
+    // opacity, lambda_min(conic) for culling, colour
+    GRec g{};
+    g.u = f.pu;
+    g.v = f.pv;
+    g.P11 = (float)(conic[0]);
+    g.P21 = (float)(conic[1]);
+    g.P22 = (float)(conic[2]);
+    g.kap2 = opac[i];
+    g.amp = opac[i];
+    g.n1 = (float)(1.0 / lam_max);
+    if (colors) { g.cr = colors[3 * i]; g.cg = colors[3 * i + 1]; g.cb = colors[3 * i + 2]; }
+    if (sh) {
+      double d[3] = {means[3 * i] - c.center[0], means[3 * i + 1] - c.center[1],
+                     means[3 * i + 2] - c.center[2]};
+      const double dn = sqrt(dot3(d, d));
+      d[0] /= dn; d[1] /= dn; d[2] /= dn;
+      double b[16], rgb[3] = {0.0, 0.0, 0.0};
+      sh_basis(d, b);
+      for (int l = 0; l < 16; ++l)
+        for (int ch = 0; ch < 3; ++ch) rgb[ch] += b[l] * sh[48 * i + 3 * l + ch];
+      g.cr = (float)rgb[0]; g.cg = (float)rgb[1]; g.cb = (float)rgb[2];
+    }
+    o.rec[i] = g;
+    return;
+  }
   if (o.gm) {
     // core.precision_matrices (core.py:111-119) and raster.prepare's
     // minv_delta (raster.py:276-280), for the gamma re-sort
@@ -157,12 +191,13 @@ __global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __re
 }
 
 void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_cut, GRec* rec,
-                       float* depth, ushort4* rect, float* frame, double* gm, cudaStream_t st) {
+                       float* depth, ushort4* rect, float* frame, double* gm, bool splat,
+                       cudaStream_t st) {
   if (n <= 0) return;
   PrepOut o{rec, depth, rect, gm, frame};
   int blocks = (int)((n + 255) / 256);
   k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
-                                       s.sh, c, bin_cut, o);
+                                       s.sh, splat ? s.splat_opacities : nullptr, c, bin_cut, o);
 }
 
 }  // namespace vg

@@ -21,7 +21,7 @@ from .tomo import TOMO_BIN_CUT
 
 class Engine:
     def __init__(self, device=None, early_stop=EARLY_STOP_T, alpha_cut=ALPHA_CUT,
-                 alpha_clamp=ALPHA_CLAMP, deterministic=False, sort_by="depth"):
+                 alpha_clamp=ALPHA_CLAMP, deterministic=False, sort_by="depth", mode="analytic"):
         torch = _lib._require_cuda()
         self.torch = torch
         self.ctx = _lib.Context(device)
@@ -29,6 +29,7 @@ class Engine:
         self.flags = (early_stop, alpha_cut, alpha_clamp)
         self.deterministic = deterministic   # fixed-order gradient sums (vg_det.cu)
         self.sort_by = sort_by
+        self.mode = mode                     # "analytic" or "splat" (the EWA comparator)
         self.lib = _lib.load()
         self._bufs = {}
         self.cam = None
@@ -64,7 +65,7 @@ class Engine:
         es, ac, cl = self.flags
         bin_cut = TOMO_BIN_CUT if tomo else ac
         opt = _lib.make_options(TILE_SIZE, es, ac, cl, bin_cut, sort_by=self.sort_by,
-                                deterministic=self.deterministic)
+                                deterministic=self.deterministic, mode=self.mode)
         c = _lib.make_camera(cam, _lib.VG_PARALLEL if parallel else _lib.VG_PINHOLE,
                              extent if parallel else 0.0)
         s = ds.struct()

@@ -77,7 +77,7 @@ class GradBuffers:
     d_background and the visibility mask."""
 
     LAYOUT = (("d_means", 3), ("d_scales", 3), ("d_rotations", 4), ("d_thetas", 1),
-              ("d_colors", 3), ("d_kappas", 1))
+              ("d_colors", 3), ("d_kappas", 1), ("d_splat_opacities", 1))
 
     def __init__(self, n, device, with_sh=False):
         import torch
@@ -98,7 +98,7 @@ class GradBuffers:
         """vg_grads view; accumulate: False/VG_OVERWRITE, True/VG_ADD or VG_DEFER."""
         g = _lib.VgGrads()
         for name in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_kappas",
-                     "d_background"):
+                     "d_background", "d_splat_opacities"):
             setattr(g, name, _lib.ptr(self.views[name]).value)
         g.d_sh = _lib.ptr(self.views["d_sh"]).value if self.views["d_sh"] is not None else None
         g.visible = _lib.ptr(self.visible).value
@@ -117,11 +117,6 @@ class GradBuffers:
         sg.d_background = _out(self.views["d_background"], torch_out)
         vis = self.visible[:n]
         sg.visible = vis.bool() if torch_out else vis.cpu().numpy().astype(bool)
-        if torch_out:
-            import torch
-            sg.d_splat_opacities = torch.zeros(n, dtype=torch.float32, device=self.flat.device)
-        else:
-            sg.d_splat_opacities = np.zeros(n)
         if self.views["d_sh"] is not None:
             sg.d_sh = _out(self.views["d_sh"], torch_out)
         return sg
@@ -168,7 +163,7 @@ def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
     bufs = GradBuffers(dscene.n, dev, with_sh=dscene.sh is not None)
     g = bufs.struct(accumulate=False)
     opt = _lib.make_options(TILE_SIZE, early_stop, alpha_cut, alpha_clamp, prep.alpha_cut,
-                            deterministic=deterministic)
+                            deterministic=deterministic, mode=prep.mode)
     _lib.check(_lib.load().vg_set_options(prep.ctx.handle, ctypes.byref(opt)), "vg_set_options")
     _lib.check(_lib.load().vg_render_backward(prep.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),
                                               _lib.ptr(dc), _lib.ptr(dt), ctypes.byref(g),

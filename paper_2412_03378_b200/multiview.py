@@ -73,7 +73,8 @@ class ViewShardedStep:
         self.engines = [engine]
         if pipeline:
             self.engines.append(Engine(engine.ctx.device, *engine.flags,
-                                       deterministic=engine.deterministic, sort_by=engine.sort_by))
+                                       deterministic=engine.deterministic, sort_by=engine.sort_by,
+                                       mode=engine.mode))
         self.ds = dscene
         self.cams = cameras
         self.targets = targets

@@ -9,9 +9,9 @@ Array types: a scene whose arrays are numpy (e.g. a reference
 `volgauss.Scene`) gets numpy float64 outputs, exactly like the reference; a
 scene whose arrays are CUDA torch tensors gets CUDA torch outputs with no host
 round trip.  sort_by='gamma' re-sorts every tile list by gamma along the
-tile's central ray on the device (raster.py:299-312).  Unsupported reference
-options raise NotImplementedError: tile_size != 16 and mode='splat' (the EWA
-comparator, out of scope); unknown modes / sort keys raise ValueError as in
+tile's central ray on the device (raster.py:299-312); mode='splat' runs the
+EWA comparator (raster.py:353-361) on the same tile pipeline.  tile_size != 16
+raises NotImplementedError; unknown modes / sort keys raise ValueError as in
 raster.py:268-269, 293-294.
 """
 
@@ -126,8 +126,6 @@ def _is_torch(x):
 def _check_mode(mode, sort_by, tile_size):
     if mode not in ("analytic", "splat"):
         raise ValueError(f"unknown mode {mode!r}")
-    if mode == "splat":
-        raise NotImplementedError("mode='splat' (EWA comparator) is outside this build's hot path")
     if sort_by not in ("depth", "gamma"):
         raise ValueError(f"unknown sort key {sort_by!r}")
     if int(tile_size) != TILE_SIZE:
@@ -161,6 +159,10 @@ class DeviceScene:
         self.colors = conv(colors, (n, 3)) if colors is not None else None
         sh = getattr(scene, "sh", None)
         self.sh = conv(sh, (n, 16, 3)) if sh is not None else None
+        op = getattr(scene, "splat_opacities", None)
+        # raster.Scene's default splat opacity is 0.5 (raster.py:49-50)
+        self.splat_opacities = conv(op, (n,)) if op is not None else \
+            torch.full((n,), 0.5, dtype=torch.float32, device=dev)
         bg = scene.background
         self.background = np.asarray(bg.detach().cpu().numpy() if _is_torch(bg) else bg,
                                      dtype=np.float64).reshape(3)
@@ -173,6 +175,7 @@ class DeviceScene:
         s.thetas = _lib.ptr(self.thetas).value
         s.colors = _lib.ptr(self.colors).value if self.colors is not None else None
         s.sh = _lib.ptr(self.sh).value if self.sh is not None else None
+        s.splat_opacities = _lib.ptr(self.splat_opacities).value
         s.n = self.n
         for i in range(3):
             s.background[i] = float(self.background[i])
@@ -243,8 +246,10 @@ class Prep:
         return z.cpu().numpy()
 
 
-def _options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth"):
-    return _lib.make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by)
+def _options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by="depth",
+             mode="analytic"):
+    return _lib.make_options(tile_size, early_stop, alpha_cut, alpha_clamp, bin_cut, sort_by,
+                             mode=mode)
 
 
 def _stream(dev):
@@ -261,7 +266,7 @@ def prepare(scene, camera, mode="analytic", tile_size=TILE_SIZE, sort_by="depth"
     dscene = scene if isinstance(scene, DeviceScene) else DeviceScene(scene)
     ctx = _ctx if _ctx is not None else _lib.Context(dscene.device.index)
     bin_cut = alpha_cut if _bin_cut is None else _bin_cut
-    opt = _options(tile_size, EARLY_STOP_T, alpha_cut, ALPHA_CLAMP, bin_cut, sort_by)
+    opt = _options(tile_size, EARLY_STOP_T, alpha_cut, ALPHA_CLAMP, bin_cut, sort_by, mode)
     cam = _lib.make_camera(camera, _projection, _extent)
     s = dscene.struct()
     import ctypes

@@ -19,8 +19,6 @@ def test_mode_and_sort_validation():
     with pytest.raises(ValueError):
         vg.render(scene, cam, sort_by="nonsense")
     with pytest.raises(NotImplementedError):
-        vg.render(scene, cam, mode="splat")
-    with pytest.raises(NotImplementedError):
         vg.render(scene, cam, tile_size=8)
 
 
@@ -31,6 +29,10 @@ def test_no_cpu_fallback():
         vg.render(scene, cam)
     with pytest.raises(RuntimeError):
         vg.tomo_forward(scene, cam)
+    with pytest.raises(RuntimeError):
+        vg.render(scene, cam, mode="splat")
+    with pytest.raises(RuntimeError):
+        vg.render(scene, cam, sort_by="gamma")
 
 
 def test_scene_container_mirrors_reference():
