@@ -308,6 +308,16 @@ int vg_densify_apply(const vg_densify_args* args, const void* scratch,
                      const uint32_t* counts_host, const double* xi, vg_train_state* out,
                      void* stream);
 
+/* oracle.raymarch_image (oracle.py:80-161): ground-truth midpoint-rule
+ * quadrature of the volume rendering equation through the full mixture
+ * density, independent of the closed-form path (validation tool; brute force
+ * over all primitives, float64).  t_min / t_max: NaN = the reference's
+ * auto-fitted bounds (support_sigmas beta around gamma, clipped to t >= 0).
+ * color (H,W,3) and final_t (H,W) device float32. */
+int vg_raymarch(const vg_scene* scene, const vg_camera* cam, int32_t n_steps,
+                double support_sigmas, double t_min, double t_max, float* color, float* final_t,
+                void* stream);
+
 /* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and
  * MUFU ex2 ops/s over all SMs of `device`. */
 int vg_probe_peaks(int32_t device, double* fp32_per_s, double* mufu_per_s);

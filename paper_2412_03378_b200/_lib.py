@@ -98,6 +98,8 @@ EXPORTS = {
     "vg_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "vg_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "vg_probe_peaks": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "vg_raymarch": (C.c_int, [C.POINTER(VgScene), C.POINTER(VgCamera), C.c_int32, C.c_double,
+                              C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vg_adam_step": (C.c_int, [C.POINTER(VgTrainState), C.POINTER(VgGrads), C.POINTER(VgAdamHparams),
                                C.c_void_p, C.c_void_p]),
     "vg_densify_scratch_bytes": (C.c_size_t, [C.c_int64]),
