@@ -305,15 +305,14 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
     // the depth bits over the identity permutation (stable => index order)
     uint32_t* ids0 = (uint32_t*)c->perm.p + n;
     uint32_t* ids1 = (uint32_t*)c->perm.p;
-    launch_iota(n, ids0, st);
-    VG_LAUNCHED(c, 1);
     uint32_t* perm = ids1;
     {
       ProfScope ps(c, VG_K_SORT, st);
       VG_TRY(ensure(c->dsort_tmp, radix_temp_bytes(n, 32), st));
       int which = 0, nl = 0;
       VG_CUDA(radix_sort_u32(c->dsort_tmp.p, c->dsort_tmp.bytes, (uint32_t*)c->depth.p,
-                             (uint32_t*)c->dkey.p, ids0, ids1, n, 32, &which, &nl, st));
+                             (uint32_t*)c->dkey.p, ids0, ids1, n, 32, &which, &nl, st,
+                             /*identity_values=*/true));
       c->launches += nl;
       perm = which ? ids1 : ids0;
     }

@@ -97,9 +97,10 @@ int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cac
 void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
 // hand-written onesweep radix sort (vg_radix.cu); result buffer in *which
 size_t radix_temp_bytes(int64_t n, int key_bits);
+// identity_values: v0 is not read, the values start as 0..n-1 (stable index order)
 cudaError_t radix_sort_u32(void* tmp, size_t tmp_bytes, uint32_t* k0, uint32_t* k1, uint32_t* v0,
                            uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
-                           cudaStream_t st);
+                           cudaStream_t st, bool identity_values = false);
 cudaError_t radix_sort_u16(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
                            uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
                            cudaStream_t st);

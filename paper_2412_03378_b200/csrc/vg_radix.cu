@@ -45,27 +45,34 @@ inline size_t temp_bytes(int64_t n, int key_bits) {
 template <typename K>
 __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, int64_t n, int passes,
                                                   uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[4][BINS];
-  for (int i = threadIdx.x; i < 4 * BINS; i += THREADS) (&h[0][0])[i] = 0;
+  // per-warp sub-histograms: shared atomics only collide within a warp, and a
+  // digit shared by the whole warp (the near-constant top byte of float
+  // depths) is added once by lane 0
+  __shared__ uint32_t h[WARPS][4][BINS];
+  for (int i = threadIdx.x; i < WARPS * 4 * BINS; i += THREADS) (&h[0][0][0])[i] = 0;
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * THREADS;
   const int64_t n_round = (n + stride - 1) / stride * stride;  // whole warps iterate together
-  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
   for (int64_t i = (int64_t)blockIdx.x * THREADS + threadIdx.x; i < n_round; i += stride) {
     const bool valid = i < n;
     const uint32_t k = valid ? (uint32_t)keys[i] : 0u;
     const unsigned vm = __ballot_sync(0xffffffffu, valid);
     for (int p = 0; p < passes; ++p) {
-      // warp-aggregated: one shared atomic per distinct digit in the warp
-      // (the top byte of float depths is nearly constant)
       const uint32_t d = (k >> (BITS * p)) & (BINS - 1);
-      const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu) & vm;
-      if (valid && (peers & lt) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+      if (vm == 0xffffffffu && __all_sync(0xffffffffu, d == d0)) {
+        if (lane == 0) h[warp][p][d0] += 32u;
+      } else if (valid) {
+        atomicAdd(&h[warp][p][d], 1u);
+      }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * BINS; i += THREADS) {
-    const uint32_t v = (&h[0][0])[i];
+    uint32_t v = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) v += (&h[w][0][0])[i];
     if (v) atomicAdd(hist + i, v);
   }
 }
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_pass(const K* __restrict__ kin, 
     const int64_t idx = wbase + i * 32;
     if (idx < n) {
       s_keys[rank[i]] = kin[idx];
-      s_vals[rank[i]] = vin[idx];
+      s_vals[rank[i]] = vin ? vin[idx] : (uint32_t)idx;  // NULL: identity values
     }
   }
   __syncthreads();
@@ -227,9 +234,12 @@ __global__ void __launch_bounds__(THREADS, 3) k_pass(const K* __restrict__ kin, 
 
 template <typename K>
 cudaError_t sort_pairs(void* tmp, size_t tmp_bytes, K* k0, K* k1, uint32_t* v0, uint32_t* v1,
-                       int64_t n, int key_bits, int* which, int* launches, cudaStream_t st) {
+                       int64_t n, int key_bits, int* which, int* launches, cudaStream_t st,
+                       bool identity = false) {
   *which = 0;
-  if (n <= 1) return cudaSuccess;
+  if (n <= 1) {  // nothing to sort; the identity of one item is 0
+    return (identity && n == 1) ? cudaMemsetAsync(v0, 0, sizeof(uint32_t), st) : cudaSuccess;
+  }
   const int passes = (key_bits + BITS - 1) / BITS;
   const int64_t tiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
   if (tmp_bytes < temp_bytes(n, key_bits)) return cudaErrorInvalidValue;
@@ -241,7 +251,7 @@ cudaError_t sort_pairs(void* tmp, size_t tmp_bytes, K* k0, K* k1, uint32_t* v0, 
   cudaError_t e = cudaMemsetAsync(
       tmp, 0, sizeof(uint32_t) * (2 * (size_t)passes * BINS + 8 + (size_t)passes * tiles * BINS), st);
   if (e != cudaSuccess) return e;
-  int hist_blocks = (int)((n + THREADS * 16 - 1) / (THREADS * 16));
+  int hist_blocks = (int)((n + THREADS * 8 - 1) / (THREADS * 8));
   if (hist_blocks > 1184) hist_blocks = 1184;
   k_hist<K><<<hist_blocks, THREADS, 0, st>>>(k0, n, passes, hist);
   k_scan<<<passes, BINS, 0, st>>>(hist, base);
@@ -251,7 +261,8 @@ cudaError_t sort_pairs(void* tmp, size_t tmp_bytes, K* k0, K* k1, uint32_t* v0, 
   uint32_t* vin = v0;
   uint32_t* vout = v1;
   for (int p = 0; p < passes; ++p) {
-    k_pass<K><<<(unsigned)tiles, THREADS, 0, st>>>(kin, kout, vin, vout, n, BITS * p,
+    k_pass<K><<<(unsigned)tiles, THREADS, 0, st>>>(kin, kout, (p == 0 && identity) ? nullptr : vin,
+                                                   vout, n, BITS * p,
                                                    base + p * BINS,
                                                    status + (size_t)p * tiles * BINS, counters + p,
                                                    min(BITS, key_bits - BITS * p));
@@ -269,9 +280,9 @@ size_t radix_temp_bytes(int64_t n, int key_bits) { return radix::temp_bytes(n, k
 
 cudaError_t radix_sort_u32(void* tmp, size_t tmp_bytes, uint32_t* k0, uint32_t* k1, uint32_t* v0,
                            uint32_t* v1, int64_t n, int key_bits, int* which, int* launches,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool identity_values) {
   return radix::sort_pairs<uint32_t>(tmp, tmp_bytes, k0, k1, v0, v1, n, key_bits, which, launches,
-                                     st);
+                                     st, identity_values);
 }
 
 cudaError_t radix_sort_u16(void* tmp, size_t tmp_bytes, uint16_t* k0, uint16_t* k1, uint32_t* v0,
