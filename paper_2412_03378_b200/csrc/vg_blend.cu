@@ -33,6 +33,14 @@
 // (16 shuffles) and added with one 13-lane red.global.add per warp.
 #include "vg_blend.cuh"
 
+// minimum resident CTAs per SM requested from ptxas (register budget); A/B knobs
+#ifndef VG_FWD_MINB
+#define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
+#endif
+#ifndef VG_BWD_MINB
+#define VG_BWD_MINB 7   // <= 72 registers
+#endif
+
 namespace vg {
 
 struct __align__(16) SRec {
@@ -168,7 +176,7 @@ __device__ unsigned long long g_vg_stats[4];  // debug: processed / visible warp
 // roofline statistics); the training step's forward skips them -- the
 // backward re-derives activity from its own transmittance replay.
 template <bool STOP, bool CUT, bool STATS = false, bool COUNTS = true>
-__global__ void __launch_bounds__(NT) k_render_fwd(const GRec* __restrict__ rec,
+__global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
                                                    const uint32_t* __restrict__ order,
@@ -400,7 +408,7 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
 // K6 backward blend (grad.backward tile_job + e_chain)
 
 template <bool CUT, int LOSS, bool DET = false>
-__global__ void __launch_bounds__(NT) k_render_bwd(const GRec* __restrict__ rec,
+__global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
                                                    const uint32_t* __restrict__ order,
