@@ -12,7 +12,10 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr float C_HALF_LOG2E = 0.72134752044448170f;  // 0.5 * log2(e)
 constexpr int ACC_STRIDE = 16;                         // floats per Gaussian accumulator
 constexpr int NT = 128;                                // threads per tile CTA
-constexpr int BATCH = 256;                             // staged records per batch
+#ifndef VG_BATCH
+#define VG_BATCH 256
+#endif
+constexpr int BATCH = VG_BATCH;                        // staged records per batch
 
 // ---------------------------------------------------------------------------
 // packed FP32x2 helpers (sm_100a FFMA2 / FMUL2 / FADD2)
