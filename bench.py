@@ -326,9 +326,26 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
     t = ms * 1e-3 / steps                       # seconds per step in this kernel
     fp_ops = fp_u * A + live_u * L
     mu_ops = mu_u * A
+    tr = load_traffic(dom) or {}
+    launch_s = t / max(cnt / steps, 1.0)           # average duration of one launch
     out = {"kernel": dom, "active_pair_pixels_per_step": A, "live_pair_pixels_per_step": L,
            "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
-           "traffic": load_traffic(dom)}
+           "traffic": tr.get("bytes_per_launch"),
+           "traffic_source": "profiles/traffic.json (ncu --set full, dram read + write per launch)"}
+    if tr.get("bytes_per_launch"):
+        # not an HBM-bound kernel: the DRAM traffic per launch over its live duration
+        hbm = measured_hbm_gbs()
+        gbs = tr["bytes_per_launch"] / launch_s / 1e9
+        out["hbm_check"] = {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if hbm else None,
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    if tr.get("warp_instructions_per_launch") and mufu_peak:
+        # executed-work roofline: warp-instruction issue rate vs 148 SMs x 4 schedulers x f
+        f_clk = mufu_peak / (148 * 16)
+        issue_peak = 148 * 4 * f_clk
+        ach = tr["warp_instructions_per_launch"] / launch_s
+        out["issue_check"] = {"achieved": ach / 1e9, "peak": issue_peak / 1e9,
+                              "unit": "G warp-instructions/s", "frac": ach / issue_peak,
+                              "note": "ncu-counted instructions of one launch over the live launch time"}
     if fp32_peak and mufu_peak:
         f_fp = fp_ops / t / fp32_peak
         f_mu = mu_ops / t / mufu_peak
@@ -342,6 +359,14 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
         out["frac_mufu"] = f_mu
         out["peak_source"] = "vg_probe_peaks on this GPU at the live clock (FFMA and MUFU.EX2 loops)"
     return out
+
+
+def measured_hbm_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0  # the profiling recipe's fallback
 
 
 def load_traffic(kernel):
