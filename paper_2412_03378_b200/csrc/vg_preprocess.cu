@@ -19,7 +19,11 @@ struct PrepOut {
   float* frame;        // e1, e2, e3 in whitened-local coordinates (12 floats)
 };
 
-__global__ void __launch_bounds__(256) k_preprocess(int64_t n, const float* __restrict__ means,
+#ifndef VG_PRE_MINB
+#define VG_PRE_MINB 3  // <= 80 registers: 3 CTAs per SM (A/B: tools/ab_bench.sh, -8%)
+#endif
+
+__global__ void __launch_bounds__(256, VG_PRE_MINB) k_preprocess(int64_t n, const float* __restrict__ means,
                                                     const float* __restrict__ scales,
                                                     const float* __restrict__ rots,
                                                     const float* __restrict__ thetas,

@@ -65,13 +65,16 @@ class ViewShardedStep:
     buffer)."""
 
     def __init__(self, engine, dscene, cameras, targets, *, world=1, rank=0, tomography=False,
-                 parallel=False, extent=1.6, group=None, pipeline=True):
+                 parallel=False, extent=1.6, group=None, pipeline=True, contexts=None):
         import torch
         from .engine import Engine
         self.torch = torch
         self.eng = engine
         self.engines = [engine]
-        if pipeline:
+        import os
+        # contexts in flight: binning runs up to (contexts - 1) views ahead of the blend
+        n_ctx = contexts if contexts is not None else int(os.environ.get("VG_CONTEXTS", "2"))
+        for _ in range((max(2, n_ctx) if pipeline else 1) - 1):
             self.engines.append(Engine(engine.ctx.device, *engine.flags,
                                        deterministic=engine.deterministic, sort_by=engine.sort_by,
                                        mode=engine.mode))
@@ -138,15 +141,20 @@ class ViewShardedStep:
         if self.side is not None:
             # the scene (and zeroed buffers) come from the main stream
             self.side.wait_stream(self.torch.cuda.current_stream(self.eng.device))
-        self._bin(0, views[0])
+        ahead = ne - 1                              # views binned ahead of the blend
+        for j in range(min(ahead, len(views)) if ahead else 1):
+            self._bin(j % ne, views[j])
         for j, v in enumerate(views):
             cur = j % ne
+            if not ahead and j > 0:
+                self._bin(cur, v)
             self._blend(cur, v)                     # enqueued before the host waits below
-            if j + 1 < len(views):
-                nxt = (j + 1) % ne
-                if self.side is not None and j >= 1:
-                    self.side.wait_event(self.ev_free[nxt])   # its previous view is done
-                self._bin(nxt, views[j + 1])
+            nxt = j + ahead
+            if ahead and nxt < len(views):
+                i = nxt % ne
+                if self.side is not None and nxt >= ne:
+                    self.side.wait_event(self.ev_free[i])   # its previous view is done
+                self._bin(i, views[nxt])
 
     def _finish(self):
         for i in sorted(getattr(self, "_used", ())):
