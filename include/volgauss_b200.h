@@ -189,7 +189,8 @@ int vg_render_backward_l2(vg_context* ctx, const float* color, const float* fina
                           void* stream);
 
 /* Per-pixel count of composited (active) entries of the last forward,
- * int32 (H,W) -- the backward replay bound, also the roofline's A count. */
+ * int32 (H,W) -- the roofline's A count; needs a counting forward
+ * (n_contrib != NULL). */
 int vg_n_active(vg_context* ctx, int32_t* out, void* stream);
 
 /* tomo.tomo_forward (tomo.py:34-57): line-integral image (H,W).  Pass
