@@ -608,3 +608,35 @@ def test_analytic_render_matches_ground_truth_on_separated_scene():
     col, tf = groundtruth.raymarch_image(scene, cam)
     assert np.max(np.abs(out.color - col)) < 1e-3
     assert np.max(np.abs(out.final_transmittance - tf)) < 1e-3
+
+
+@pytest.mark.parametrize("mode", ["analytic", "splat"])
+@pytest.mark.parametrize("sort_by", ["depth", "gamma"])
+def test_single_and_empty_scenes_all_modes(mode, sort_by):
+    """Degenerate sizes through every mode / order / reduction combination:
+    one primitive (the depth sort's n == 1 path), an empty scene (background
+    only, d_background = sum of d_color, grad.py:126-128)."""
+    from types import SimpleNamespace
+    from oracle import splat_oracle as SO
+    cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=24, fov_x_deg=60.0)
+    one = SimpleNamespace(means=np.array([[0.1, -0.05, 0.2]]), scales=np.array([[0.3, 0.2, 0.25]]),
+                          rotations=np.array([[0.9, 0.1, 0.2, 0.3]]), thetas=np.array([0.6]),
+                          colors=np.array([[0.8, 0.3, 0.1]]), splat_opacities=np.array([0.7]),
+                          background=np.array([0.1, 0.2, 0.3]))
+    rng = np.random.default_rng(5)
+    dc = rng.uniform(-1, 1, (24, 40, 3))
+    out = vg().render(one, cam, mode=mode, sort_by=sort_by)
+    ref = (SO.render(one, cam) if mode == "splat" else O.render(one, cam)).color
+    np.testing.assert_allclose(out.color, ref, rtol=1e-3, atol=1e-4)
+    for det in (True, False):
+        g = vg().backward(one, cam, dc, mode=mode, sort_by=sort_by, deterministic=det)
+        rg = SO.backward(one, cam, dc) if mode == "splat" else O.backward(one, cam, dc)
+        for f in ("d_means", "d_scales", "d_rotations", "d_colors", "d_background"):
+            check_field(getattr(g, f), getattr(rg, f), f"one {mode} {sort_by} {det} {f}")
+    empty = SimpleNamespace(means=np.zeros((0, 3)), scales=np.zeros((0, 3)), rotations=np.zeros((0, 4)),
+                            thetas=np.zeros(0), colors=np.zeros((0, 3)), splat_opacities=np.zeros(0),
+                            background=np.array([0.1, 0.2, 0.3]))
+    out = vg().render(empty, cam, mode=mode, sort_by=sort_by)
+    np.testing.assert_allclose(out.color, np.broadcast_to([0.1, 0.2, 0.3], (24, 40, 3)), atol=1e-7)
+    g = vg().backward(empty, cam, dc, mode=mode, sort_by=sort_by)
+    np.testing.assert_allclose(g.d_background, dc.reshape(-1, 3).sum(axis=0), rtol=1e-5)
