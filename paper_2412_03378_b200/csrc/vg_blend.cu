@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
 // (Gaussian, tile) pair and walks the tile's 256 pixels -- d_image staged once
 // per tile in shared memory and read as a broadcast -- accumulating its 10
 // gradient sums in registers; one 10-lane-op atomic flush per pair.
-template <int RAY, int LOSS>
+template <int RAY, int LOSS, bool DET = false>
 __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
                                                  const uint32_t* __restrict__ vals,
                                                  const uint2* __restrict__ ranges,
@@ -545,7 +545,9 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
                                                  const float* __restrict__ target,
                                                  float loss_scale, double* loss_sum,
                                                  float* __restrict__ acc,
-                                                 uint8_t* __restrict__ visible) {
+                                                 uint8_t* __restrict__ visible,
+                                                 float* __restrict__ det_part,
+                                                 double* __restrict__ det_loss) {
   __shared__ SRec sm[BATCH];
   __shared__ float sde[TILE_PIX];
   __shared__ float slp[TILE_PIX];
@@ -569,7 +571,8 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
     sde[q] = de;
     slp[q] = RAY == VG_PINHOLE ? pixel_lp(p, col, row) : 0.f;
   }
-  if (LOSS) block_flush(0.f, 0.f, 0.f, lossv, nullptr, loss_sum);
+  // deterministic mode: this tile's loss partial, summed in tile order later
+  if (LOSS) block_flush(0.f, 0.f, 0.f, lossv, nullptr, DET ? det_loss + tile : loss_sum, DET);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     __syncthreads();
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
@@ -636,8 +639,16 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
       float* o = acc + (size_t)gid * ACC_STRIDE;
       const float vv[10] = {a0, a1, a2, a3, a4, a5, b0, b1, b2, hs};
 #pragma unroll
-      for (int q = 0; q < 10; ++q)
-        if (vv[q] != 0.f) atomicAdd(o + q, vv[q]);
+      if (DET) {
+        // the pair's own slot (warp slot 0 of its list position; vg_det.cu)
+        float* sl = det_part + (size_t)(base + k) * (NT / 32) * ACC_STRIDE;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) sl[q] = vv[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 10; ++q)
+          if (vv[q] != 0.f) atomicAdd(o + q, vv[q]);
+      }
       if (gmax > 0.f && s.b.w > 0.f) visible[gid] = 1;
     }
   }
@@ -702,15 +713,20 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
                      const float* d_image, const float* image, const float* target,
                      float loss_scale, double* loss_sum, float* acc, uint8_t* visible,
-                     cudaStream_t st) {
-#define VG_TB(R, L)                                                                            \
-  k_tomo_bwd<R, L><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, d_image, image, target, \
-                                           loss_scale, loss_sum, acc, visible)
-  if (ray == VG_PINHOLE) {
-    if (loss) VG_TB(VG_PINHOLE, 1); else VG_TB(VG_PINHOLE, 0);
-  } else {
-    if (loss) VG_TB(VG_PARALLEL, 1); else VG_TB(VG_PARALLEL, 0);
-  }
+                     float* det_part, double* det_loss, cudaStream_t st) {
+#define VG_TB(R, L, D)                                                                            \
+  k_tomo_bwd<R, L, D><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, d_image, image, target, \
+                                              loss_scale, loss_sum, acc, visible, det_part, det_loss)
+#define VG_TB2(D)                                                       \
+  do {                                                                  \
+    if (ray == VG_PINHOLE) {                                            \
+      if (loss) VG_TB(VG_PINHOLE, 1, D); else VG_TB(VG_PINHOLE, 0, D);  \
+    } else {                                                            \
+      if (loss) VG_TB(VG_PARALLEL, 1, D); else VG_TB(VG_PARALLEL, 0, D); \
+    }                                                                   \
+  } while (0)
+  if (det_part) VG_TB2(true); else VG_TB2(false);
+#undef VG_TB2
 #undef VG_TB
 }
 

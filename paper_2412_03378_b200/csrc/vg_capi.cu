@@ -597,6 +597,31 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   return VG_OK;
 }
 
+// Deterministic mode: the Gaussian -> slot map of the current lists (once per
+// prepare) and zeroed per-(entry, warp) slots for one backward.
+static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cudaStream_t st) {
+  const int64_t n = c->scene.n, P = c->pairs;
+  if (!c->det_ready) {
+    VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
+    VG_TRY(ensure(c->det_off, sizeof(uint32_t) * ((size_t)n + 1), st));
+    VG_TRY(ensure(c->det_slot, sizeof(uint32_t) * (size_t)P, st));
+    VG_TRY(ensure(c->det_scan, scan_u32_scratch_bytes(n) + 16, st));
+    VG_CUDA(det_prepare(n, (const ushort4*)c->rect.p, (const uint2*)c->ranges.p, c->vals,
+                        c->n_tiles, c->cam.ntx, (uint32_t*)c->det_cnt.p, (uint32_t*)c->det_off.p,
+                        (uint32_t*)c->det_slot.p, c->det_scan.p, (uint32_t*)c->det_off.p + n, st));
+    c->det_ready = true;
+  }
+  VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
+  VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+  VG_TRY(ensure(c->det_bg, sizeof(float) * 3 * (size_t)c->n_tiles, st));
+  VG_TRY(ensure(c->det_loss, sizeof(double) * (size_t)c->n_tiles, st));
+  VG_CUDA(cudaMemsetAsync(c->det_bg.p, 0, sizeof(float) * 3 * (size_t)c->n_tiles, st));
+  part = (float*)c->det_part.p;
+  bg = (float*)c->det_bg.p;
+  loss = (double*)c->det_loss.p;
+  return VG_OK;
+}
+
 static int render_bwd_common(vg_context* c, const float* color, const float* final_t,
                              const float* d_color, const float* d_t, const float* target,
                              double* loss_sum, vg_grads* g, void* stream) {
@@ -623,26 +648,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     io.visible = (uint8_t*)c->offset.p;
   }
   const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
-  if (det) {
-    const int64_t n = c->scene.n, P = c->pairs;
-    if (!c->det_ready) {
-      VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
-      VG_TRY(ensure(c->det_off, sizeof(uint32_t) * ((size_t)n + 1), st));
-      VG_TRY(ensure(c->det_slot, sizeof(uint32_t) * (size_t)P, st));
-      VG_TRY(ensure(c->det_scan, scan_u32_scratch_bytes(n) + 16, st));
-      VG_CUDA(det_prepare(n, (const ushort4*)c->rect.p, (const uint2*)c->ranges.p, c->vals,
-                          c->n_tiles, c->cam.ntx, (uint32_t*)c->det_cnt.p, (uint32_t*)c->det_off.p,
-                          (uint32_t*)c->det_slot.p, c->det_scan.p, (uint32_t*)c->det_off.p + n, st));
-      c->det_ready = true;
-    }
-    VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
-    VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
-    VG_TRY(ensure(c->det_bg, sizeof(float) * 3 * (size_t)c->n_tiles, st));
-    VG_TRY(ensure(c->det_loss, sizeof(double) * (size_t)c->n_tiles, st));
-    io.det_part = (float*)c->det_part.p;
-    io.det_bg = (float*)c->det_bg.p;
-    io.det_loss = (double*)c->det_loss.p;
-  }
+  if (det) VG_TRY(det_setup(c, io.det_part, io.det_bg, io.det_loss, st));
   if (c->scene.n > 0) {
     {
       ProfScope ps(c, VG_K_RENDER_BWD, st);
@@ -715,13 +721,25 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
     vis = (uint8_t*)c->offset.p;
   }
   float scale = (float)(2.0 / ((double)c->cam.width * (double)c->cam.height));
+  const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
+  float *dpart = nullptr, *dbg = nullptr;
+  double* dloss = nullptr;
+  if (det) VG_TRY(det_setup(c, dpart, dbg, dloss, st));
   {
     ProfScope ps(c, VG_K_TOMO_BWD, st);
     launch_tomo_bwd(c->n_tiles, c->cam.projection, target ? 1 : 0, (const GRec*)c->rec.p, c->vals,
                     (const uint2*)c->ranges.p, (const uint32_t*)c->tord.p, p, d_image, image,
-                    target, scale, loss_sum, (float*)c->acc.p, vis, st);
+                    target, scale, loss_sum, (float*)c->acc.p, vis, dpart, dloss, st);
   }
   VG_LAUNCHED(c, 1);
+  if (det) {
+    // tile loss partials exist only with the fused L2 (target); no d_background in tomography
+    VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
+                       (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
+                       (float*)c->acc.p, c->n_tiles, dbg, target ? dloss : nullptr, nullptr,
+                       loss_sum, st));
+    VG_LAUNCHED(c, 2);
+  }
   VG_TRY(finish_view(c, g, st));
   return VG_OK;
 }

@@ -84,7 +84,8 @@ void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
                      const float* d_image,
                      const float* image, const float* target, float loss_scale, double* loss_sum,
-                     float* acc, uint8_t* visible, cudaStream_t st);
+                     float* acc, uint8_t* visible, float* det_part, double* det_loss,
+                     cudaStream_t st);
 // SH scenes: dcol / center receive this view's dL/dRGB slab [3][n] and camera centre
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,

@@ -56,9 +56,11 @@ def tomo_forward(scene, camera, *, tile_size=TILE_SIZE, threads=None, prep=None,
 
 
 def tomo_backward(scene, camera, d_image, *, tile_size=TILE_SIZE, threads=None, prep=None,
-                  parallel=False, extent=1.6):
+                  parallel=False, extent=1.6, deterministic=True):
     """Gradients of sum(d_image * tomo_forward) for every scene parameter
-    (tomo.py:60-103); colour gradients are zero."""
+    (tomo.py:60-103); colour gradients are zero.  deterministic=True (the
+    default, like the reference's fixed tile-order reduction) sums with
+    fixed-order reductions: bitwise reproducible."""
     _finite_or_raise(d_image)
     prep = _tomo_prep(scene, camera, tile_size, prep, parallel, extent)
     H, W = int(camera.height), int(camera.width)
@@ -66,6 +68,9 @@ def tomo_backward(scene, camera, d_image, *, tile_size=TILE_SIZE, threads=None, 
     di = _dev_image(d_image, (H, W), dev)
     bufs = GradBuffers(prep.dscene.n, dev)
     g = bufs.struct(accumulate=False)
+    opt = _lib.make_options(TILE_SIZE, None, TOMO_BIN_CUT, 0.99, TOMO_BIN_CUT,
+                            deterministic=deterministic)
+    _lib.check(_lib.load().vg_set_options(prep.ctx.handle, ctypes.byref(opt)), "vg_set_options")
     _lib.check(_lib.load().vg_tomo_backward(prep.ctx.handle, _lib.ptr(di), ctypes.byref(g),
                                             _stream(dev)), "vg_tomo_backward")
     return bufs.to_scene_grads("analytic", prep.dscene.torch_in)

@@ -640,3 +640,20 @@ def test_single_and_empty_scenes_all_modes(mode, sort_by):
     np.testing.assert_allclose(out.color, np.broadcast_to([0.1, 0.2, 0.3], (24, 40, 3)), atol=1e-7)
     g = vg().backward(empty, cam, dc, mode=mode, sort_by=sort_by)
     np.testing.assert_allclose(g.d_background, dc.reshape(-1, 3).sum(axis=0), rtol=1e-5)
+
+
+@pytest.mark.parametrize("parallel", [False, True])
+def test_tomography_deterministic_adjoint(parallel):
+    """The tomography adjoint in deterministic mode (default of the drop-in):
+    bitwise reproducible and equal to the atomic path within tolerance."""
+    scene, cam, d = load_case("tiny")
+    rng = np.random.default_rng(9)
+    w = rng.uniform(0.1, 1.0, (cam.height, cam.width))
+    a = vg().tomo_backward(scene, cam, w, parallel=parallel)
+    b = vg().tomo_backward(scene, cam, w, parallel=parallel)
+    f = vg().tomo_backward(scene, cam, w, parallel=parallel, deterministic=False)
+    for k in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_kappas"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+        np.testing.assert_allclose(getattr(a, k), getattr(f, k), rtol=1e-4,
+                                   atol=1e-5 * max(1.0, float(np.abs(getattr(f, k)).max())))
+    assert np.array_equal(a.visible, f.visible)
