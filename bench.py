@@ -132,11 +132,6 @@ class ClockSampler:
 # GPU arm
 
 
-def roofline_counts(n_act, n_con):
-    """Active / live pair-pixels of one view."""
-    return float(n_act.sum()), float(n_con.sum())
-
-
 # canonical per-unit costs (BASELINE.md section 4 / SURVEY 8(d))
 COST = {"render_fwd": (21.0, 3.0, 5.0), "render_bwd": (24.0, 4.0, 46.0)}
 

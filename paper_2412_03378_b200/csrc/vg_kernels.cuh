@@ -95,7 +95,6 @@ int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cac
                            const float* dcol, const double* centers, int sh_views,
                            const vg_grads& g, bool splat, cudaStream_t st);
 
-void launch_iota(int64_t n, uint32_t* ids, cudaStream_t st);
 // hand-written onesweep radix sort (vg_radix.cu); result buffer in *which
 size_t radix_temp_bytes(int64_t n, int key_bits);
 // identity_values: v0 is not read, the values start as 0..n-1 (stable index order)
