@@ -160,16 +160,127 @@ class ViewShardedStep:
         for i in sorted(getattr(self, "_used", ())):
             self.engines[i].finalize(self.grads, accumulate=True)
 
-    def __call__(self, dscene=None, targets=None, ready=None):
+    def __call__(self, dscene=None, targets=None, ready=None, grads=None, loss=None):
         """Run the step.  `ready` optionally maps view -> CUDA event that the
-        view's target upload recorded (host->device copies overlap compute)."""
+        view's target upload recorded (host->device copies overlap compute);
+        grads / loss optionally redirect the outputs (double buffering)."""
         if dscene is not None:
             self.ds = dscene
         if targets is not None:
             self.targets = targets
+        if grads is not None:
+            self.grads = grads
+        if loss is not None:
+            self.loss = loss
         self.ready = ready
         self.loss.zero_()
         self._run_views()
         self._finish()
         reduce_across_ranks(self.grads.flat, self.loss, self.group)
         return self.loss
+
+
+class HostFedStep:
+    """A ViewShardedStep fed from pinned host memory: every step uploads the
+    scene and this rank's targets and downloads the flat gradient buffer and
+    the loss.  The device copies are double-buffered on two copy streams, so
+    step k's uploads overlap step k-1's compute and its download overlaps
+    step k+1's -- the host<->device traffic of a training loop whose data
+    lives on the host, hidden behind the kernels.
+
+        fed = HostFedStep(step, host_scene, host_targets)
+        for k in range(K): fed.step()
+        fed.drain()        # grads_host / loss_host hold the last step's results
+    """
+
+    def __init__(self, runner, host_scene, host_targets, lookahead=False):
+        import torch
+        from types import SimpleNamespace
+        from .raster import DeviceScene
+        self.torch = torch
+        self.runner = runner
+        dev = runner.eng.device
+        self.host_scene = host_scene                    # name -> pinned tensor
+        self.host_targets = host_targets                # view -> pinned tensor
+        tmpl = runner.ds
+        self.names = [k for k in ("means", "scales", "rotations", "thetas", "colors", "sh",
+                                  "splat_opacities") if getattr(tmpl, k, None) is not None and k in host_scene]
+        self.ds, self.tg, self.grads, self.loss = [], [], [], []
+        for _ in range(2):
+            fields = {k: getattr(tmpl, k).clone() for k in ("means", "scales", "rotations", "thetas")}
+            for k in ("colors", "sh", "splat_opacities"):
+                v = getattr(tmpl, k, None)
+                fields[k] = v.clone() if v is not None else None
+            self.ds.append(DeviceScene(SimpleNamespace(**fields, background=tmpl.background), dev.index))
+            self.tg.append({v: torch.empty_like(t, device=dev) for v, t in host_targets.items()})
+            self.grads.append(runner.eng.new_grads(self.ds[-1]))
+            self.loss.append(torch.zeros((), dtype=torch.float64, device=dev))
+        self.grads_host = torch.empty(self.grads[0].flat.shape, dtype=torch.float32).pin_memory()
+        self.loss_host = torch.empty((), dtype=torch.float64).pin_memory()
+        self.up = torch.cuda.Stream(device=dev)
+        self.down = torch.cuda.Stream(device=dev)
+        E = torch.cuda.Event
+        self.scene_up = [E(), E()]
+        self.tgt_up = [{v: E() for v in host_targets} for _ in range(2)]
+        self.computed = [E(), E()]
+        self.downloaded = [E(), E()]
+        self.k = 0
+        self.lookahead = lookahead
+        self.used = [False, False]
+        self.staged = [False, False]
+
+    def h2d_bytes(self):
+        return sum(t.numel() * t.element_size() for k, t in self.host_scene.items() if k in self.names) + \
+            sum(t.numel() * t.element_size() for t in self.host_targets.values())
+
+    def d2h_bytes(self):
+        return self.grads_host.numel() * 4 + 8
+
+    def _upload(self, s):
+        torch = self.torch
+        if self.used[s]:
+            self.up.wait_event(self.computed[s])       # slot s last read two steps ago
+        with torch.cuda.stream(self.up):
+            ds = self.ds[s]
+            for name in self.names:
+                dst = getattr(ds, name)
+                dst.copy_(self.host_scene[name].view(dst.shape), non_blocking=True)
+            self.scene_up[s].record(self.up)
+            for v, t in self.host_targets.items():      # each view waits for its own target only
+                self.tg[s][v].copy_(t, non_blocking=True)
+                self.tgt_up[s][v].record(self.up)
+
+    def step(self):
+        """One step: upload (unless prefetched), run, download.  With
+        lookahead, the NEXT step's inputs are read from the host buffers now
+        (data-loader-style prefetch) so their upload overlaps this step."""
+        torch = self.torch
+        s = self.k % 2
+        main = torch.cuda.current_stream(self.runner.eng.device)
+        if not self.staged[s]:
+            self._upload(s)
+        self.staged[s] = False
+        if self.lookahead:
+            nxt = (self.k + 1) % 2
+            self._upload(nxt)
+            self.staged[nxt] = True
+        main.wait_event(self.scene_up[s])
+        if self.used[s]:
+            main.wait_event(self.downloaded[s])        # gradients of step k-2 are out
+        self.runner(self.ds[s], self.tg[s], ready=self.tgt_up[s], grads=self.grads[s],
+                    loss=self.loss[s])
+        self.computed[s].record(main)
+        self.used[s] = True
+        self.down.wait_event(self.computed[s])
+        with torch.cuda.stream(self.down):
+            self.grads_host.copy_(self.grads[s].flat, non_blocking=True)
+            self.loss_host.copy_(self.loss[s], non_blocking=True)
+            self.downloaded[s].record(self.down)
+        self.k += 1
+
+    def drain(self):
+        """Make the current stream wait for the last download (and any
+        prefetched upload)."""
+        cur = self.torch.cuda.current_stream(self.runner.eng.device)
+        cur.wait_stream(self.down)
+        cur.wait_stream(self.up)
