@@ -132,10 +132,6 @@ class ClockSampler:
 # GPU arm
 
 
-# canonical per-unit costs (BASELINE.md section 4 / SURVEY 8(d))
-COST = {"render_fwd": (21.0, 3.0, 5.0), "render_bwd": (24.0, 4.0, 46.0)}
-
-
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -286,8 +282,17 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
 
 def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak):
     """Roofline of the dominant blend kernel from this run's CUDA-event times.
-    Algorithmic units: A = active pair-pixels, L = live pair-pixels of the
-    views of one step; counted in an untimed pass."""
+
+    The blend kernels are neither HBM- nor tensor-core-bound (ncu: DRAM
+    throughput ~3%, no MMA); they are instruction-issue-bound (ncu issue-active
+    75-82%, no single pipe saturated), so the roofline is the SM issue rate,
+    148 SMs x 4 schedulers x 1 warp-instruction / clock at the live clock.
+    Algorithmic units, counted in an untimed pass over this rank's views:
+    V = visible (entry, 64-pixel warp block) pairs -- what the backward walks,
+    one warp iteration each; A = active pair-pixels (composited before early
+    stop), L = live pair-pixels (alpha above the cut).
+    achieved = (ncu warp instructions per visible pair of the profiled view,
+    profiles/traffic.json) x V per step / the kernel's CUDA-event time per step."""
     import torch
     if tomo:
         return None
@@ -295,50 +300,46 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
     ms, cnt = prof[dom]
     if not cnt:
         return None
-    A = L = 0.0
-    for v in my_views:
+    tr = load_traffic(dom) or {}
+    pv = tr.get("view", 0)
+    A = L = V = 0.0
+    V_prof = None
+    for v in my_views if pv in my_views else list(my_views) + [pv]:
         eng.prepare(ds, cams[v])
         _, _, nc = eng.forward()
         na = eng.n_active()
-        A += float(na.double().sum())
-        L += float(nc.double().sum())
+        vp = eng.visible_pairs()
+        if v == pv:
+            V_prof = vp
+        if v in my_views:
+            A += float(na.double().sum())
+            L += float(nc.double().sum())
+            V += vp
     torch.cuda.synchronize()
-    fp_u, mu_u, live_u = COST[dom]
     t = ms * 1e-3 / steps                       # seconds per step in this kernel
-    fp_ops = fp_u * A + live_u * L
-    mu_ops = mu_u * A
-    tr = load_traffic(dom) or {}
-    launch_s = t / max(cnt / steps, 1.0)           # average duration of one launch
-    out = {"kernel": dom, "active_pair_pixels_per_step": A, "live_pair_pixels_per_step": L,
+    launch_s = t / max(cnt / steps, 1.0)        # average duration of one launch
+    out = {"kernel": dom, "visible_pairs_per_step": V, "visible_pair_pixels_per_step": 64.0 * V,
+           "active_pair_pixels_per_step": A, "live_pair_pixels_per_step": L,
            "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
+           "ns_per_visible_pair": t / V * 1e9 if V else None,
            "traffic": tr.get("bytes_per_launch"),
            "traffic_source": "profiles/traffic.json (ncu --set full, dram read + write per launch)"}
     if tr.get("bytes_per_launch"):
-        # not an HBM-bound kernel: the DRAM traffic per launch over its live duration
         hbm = measured_hbm_gbs()
         gbs = tr["bytes_per_launch"] / launch_s / 1e9
         out["hbm_check"] = {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if hbm else None,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
-    if tr.get("warp_instructions_per_launch") and mufu_peak:
-        # executed-work roofline: warp-instruction issue rate vs 148 SMs x 4 schedulers x f
-        f_clk = mufu_peak / (148 * 16)
+    if tr.get("warp_instructions_per_launch") and V_prof and mufu_peak:
+        f_clk = mufu_peak / (148 * 16)          # live SM clock from the MUFU probe (16 ex2/clk/SM)
         issue_peak = 148 * 4 * f_clk
-        ach = tr["warp_instructions_per_launch"] / launch_s
-        out["issue_check"] = {"achieved": ach / 1e9, "peak": issue_peak / 1e9,
-                              "unit": "G warp-instructions/s", "frac": ach / issue_peak,
-                              "note": "ncu-counted instructions of one launch over the live launch time"}
-    if fp32_peak and mufu_peak:
-        f_fp = fp_ops / t / fp32_peak
-        f_mu = mu_ops / t / mufu_peak
-        if f_mu >= f_fp:
-            out.update(bound="sfu", achieved=mu_ops / t / 1e9, peak=mufu_peak / 1e9, unit="Gop/s (MUFU)",
-                       frac=f_mu)
-        else:
-            out.update(bound="fp32", achieved=fp_ops / t / 1e9, peak=fp32_peak / 1e9,
-                       unit="Ginstr/s (FP32 lane-ops)", frac=f_fp)
-        out["frac_fp32"] = f_fp
-        out["frac_mufu"] = f_mu
-        out["peak_source"] = "vg_probe_peaks on this GPU at the live clock (FFMA and MUFU.EX2 loops)"
+        ipp = tr["warp_instructions_per_launch"] / V_prof
+        ach = ipp * V / t
+        out.update(bound="issue", achieved=ach / 1e9, peak=issue_peak / 1e9,
+                   unit="G warp-instructions/s", frac=ach / issue_peak,
+                   warp_instructions_per_visible_pair=ipp,
+                   peak_source="148 SMs x 4 issue/clk at the live clock (vg_probe_peaks MUFU loop / 16)",
+                   ncu_pipes_pct={k: tr.get(k) for k in ("issue_active_pct", "xu_pipe_pct", "fma_pipe_pct",
+                                                          "alu_pipe_pct", "lsu_pipe_pct", "occupancy_pct")})
     return out
 
 

@@ -193,6 +193,13 @@ int vg_render_backward_l2(vg_context* ctx, const float* color, const float* fina
  * (n_contrib != NULL). */
 int vg_n_active(vg_context* ctx, int32_t* out, void* stream);
 
+/* Number of (entry, 64-pixel warp block) pairs the last forward marked
+ * visible -- the pairs the backward blend walks (its algorithmic unit count;
+ * x 64 = visible pair-pixels).  Synchronises; 0 when the forward kept no
+ * visibility mask (alpha_cut == 0 or splat mode).  Diagnostic, no reference
+ * counterpart. */
+int vg_visible_pairs(vg_context* ctx, int64_t* out);
+
 /* tomo.tomo_forward (tomo.py:34-57): line-integral image (H,W).  Pass
  * intensity != NULL to also write exp(-image). */
 int vg_tomo_forward(vg_context* ctx, float* image, float* intensity, void* stream);

@@ -560,6 +560,18 @@ int vg_n_active(vg_context* c, int32_t* out, void* stream) {
   return VG_OK;
 }
 
+int vg_visible_pairs(vg_context* c, int64_t* out) {
+  if (!c || !out) return fail(VG_EINVAL, "vg_visible_pairs: NULL argument");
+  *out = 0;
+  if (!c->have_fwd || !c->vmask_valid) return VG_OK;
+  std::vector<uint32_t> h(4 * (size_t)c->vm_words);
+  VG_CUDA(cudaMemcpy(h.data(), c->vmask.p, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost));
+  int64_t n = 0;
+  for (uint32_t w : h) n += __builtin_popcount(w);
+  *out = n;
+  return VG_OK;
+}
+
 static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
   if (!g) return fail(VG_EINVAL, "grads is NULL");
   if (g->accumulate < VG_OVERWRITE || g->accumulate > VG_DEFER)

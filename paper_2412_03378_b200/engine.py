@@ -96,6 +96,13 @@ class Engine:
         _lib.check(self.lib.vg_n_active(self.ctx.handle, _lib.ptr(out), self.stream()), "vg_n_active")
         return out
 
+    def visible_pairs(self):
+        """(entry, 64-pixel warp block) pairs the last forward marked visible:
+        the pairs the backward walks (synchronises; diagnostic)."""
+        out = ctypes.c_int64()
+        _lib.check(self.lib.vg_visible_pairs(self.ctx.handle, ctypes.byref(out)), "vg_visible_pairs")
+        return int(out.value)
+
     def backward(self, color, tfin, d_color, grads, d_t=None, accumulate=False):
         g = grads.struct(accumulate)
         _lib.check(self.lib.vg_render_backward(self.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),

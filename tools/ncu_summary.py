@@ -67,5 +67,46 @@ def full(path):
         print(f"| `{name}` | " + " | ".join(vals) + " |")
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
+         "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
+FAMILY = {"k_render_fwd": "render_fwd", "k_render_bwd": "render_bwd", "k_preprocess": "preprocess",
+          "k_view_accumulate": "view_accumulate"}
+
+
+def traffic(path, source=""):
+    """Per-launch averages of the blend / preprocess kernels -> profiles/traffic.json."""
+    import json
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+
+    def val(r, key):
+        v = float(r[idx[key]].replace(",", ""))
+        return v * SCALE.get(units[idx[key]], 1.0)
+    acc = defaultdict(list)
+    for r in rows[2:]:
+        name = r[idx["Kernel Name"]].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+        if name in FAMILY:
+            acc[FAMILY[name]].append(r)
+    res = {}
+    for fam, rs in acc.items():
+        def mean(key, rs=rs):
+            return sum(val(r, key) for r in rs) / len(rs)
+        rd, wr = mean("dram__bytes_read.sum"), mean("dram__bytes_write.sum")
+        res[fam] = {"bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                    "warp_instructions_per_launch": mean("smsp__inst_executed.sum"),
+                    "issue_active_pct": mean("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                    "xu_pipe_pct": mean("sm__inst_executed_pipe_xu.sum.pct_of_peak_sustained_active"),
+                    "fma_pipe_pct": mean("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "alu_pipe_pct": mean("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "lsu_pipe_pct": mean("sm__inst_executed_pipe_lsu.sum.pct_of_peak_sustained_active"),
+                    "occupancy_pct": mean("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                    "duration_ms_cold": mean("gpu__time_duration.sum"), "launches": len(rs)}
+    res["_source"] = source
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
