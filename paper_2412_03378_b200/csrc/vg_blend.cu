@@ -29,8 +29,9 @@
 //   suffix_i = total - sum_{j<=i} dot_j contrib_j, and for live entries
 //   dL/de_i = dL/dalpha_i (1 - alpha_i) = dot_i T_after_i - suffix_i.
 // Per-Gaussian accumulators (13 floats, whitened e-frame, see vg_finalize.cu)
-// are summed over the lane's two pixels, warp-reduced with a transpose-reduce
-// (16 shuffles) and added with one 13-lane red.global.add per warp.
+// are summed over the lane's two pixels, warp-reduced through shared memory
+// (smem_reduce13x2: two entries per pass) and added with one 13-lane
+// red.global.add per warp and entry.
 #include "vg_blend.cuh"
 
 // minimum resident CTAs per SM requested from ptxas (register budget); A/B knobs
@@ -38,7 +39,16 @@
 #define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
 #endif
 #ifndef VG_BWD_MINB
-#define VG_BWD_MINB 7   // <= 72 registers
+#define VG_BWD_MINB 6   // <= 80 registers (shared memory also caps it at 6 CTAs)
+#endif
+#ifndef VG_BWD_PAIR
+// two visible entries per step: 1 = both replays, then both entries' gradient
+// terms, two reductions; 2 = the same with one shared-memory pass for both
+// (A/B on config 3, 16 views: backward 21.1 -> 20.0 -> 18.9 ms)
+#define VG_BWD_PAIR 2
+#endif
+#ifndef VG_SMEM_RED
+#define VG_SMEM_RED 1   // backward warp sums through shared memory (smem_reduce13)
 #endif
 
 namespace vg {
@@ -360,7 +370,8 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
 template <bool CUT, bool DET>
 __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in0, bool in1,
                                           F2 dcr, F2 dcg, F2 dcb, F2 tot, const BlendParams& p,
-                                          F2& T, F2& P, int lane, const BwdIO& io, uint32_t pos) {
+                                          F2& T, F2& P, int lane, const BwdIO& io, uint32_t pos,
+                                          float* wb) {
   // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
   // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
@@ -398,10 +409,106 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
   v[13] = v[14] = v[15] = 0.f;
   const uint32_t gid = __float_as_uint(s.c.w);
   if (lane == 0 && any_vis) io.visible[gid] = 1;
+#if VG_SMEM_RED
+  if (DET)
+    flush_det_smem(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE,
+                   wb);
+  else
+    flush_acc_smem(v, lane, gid, io.acc, wb);
+#else
   if (DET)
     flush_det(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE);
   else
     flush_acc(v, lane, gid, io.acc);
+#endif
+}
+
+// Two consecutive visible entries: both replays first (the sequential
+// transmittance chain), then both entries' gradient terms (independent
+// math the scheduler can interleave), then the two flushes.
+struct Replay {
+  F2 h, contrib;
+  bool flush, any_vis;
+};
+
+template <bool CUT>
+__device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool in0, bool in1, F2 dcr,
+                                             F2 dcg, F2 dcb, F2 tot, const BlendParams& p, F2& T,
+                                             F2& P) {
+  const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
+  float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
+  float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
+  const bool cut0 = CUT ? om0 > p.omcut : !act0;
+  const bool cut1 = CUT ? om1 > p.omcut : !act1;
+  om0 = cut0 ? 1.f : om0;
+  om1 = cut1 ? 1.f : om1;
+  const F2 om = f2(om0, om1);
+  Replay r;
+  r.contrib = mul2(sub2(f2s(1.f), om), T);
+  const F2 Tn = mul2(T, om);
+  const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
+  P = fma2(dot, r.contrib, P);
+  T = Tn;
+  const bool live0 = !cut0 && lo(e.ex) > p.cc;
+  const bool live1 = !cut1 && hi(e.ex) > p.cc;
+  r.h = mul2(sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f)), e.G);
+  r.any_vis = __any_sync(FULL, om0 < 1.f || om1 < 1.f);
+  r.flush = r.any_vis || __any_sync(FULL, live0 || live1);
+  return r;
+}
+
+template <bool DET>
+__device__ __forceinline__ void bwd_flush(const SRec& s, const Replay& r, float (&v)[16], int lane,
+                                          const BwdIO& io, uint32_t pos, float* wb) {
+  if (!r.flush) return;
+  const uint32_t gid = __float_as_uint(s.c.w);
+  if (lane == 0 && r.any_vis) io.visible[gid] = 1;
+  if (DET)
+    flush_det_smem(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE,
+                   wb);
+  else
+    flush_acc_smem(v, lane, gid, io.acc, wb);
+}
+
+template <bool CUT, bool DET>
+__device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, const SRec& sb,
+                                           const Pair2& eb, bool in0, bool in1, F2 dcr, F2 dcg, F2 dcb,
+                                           F2 tot, const BlendParams& p, F2& T, F2& P, int lane,
+                                           const BwdIO& io, uint32_t pa, uint32_t pb, float* wb) {
+  const Replay ra = bwd_replay<CUT>(sa, ea, in0, in1, dcr, dcg, dcb, tot, p, T, P);
+  const Replay rb = bwd_replay<CUT>(sb, eb, in0, in1, dcr, dcg, dcb, tot, p, T, P);
+  float va[16], vb[16];
+  pinhole_grad_terms(ea, sa, ra.h, va);
+  pinhole_grad_terms(eb, sb, rb.h, vb);
+  va[10] = hsum(mul2(ra.contrib, dcr));
+  va[11] = hsum(mul2(ra.contrib, dcg));
+  va[12] = hsum(mul2(ra.contrib, dcb));
+  vb[10] = hsum(mul2(rb.contrib, dcr));
+  vb[11] = hsum(mul2(rb.contrib, dcg));
+  vb[12] = hsum(mul2(rb.contrib, dcb));
+#if VG_BWD_PAIR == 2
+  // one shared-memory pass for both entries (all-zero sums are not stored)
+  if (!(ra.flush || rb.flush)) return;
+  const uint32_t ga = __float_as_uint(sa.c.w), gb = __float_as_uint(sb.c.w);
+  if (lane == 0 && ra.any_vis) io.visible[ga] = 1;
+  if (lane == 0 && rb.any_vis) io.visible[gb] = 1;
+  float xa, xb;
+  smem_reduce13x2(va, vb, lane, wb, xa, xb);
+  if (!(lane & 1) && lane < 26) {
+    const int q = lane >> 1;
+    if (DET) {
+      const size_t w = threadIdx.x >> 5;
+      if (xa != 0.f) io.det_part[((size_t)pa * (NT / 32) + w) * ACC_STRIDE + q] = xa;
+      if (xb != 0.f) io.det_part[((size_t)pb * (NT / 32) + w) * ACC_STRIDE + q] = xb;
+    } else {
+      if (xa != 0.f) atomicAdd(io.acc + (size_t)ga * ACC_STRIDE + q, xa);
+      if (xb != 0.f) atomicAdd(io.acc + (size_t)gb * ACC_STRIDE + q, xb);
+    }
+  }
+#else
+  bwd_flush<DET>(sa, ra, va, lane, io, pa, wb);
+  bwd_flush<DET>(sb, rb, vb, lane, io, pb, wb);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -417,9 +524,11 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
                                                    int vm_words) {
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
+  __shared__ __align__(16) float sred[NT / 32][VG_SMEM_RED ? (VG_BWD_PAIR == 2 ? 2 : 1) * RED_WORDS : 4];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* wb = sred[warp];
   const LaneGeo G = lane_geo(p, tx, ty);
   const float lx = (float)G.lxi;
   const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
@@ -471,11 +580,16 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           bits &= bits - 1;
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
-          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k);
+#if VG_BWD_PAIR
+          bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
+                               base + k, base + kb, wb);
+#else
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k, wb);
           bwd_entry<CUT, DET>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                              base + kb);
+                              base + kb, wb);
+#endif
         } else {
-          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k);
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k, wb);
         }
       }
       done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);

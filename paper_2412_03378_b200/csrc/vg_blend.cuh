@@ -57,6 +57,7 @@ __device__ __forceinline__ F2 neg2(F2 x) { return f2(-lo(x), -hi(x)); }
 __device__ __forceinline__ F2 sel2(bool p0, bool p1, F2 a, F2 b) {
   return f2(p0 ? lo(a) : lo(b), p1 ? hi(a) : hi(b));
 }
+__device__ __forceinline__ float hsum(F2 x) { return lo(x) + hi(x); }
 
 // ---------------------------------------------------------------------------
 // staging + culling
@@ -124,6 +125,70 @@ __device__ __forceinline__ void flush_acc(float (&v)[16], int lane, uint32_t gid
   if (!(lane & 1) && idx < 13 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + idx, s);
 }
 
+// Warp sum of 13 per-lane values through shared memory (wb: RED_WORDS floats
+// per warp, 16-byte aligned): each lane stores its 13 values as column `lane`
+// of a 13 x 36 array (conflict-free), lanes 2q and 2q+1 each sum one half
+// row of value q with four 128-bit loads (the 4-float row padding spreads
+// the eight rows a quarter-warp reads over all 32 banks) and packed adds,
+// and one shuffle joins the halves: lane 2q (q < 13) returns the sum of
+// value q.  About 30 instructions against the 62 of transpose_reduce16.
+constexpr int RED_ROW = 36;
+constexpr int RED_WORDS = 13 * RED_ROW;
+__device__ __forceinline__ float smem_reduce13(const float (&v)[16], int lane, float* wb) {
+#pragma unroll
+  for (int q = 0; q < 13; ++q) wb[q * RED_ROW + lane] = v[q];
+  __syncwarp();
+  float s = 0.f;
+  if (lane < 26) {
+    const float4* src = reinterpret_cast<const float4*>(wb + (lane >> 1) * RED_ROW + (lane & 1) * 16);
+    const float4 x0 = src[0], x1 = src[1], x2 = src[2], x3 = src[3];
+    const F2 a = add2(add2(f2(x0.x, x0.y), f2(x1.x, x1.y)), add2(f2(x2.x, x2.y), f2(x3.x, x3.y)));
+    const F2 b = add2(add2(f2(x0.z, x0.w), f2(x1.z, x1.w)), add2(f2(x2.z, x2.w), f2(x3.z, x3.w)));
+    s = hsum(add2(a, b));
+  }
+  s += __shfl_xor_sync(FULL, s, 1);
+  __syncwarp();  // the buffer is rewritten by the warp's next entry
+  return s;
+}
+
+// The same for two entries at once (wb: 2 * RED_WORDS floats): lane 2q
+// returns the sums of value q of entry a (sa) and entry b (sb).
+__device__ __forceinline__ void smem_reduce13x2(const float (&va)[16], const float (&vb)[16], int lane,
+                                                float* wb, float& sa, float& sb) {
+#pragma unroll
+  for (int q = 0; q < 13; ++q) {
+    wb[q * RED_ROW + lane] = va[q];
+    wb[(13 + q) * RED_ROW + lane] = vb[q];
+  }
+  __syncwarp();
+  sa = sb = 0.f;
+  if (lane < 26) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const float4* src =
+          reinterpret_cast<const float4*>(wb + (13 * t + (lane >> 1)) * RED_ROW + (lane & 1) * 16);
+      const float4 x0 = src[0], x1 = src[1], x2 = src[2], x3 = src[3];
+      const F2 a = add2(add2(f2(x0.x, x0.y), f2(x1.x, x1.y)), add2(f2(x2.x, x2.y), f2(x3.x, x3.y)));
+      const F2 b = add2(add2(f2(x0.z, x0.w), f2(x1.z, x1.w)), add2(f2(x2.z, x2.w), f2(x3.z, x3.w)));
+      (t ? sb : sa) = hsum(add2(a, b));
+    }
+  }
+  sa += __shfl_xor_sync(FULL, sa, 1);
+  sb += __shfl_xor_sync(FULL, sb, 1);
+  __syncwarp();
+}
+
+__device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, uint32_t gid, float* acc,
+                                               float* wb) {
+  const float s = smem_reduce13(v, lane, wb);
+  if (!(lane & 1) && lane < 26 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + (lane >> 1), s);
+}
+
+__device__ __forceinline__ void flush_det_smem(const float (&v)[16], int lane, float* slot, float* wb) {
+  const float s = smem_reduce13(v, lane, wb);
+  if (!(lane & 1) && lane < 26 && s != 0.f) slot[lane >> 1] = s;
+}
+
 // Deterministic mode: the warp's 13 sums go to the (entry, warp) slot (no
 // atomics); vg_det.cu reduces the slots per Gaussian in a fixed order.
 __device__ __forceinline__ void flush_det(float (&v)[16], int lane, float* slot) {
@@ -163,8 +228,6 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
     }
   }
 }
-
-__device__ __forceinline__ float hsum(F2 x) { return lo(x) + hi(x); }
 
 // Per-pixel prologue of the backward: upstream gradient (explicit or fused
 // L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
