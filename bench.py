@@ -224,7 +224,7 @@ def run_gpu(args):
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                    for k, v in prof.items() if v[1]}
         roof = build_roofline(prof, args.steps, eng, ds, cams, my_views, tomo, cfg,
-                              fp32_peak, mufu_peak)
+                              fp32_peak, mufu_peak, args.config)
         result = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mpixels/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
@@ -280,63 +280,71 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
             "api": "multiview.HostFedStep(lookahead=True): every step uploads its scene + targets and downloads grads + loss, double-buffered and overlapped with compute; the timed region holds K uploads and K downloads"}
 
 
-def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak):
+def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak, cfg_name):
     """Roofline of the dominant blend kernel from this run's CUDA-event times.
 
     The blend kernels are neither HBM- nor tensor-core-bound (ncu: DRAM
-    throughput ~3%, no MMA); they are instruction-issue-bound (ncu issue-active
-    75-82%, no single pipe saturated), so the roofline is the SM issue rate,
-    148 SMs x 4 schedulers x 1 warp-instruction / clock at the live clock.
+    throughput ~3%, no MMA); they are instruction-issue-bound (no single pipe
+    saturated), so the roofline is the SM issue rate, 148 SMs x 4 schedulers
+    x 1 warp-instruction / clock at the live clock.
     Algorithmic units, counted in an untimed pass over this rank's views:
-    V = visible (entry, 64-pixel warp block) pairs -- what the backward walks,
-    one warp iteration each; A = active pair-pixels (composited before early
-    stop), L = live pair-pixels (alpha above the cut).
-    achieved = (ncu warp instructions per visible pair of the profiled view,
-    profiles/traffic.json) x V per step / the kernel's CUDA-event time per step."""
+    render -- V = visible (entry, 64-pixel warp block) pairs, what the
+    backward walks (one warp iteration each), plus A = active pair-pixels
+    and L = live pair-pixels; tomography -- the binned
+    (tile, Gaussian) pairs, one thread walking the tile's 256 pixels each.
+    achieved = (ncu warp instructions per unit of the profiled view of this
+    config, profiles/traffic.json) x units per step / the kernel's CUDA-event
+    time per step."""
     import torch
-    if tomo:
-        return None
-    dom = max(("render_fwd", "render_bwd"), key=lambda k: prof.get(k, (0, 0))[0])
-    ms, cnt = prof[dom]
+    kinds = ("tomo_fwd", "tomo_bwd") if tomo else ("render_fwd", "render_bwd")
+    dom = max(kinds, key=lambda k: prof.get(k, (0, 0))[0])
+    ms, cnt = prof.get(dom, (0.0, 0))
     if not cnt:
         return None
-    tr = load_traffic(dom) or {}
+    tr = load_traffic(cfg_name, dom) or {}
     pv = tr.get("view", 0)
-    A = L = V = 0.0
-    V_prof = None
+    A = L = U = 0.0
+    U_prof = None
     for v in my_views if pv in my_views else list(my_views) + [pv]:
-        eng.prepare(ds, cams[v])
-        _, _, nc = eng.forward()
-        na = eng.n_active()
-        vp = eng.visible_pairs()
+        if tomo:
+            eng.prepare(ds, cams[v], tomo=True, parallel=cfg.parallel, extent=cfg.extent)
+            u = eng.pair_count()
+        else:
+            eng.prepare(ds, cams[v])
+            _, _, nc = eng.forward()
+            u = eng.visible_pairs()
         if v == pv:
-            V_prof = vp
+            U_prof = u
         if v in my_views:
-            A += float(na.double().sum())
-            L += float(nc.double().sum())
-            V += vp
+            U += u
+            if not tomo:
+                A += float(eng.n_active().double().sum())
+                L += float(nc.double().sum())
     torch.cuda.synchronize()
     t = ms * 1e-3 / steps                       # seconds per step in this kernel
     launch_s = t / max(cnt / steps, 1.0)        # average duration of one launch
-    out = {"kernel": dom, "visible_pairs_per_step": V, "visible_pair_pixels_per_step": 64.0 * V,
-           "active_pair_pixels_per_step": A, "live_pair_pixels_per_step": L,
+    unit = "binned pairs" if tomo else "visible pairs"
+    out = {"kernel": dom, "unit_of_work": unit, "units_per_step": U,
            "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
-           "ns_per_visible_pair": t / V * 1e9 if V else None,
+           "ns_per_unit": t / U * 1e9 if U else None,
            "traffic": tr.get("bytes_per_launch"),
-           "traffic_source": "profiles/traffic.json (ncu --set full, dram read + write per launch)"}
+           "traffic_source": f"profiles/traffic.json[{cfg_name}] (ncu --set full, dram read + write per launch)"}
+    if not tomo:
+        out.update(visible_pair_pixels_per_step=64.0 * U, active_pair_pixels_per_step=A,
+                   live_pair_pixels_per_step=L)
     if tr.get("bytes_per_launch"):
         hbm = measured_hbm_gbs()
         gbs = tr["bytes_per_launch"] / launch_s / 1e9
         out["hbm_check"] = {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm if hbm else None,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
-    if tr.get("warp_instructions_per_launch") and V_prof and mufu_peak:
+    if tr.get("warp_instructions_per_launch") and U_prof and mufu_peak:
         f_clk = mufu_peak / (148 * 16)          # live SM clock from the MUFU probe (16 ex2/clk/SM)
         issue_peak = 148 * 4 * f_clk
-        ipp = tr["warp_instructions_per_launch"] / V_prof
-        ach = ipp * V / t
+        ipu = tr["warp_instructions_per_launch"] / U_prof
+        ach = ipu * U / t
         out.update(bound="issue", achieved=ach / 1e9, peak=issue_peak / 1e9,
                    unit="G warp-instructions/s", frac=ach / issue_peak,
-                   warp_instructions_per_visible_pair=ipp,
+                   warp_instructions_per_unit=ipu,
                    peak_source="148 SMs x 4 issue/clk at the live clock (vg_probe_peaks MUFU loop / 16)",
                    ncu_pipes_pct={k: tr.get(k) for k in ("issue_active_pct", "xu_pipe_pct", "fma_pipe_pct",
                                                           "alu_pipe_pct", "lsu_pipe_pct", "occupancy_pct")})
@@ -351,12 +359,12 @@ def measured_hbm_gbs():
         return 6650.0  # the profiling recipe's fallback
 
 
-def load_traffic(kernel):
+def load_traffic(config, kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
-    except (OSError, ValueError):
+            return json.load(f).get(config, {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
         return None
 
 

@@ -60,6 +60,18 @@ struct __align__(16) SRec {
   float4 d;  // r, g, b, 0
 };
 
+// Tile-relative record of Gaussian gid for the tile at pixel origin (x0, y0).
+__device__ __forceinline__ SRec make_srec(const GRec& g, uint32_t gid, int x0, int y0) {
+  const float bu = (float)((double)x0 + 0.5 - g.u);
+  const float bv = (float)((double)y0 + 0.5 - g.v);
+  SRec s;
+  s.a = make_float4(g.P11 * bu, fmaf(g.P22, bv, g.P21 * bu), fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm)), g.cD2);
+  s.b = make_float4(g.P11, g.P21, g.P22, g.kap2);
+  s.c = make_float4(g.n1, g.n2, g.D, __uint_as_float(gid));
+  s.d = make_float4(g.cr, g.cg, g.cb, 0.f);
+  return s;
+}
+
 // Stage one record for the tile at pixel origin (x0, y0); return the 4-bit
 // mask of 8x8 warp blocks the Gaussian may reach with alpha >= cut.
 // Bound per block: e = K beta exp(-expo/2) with K = kappa sqrt(2pi),
@@ -71,16 +83,8 @@ __device__ __forceinline__ uint32_t stage(SRec* sm, int slot, const GRec* __rest
                                           uint32_t gid, int x0, int y0, bool cull, float ecut,
                                           const float* __restrict__ dmax4 = nullptr) {
   const GRec g = rec[gid];
-  float bu = (float)((double)x0 + 0.5 - g.u);
-  float bv = (float)((double)y0 + 0.5 - g.v);
-  float c1 = g.P11 * bu;
-  float c2 = fmaf(g.P22, bv, g.P21 * bu);
-  float c3 = fmaf(g.n2, bv, fmaf(g.n1, bu, g.wm));
-  SRec s;
-  s.a = make_float4(c1, c2, c3, g.cD2);
-  s.b = make_float4(g.P11, g.P21, g.P22, g.kap2);
-  s.c = make_float4(g.n1, g.n2, g.D, __uint_as_float(gid));
-  s.d = make_float4(g.cr, g.cg, g.cb, 0.f);
+  const SRec s = make_srec(g, gid, x0, y0);
+  const float c1 = s.a.x, c2 = s.a.y, c3 = s.a.z;
   sm[slot] = s;
   if (!cull) return 0xFu;
   if (!(g.amp > ecut)) return 0u;  // alpha < cut at every pixel
@@ -607,9 +611,11 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
                                                  const uint2* __restrict__ ranges,
                                                  const uint32_t* __restrict__ order,
                                                  BlendParams p, float* __restrict__ image,
-                                                 float* __restrict__ intensity) {
+                                                 float* __restrict__ intensity,
+                                                 float* __restrict__ part) {
   __shared__ SRec sm[BATCH];
   const int tile = order[blockIdx.x];
+  const int split = blockIdx.y, S = gridDim.y;
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const LaneGeo G = lane_geo(p, tx, ty);
   const float lx = (float)G.lxi;
@@ -618,7 +624,8 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
                                   : f2s(0.f);
   const uint2 r = ranges[tile];
   F2 sum = f2s(0.f);
-  for (uint32_t base = r.x; base < r.y; base += BATCH) {
+  // split s walks batches s, s + S, ... of the tile's list
+  for (uint32_t base = r.x + split * BATCH; base < r.y; base += BATCH * S) {
     __syncthreads();
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
@@ -637,10 +644,26 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
     const bool in = q ? G.in1 : G.in0;
     if (!in) continue;
     const int pix = (q ? G.row1 : G.row0) * p.width + G.col;
+    if (S > 1) {
+      part[(size_t)split * p.width * p.height + pix] = q ? hi(sum) : lo(sum);
+      continue;
+    }
     const float I = (q ? hi(sum) : lo(sum)) * (float)LN2;
     image[pix] = I;
     if (intensity) intensity[pix] = __expf(-I);
   }
+}
+
+// Sum of the per-split partial images in split order (deterministic).
+__global__ void k_tomo_combine(int npix, int S, const float* __restrict__ part, float* __restrict__ image,
+                               float* __restrict__ intensity) {
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= npix) return;
+  float sum = 0.f;
+  for (int s = 0; s < S; ++s) sum += part[(size_t)s * npix + pix];
+  const float I = sum * (float)LN2;
+  image[pix] = I;
+  if (intensity) intensity[pix] = __expf(-I);
 }
 
 // Tomography adjoint, Gaussian-parallel.  The line-integral sum has no
@@ -662,10 +685,10 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
                                                  uint8_t* __restrict__ visible,
                                                  float* __restrict__ det_part,
                                                  double* __restrict__ det_loss) {
-  __shared__ SRec sm[BATCH];
   __shared__ float sde[TILE_PIX];
   __shared__ float slp[TILE_PIX];
   const int tile = order[blockIdx.x];
+  const int split = blockIdx.y, S = gridDim.y;
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const uint2 r = ranges[tile];
   double lossv = 0.0;
@@ -686,17 +709,13 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
     slp[q] = RAY == VG_PINHOLE ? pixel_lp(p, col, row) : 0.f;
   }
   // deterministic mode: this tile's loss partial, summed in tile order later
-  if (LOSS) block_flush(0.f, 0.f, 0.f, lossv, nullptr, DET ? det_loss + tile : loss_sum, DET);
-  for (uint32_t base = r.x; base < r.y; base += BATCH) {
-    __syncthreads();
-    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
-      uint32_t i = base + sidx;
-      if (i < r.y) stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, false, 0.f);
-    }
-    __syncthreads();
-    const int nb = min((uint32_t)BATCH, r.y - base);
-    for (int k = threadIdx.x; k < nb; k += NT) {
-      const SRec s = sm[k];
+  if (LOSS && split == 0) block_flush(0.f, 0.f, 0.f, lossv, nullptr, DET ? det_loss + tile : loss_sum, DET);
+  __syncthreads();
+  // split s owns pairs r.x + s NT + thread, stepping NT S: one thread per pair
+  {
+    for (uint32_t i = r.x + split * NT + threadIdx.x; i < r.y; i += NT * S) {
+      const uint32_t gi = vals[i];
+      const SRec s = make_srec(rec[gi], gi, tx * TILE, ty * TILE);
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
       float b0 = 0.f, b1 = 0.f, b2 = 0.f, hs = 0.f, gmax = 0.f;
       for (int ly = 0; ly < TILE; ++ly) {
@@ -755,7 +774,7 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
 #pragma unroll
       if (DET) {
         // the pair's own slot (warp slot 0 of its list position; vg_det.cu)
-        float* sl = det_part + (size_t)(base + k) * (NT / 32) * ACC_STRIDE;
+        float* sl = det_part + (size_t)i * (NT / 32) * ACC_STRIDE;
 #pragma unroll
         for (int q = 0; q < 10; ++q) sl[q] = vv[q];
       } else {
@@ -816,20 +835,26 @@ void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
 
 void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
-                     float* image, float* intensity, cudaStream_t st) {
+                     float* image, float* intensity, int splits, float* part, cudaStream_t st) {
+  const dim3 grid(n_tiles, splits);
   if (ray == VG_PINHOLE)
-    k_tomo_fwd<VG_PINHOLE><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity);
+    k_tomo_fwd<VG_PINHOLE><<<grid, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity, part);
   else
-    k_tomo_fwd<VG_PARALLEL><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity);
+    k_tomo_fwd<VG_PARALLEL><<<grid, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity, part);
+  if (splits > 1) {
+    const int npix = p.width * p.height;
+    k_tomo_combine<<<(npix + 255) / 256, 256, 0, st>>>(npix, splits, part, image, intensity);
+  }
 }
 
-void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint32_t* vals,
+void launch_tomo_bwd(int n_tiles, int splits, int ray, int loss, const GRec* rec, const uint32_t* vals,
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
                      const float* d_image, const float* image, const float* target,
                      float loss_scale, double* loss_sum, float* acc, uint8_t* visible,
                      float* det_part, double* det_loss, cudaStream_t st) {
 #define VG_TB(R, L, D)                                                                            \
-  k_tomo_bwd<R, L, D><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, d_image, image, target, \
+  k_tomo_bwd<R, L, D><<<dim3(n_tiles, splits), NT, 0, st>>>(rec, vals, ranges, order, p, d_image, \
+                                                            image, target,                        \
                                               loss_scale, loss_sum, acc, visible, det_part, det_loss)
 #define VG_TB2(D)                                                       \
   do {                                                                  \

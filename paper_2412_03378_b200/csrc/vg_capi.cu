@@ -62,6 +62,7 @@ struct vg_context {
   bool det_ready = false;            // det_slot maps the lists of the last prepare
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
+  Buf tpart;                         // tomography forward: per-split partial images
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
@@ -214,7 +215,7 @@ void vg_destroy(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -745,6 +746,25 @@ int vg_render_backward_l2(vg_context* c, const float* color, const float* final_
   return render_bwd_common(c, color, final_t, nullptr, nullptr, target, loss_sum, g, stream);
 }
 
+// Tomography CTAs per tile: enough to fill the GPU when a small detector has
+// long per-tile lists (config 5: 1024 tiles x ~5k pairs).  The forward splits
+// in batches of 256 entries (and sums partial images), the adjoint per pair.
+static int tomo_splits(const vg_context* c, bool fwd) {
+  static int env_f = -2, env_b = -2;
+  int& e = fwd ? env_f : env_b;
+  if (e == -2) {
+    const char* v = getenv(fwd ? "VG_TOMO_SPLIT_F" : "VG_TOMO_SPLIT_B");
+    e = v ? atoi(v) : -1;
+  }
+  if (e > 0) return e;
+  if (c->n_tiles <= 0 || c->pairs <= 0) return 1;
+  const int64_t avg = c->pairs / c->n_tiles;
+  // forward: about one 256-entry batch per split; adjoint: about one pair
+  // per thread (config 5 sweep: 383.7 ms/step unsplit -> 259-262 at 16-32 x 64)
+  const int64_t s = fwd ? (avg + 255) / 256 : (avg + 127) / 128;
+  return (int)(s < 1 ? 1 : s > 64 ? 64 : s);
+}
+
 int vg_tomo_forward(vg_context* c, float* image, float* intensity, void* stream) {
   if (!c || !image) return fail(VG_EINVAL, "vg_tomo_forward: NULL argument");
   if (!c->prepared) return fail(VG_EINVAL, "vg_tomo_forward: call vg_prepare first");
@@ -753,8 +773,13 @@ int vg_tomo_forward(vg_context* c, float* image, float* intensity, void* stream)
   BlendParams p = blend_params(c);
   {
     ProfScope ps(c, VG_K_TOMO_FWD, st);
+    const int S = tomo_splits(c, true);
+    if (S > 1)
+      VG_TRY(ensure(c->tpart, sizeof(float) * (size_t)S * c->cam.width * c->cam.height, st));
     launch_tomo_fwd(c->n_tiles, c->cam.projection, (const GRec*)c->rec.p, c->vals,
-                    (const uint2*)c->ranges.p, (const uint32_t*)c->tord.p, p, image, intensity, st);
+                    (const uint2*)c->ranges.p, (const uint32_t*)c->tord.p, p, image, intensity, S,
+                    (float*)c->tpart.p, st);
+    if (S > 1) VG_LAUNCHED(c, 1);
   }
   VG_LAUNCHED(c, 1);
   return VG_OK;
@@ -779,7 +804,8 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
   if (det) VG_TRY(det_setup(c, dpart, dbg, dloss, st));
   {
     ProfScope ps(c, VG_K_TOMO_BWD, st);
-    launch_tomo_bwd(c->n_tiles, c->cam.projection, target ? 1 : 0, (const GRec*)c->rec.p, c->vals,
+    launch_tomo_bwd(c->n_tiles, tomo_splits(c, false), c->cam.projection, target ? 1 : 0,
+                    (const GRec*)c->rec.p, c->vals,
                     (const uint2*)c->ranges.p, (const uint32_t*)c->tord.p, p, d_image, image,
                     target, scale, loss_sum, (float*)c->acc.p, vis, dpart, dloss, st);
   }

@@ -77,10 +77,15 @@ int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, cons
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st);
+// Tomography splits each tile's pair list over `splits` CTAs (small detectors
+// with long lists would otherwise leave most SMs idle): the forward writes
+// per-split partial images into `part` (splits * H * W floats, unused when
+// splits == 1) and sums them in split order; the adjoint's pairs are
+// independent.
 void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals,
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
-                     float* image, float* intensity, cudaStream_t st);
-void launch_tomo_bwd(int n_tiles, int ray, int loss, const GRec* rec, const uint32_t* vals,
+                     float* image, float* intensity, int splits, float* part, cudaStream_t st);
+void launch_tomo_bwd(int n_tiles, int splits, int ray, int loss, const GRec* rec, const uint32_t* vals,
                      const uint2* ranges, const uint32_t* order, const BlendParams& p,
                      const float* d_image,
                      const float* image, const float* target, float loss_scale, double* loss_sum,

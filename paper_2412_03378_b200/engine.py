@@ -96,6 +96,12 @@ class Engine:
         _lib.check(self.lib.vg_n_active(self.ctx.handle, _lib.ptr(out), self.stream()), "vg_n_active")
         return out
 
+    def pair_count(self):
+        """(tile, Gaussian) pairs of the last prepare (synchronises)."""
+        out = ctypes.c_int64()
+        _lib.check(self.lib.vg_pair_count(self.ctx.handle, ctypes.byref(out)), "vg_pair_count")
+        return int(out.value)
+
     def visible_pairs(self):
         """(entry, 64-pixel warp block) pairs the last forward marked visible:
         the pairs the backward walks (synchronises; diagnostic)."""

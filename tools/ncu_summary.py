@@ -70,11 +70,12 @@ def full(path):
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
          "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
 FAMILY = {"k_render_fwd": "render_fwd", "k_render_bwd": "render_bwd", "k_preprocess": "preprocess",
-          "k_view_accumulate": "view_accumulate"}
+          "k_view_accumulate": "view_accumulate", "k_tomo_fwd": "tomo_fwd", "k_tomo_bwd": "tomo_bwd"}
 
 
-def traffic(path, source=""):
-    """Per-launch averages of the blend / preprocess kernels -> profiles/traffic.json."""
+def traffic(path, source="", config=None, out_path=None, view="0"):
+    """Per-launch averages of the blend / preprocess kernels; with config and
+    out_path, merged into that JSON under the config's key."""
     import json
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -104,7 +105,18 @@ def traffic(path, source=""):
                     "lsu_pipe_pct": mean("sm__inst_executed_pipe_lsu.sum.pct_of_peak_sustained_active"),
                     "occupancy_pct": mean("sm__warps_active.avg.pct_of_peak_sustained_active"),
                     "duration_ms_cold": mean("gpu__time_duration.sum"), "launches": len(rs)}
+    for v in res.values():
+        v["view"] = int(view)
     res["_source"] = source
+    if config and out_path:
+        try:
+            with open(out_path) as f:
+                allr = json.load(f)
+        except (OSError, ValueError):
+            allr = {}
+        allr[config] = res
+        with open(out_path, "w") as f:
+            json.dump(allr, f, indent=1)
     print(json.dumps(res, indent=1))
 
 
