@@ -716,61 +716,71 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
     for (uint32_t i = r.x + split * NT + threadIdx.x; i < r.y; i += NT * S) {
       const uint32_t gi = vals[i];
       const SRec s = make_srec(rec[gi], gi, tx * TILE, ty * TILE);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-      float b0 = 0.f, b1 = 0.f, b2 = 0.f, hs = 0.f, gmax = 0.f;
+      // two horizontally adjacent pixels per step in packed FP32x2; b0 / b1
+      // accumulate with the opposite sign and are negated at the end
+      const F2 zero = f2s(0.f);
+      F2 a0 = zero, a1 = zero, a2 = zero, a3 = zero, a4 = zero, a5 = zero;
+      F2 b0 = zero, b1 = zero, b2 = zero, hs = zero, gs = zero;
+      const F2 bx = f2s(s.b.x), by = f2s(s.b.y), ax = f2s(s.a.x), cx = f2s(s.c.x);
+      const F2 cz = f2s(s.c.z), naw = f2s(-s.a.w), nch = f2s(-C_HALF_LOG2E);
       for (int ly = 0; ly < TILE; ++ly) {
         const float fy = (float)ly;
-        const float t2 = fmaf(s.b.z, fy, s.a.y);
-        const float tw = fmaf(s.c.y, fy, s.a.z);
+        const F2 t2 = f2s(fmaf(s.b.z, fy, s.a.y));
+        const F2 tw = f2s(fmaf(s.c.y, fy, s.a.z));
+        F2 fx = f2(0.f, 1.f);
 #pragma unroll 4
-        for (int lx = 0; lx < TILE; ++lx) {
-          const float fx = (float)lx;
-          const float d = sde[ly * TILE + lx];
-          const float q1 = fmaf(s.b.x, fx, s.a.x);
-          const float q2 = fmaf(s.b.y, fx, t2);
-          const float X = fmaf(q1, q1, q2 * q2);
+        for (int lx = 0; lx < TILE; lx += 2) {
+          F2 d;
+          d.v = *reinterpret_cast<const unsigned long long*>(&sde[ly * TILE + lx]);
+          const F2 q1 = fma2(bx, fx, ax);
+          const F2 q2 = fma2(by, fx, t2);
+          const F2 X = fma2(q1, q1, mul2(q2, q2));
           if (RAY == VG_PINHOLE) {
-            const float wp = fmaf(s.c.x, fx, tw);
-            const float rs = rsqf(fmaf(wp, wp, X));
-            const float ri = rs * rs;
-            const float G = rs * ex2f(fmaf(-s.a.w, X * ri, slp[ly * TILE + lx]));
-            gmax = fmaxf(gmax, G);
-            const float h = d * G;
+            F2 lp;
+            lp.v = *reinterpret_cast<const unsigned long long*>(&slp[ly * TILE + lx]);
+            const F2 wp = fma2(cx, fx, tw);
+            const F2 rs = rsq_2(fma2(wp, wp, X));
+            const F2 ri = mul2(rs, rs);
+            const F2 G = mul2(rs, ex2_2(fma2(naw, mul2(X, ri), lp)));
+            gs = add2(gs, G);
+            const F2 h = mul2(d, G);
             // factored h (rho rho^T + w^ w^T), h rho (see pinhole_grad_terms)
-            const float sD = s.c.z * ri, s2 = sD * sD, wp2 = wp * wp;
-            const float k1 = h * fmaf(s2, wp2, ri);
-            const float k2 = h * wp * fmaf(-s2, X, ri);
-            const float k1q1 = k1 * q1;
-            a0 = fmaf(k1q1, q1, a0);
-            a1 = fmaf(k1q1, q2, a1);
-            a2 = fmaf(k2, q1, a2);
-            a3 = fmaf(k1 * q2, q2, a3);
-            a4 = fmaf(k2, q2, a4);
-            a5 = fmaf(h, fmaf(s2, X * X, ri * wp2), a5);
-            const float hsD = h * sD, hsw = hsD * wp;
-            b0 = fmaf(-hsw, q1, b0);
-            b1 = fmaf(-hsw, q2, b1);
-            b2 = fmaf(hsD, X, b2);
-            hs += h;
+            const F2 sD = mul2(cz, ri), s2 = mul2(sD, sD), wp2 = mul2(wp, wp);
+            const F2 k1 = mul2(h, fma2(s2, wp2, ri));
+            const F2 k2 = mul2(mul2(h, wp), sub2(ri, mul2(s2, X)));
+            const F2 k1q1 = mul2(k1, q1);
+            a0 = fma2(k1q1, q1, a0);
+            a1 = fma2(k1q1, q2, a1);
+            a2 = fma2(k2, q1, a2);
+            a3 = fma2(mul2(k1, q2), q2, a3);
+            a4 = fma2(k2, q2, a4);
+            a5 = fma2(h, fma2(s2, mul2(X, X), mul2(ri, wp2)), a5);
+            const F2 hsD = mul2(h, sD), hsw = mul2(hsD, wp);
+            b0 = fma2(hsw, q1, b0);
+            b1 = fma2(hsw, q2, b1);
+            b2 = fma2(hsD, X, b2);
+            hs = add2(hs, h);
           } else {
-            const float G = s.c.z * ex2f(-C_HALF_LOG2E * X);
-            gmax = fmaxf(gmax, G);
-            const float h = d * G;
+            const F2 G = mul2(cz, ex2_2(mul2(nch, X)));
+            gs = add2(gs, G);
+            const F2 h = mul2(d, G);
             // rho = -(q1, q2, 0), w^ = (0, 0, 1)
-            const float hq1 = h * q1, hq2 = h * q2;
-            a0 = fmaf(hq1, q1, a0);
-            a1 = fmaf(hq1, q2, a1);
-            a3 = fmaf(hq2, q2, a3);
-            b0 -= hq1;
-            b1 -= hq2;
-            hs += h;
+            const F2 hq1 = mul2(h, q1), hq2 = mul2(h, q2);
+            a0 = fma2(hq1, q1, a0);
+            a1 = fma2(hq1, q2, a1);
+            a3 = fma2(hq2, q2, a3);
+            b0 = add2(b0, hq1);
+            b1 = add2(b1, hq2);
+            hs = add2(hs, h);
           }
+          fx = add2(fx, f2s(2.f));
         }
       }
-      if (RAY != VG_PINHOLE) a5 = hs;
+      const float hsum_h = hsum(hs);
       const uint32_t gid = __float_as_uint(s.c.w);
       float* o = acc + (size_t)gid * ACC_STRIDE;
-      const float vv[10] = {a0, a1, a2, a3, a4, a5, b0, b1, b2, hs};
+      const float vv[10] = {hsum(a0), hsum(a1), hsum(a2), hsum(a3), hsum(a4),
+                            RAY != VG_PINHOLE ? hsum_h : hsum(a5), -hsum(b0), -hsum(b1), hsum(b2), hsum_h};
 #pragma unroll
       if (DET) {
         // the pair's own slot (warp slot 0 of its list position; vg_det.cu)
@@ -782,7 +792,7 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
         for (int q = 0; q < 10; ++q)
           if (vv[q] != 0.f) atomicAdd(o + q, vv[q]);
       }
-      if (gmax > 0.f && s.b.w > 0.f) visible[gid] = 1;
+      if (hsum(gs) > 0.f && s.b.w > 0.f) visible[gid] = 1;
     }
   }
 }
