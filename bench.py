@@ -342,12 +342,26 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
         issue_peak = 148 * 4 * f_clk
         ipu = tr["warp_instructions_per_launch"] / U_prof
         ach = ipu * U / t
+        f_issue = ach / issue_peak
         out.update(bound="issue", achieved=ach / 1e9, peak=issue_peak / 1e9,
-                   unit="G warp-instructions/s", frac=ach / issue_peak,
+                   unit="G warp-instructions/s", frac=f_issue,
                    warp_instructions_per_unit=ipu,
                    peak_source="148 SMs x 4 issue/clk at the live clock (vg_probe_peaks MUFU loop / 16)",
                    ncu_pipes_pct={k: tr.get(k) for k in ("issue_active_pct", "xu_pipe_pct", "fma_pipe_pct",
                                                           "alu_pipe_pct", "lsu_pipe_pct", "occupancy_pct")})
+        # the busiest pipe: ncu's pipe / issue utilisation ratio scaled to the live issue rate
+        ia = tr.get("issue_active_pct") or 0.0
+        if ia > 0:
+            fr = {"issue": f_issue}
+            for name, key in (("fma pipe", "fma_pipe_pct"), ("xu (MUFU) pipe", "xu_pipe_pct"),
+                              ("alu pipe", "alu_pipe_pct")):
+                if tr.get(key) is not None:
+                    fr[name] = f_issue * tr[key] / ia
+            out["pipe_fracs"] = fr
+            top = max(fr, key=fr.get)
+            if top != "issue":
+                out.update(bound=top, frac=fr[top],
+                           frac_note=f"{top} utilisation = live issue fraction x ncu {top} / issue-active")
     return out
 
 
