@@ -34,6 +34,29 @@ class Variant(HostFedStep):
             self.names = []
         if not tgt:
             self.host_targets_saved = self.host_targets
+        if not down:
+            self.grads_host = self.grads_host[:1]
+            self.grads_dev_view = True
+
+    def step(self):
+        if self.v_down:
+            return super().step()
+        # same as HostFedStep.step without the gradient download
+        torch_ = torch
+        s = self.k % 2
+        main = torch_.cuda.current_stream(self.runner.eng.device)
+        if not self.staged[s]:
+            self._upload(s)
+        self.staged[s] = False
+        if self.lookahead:
+            nxt = (self.k + 1) % 2
+            self._upload(nxt)
+            self.staged[nxt] = True
+        main.wait_event(self.scene_up[s])
+        self.runner(self.ds[s], self.tg[s], ready=self.tgt_up[s], grads=self.grads[s], loss=self.loss[s])
+        self.computed[s].record(main)
+        self.used[s] = True
+        self.k += 1
 
     def _upload(self, s):
         if not self.v_tgt:
@@ -65,8 +88,9 @@ def main():
     if s.sh is not None:
         host["sh"] = torch.from_numpy(np.ascontiguousarray(s.sh)).pin_memory()
     print("device step        %.2f ms" % timed(lambda: runner(ds, targets)))
-    for name, kw in [("fed lookahead", {}), ("fed no scene", dict(scene=False)),
-                     ("fed no targets", dict(tgt=False)), ("fed no uploads", dict(scene=False, tgt=False))]:
+    for name, kw in [("fed lookahead", {}), ("fed no downloads", dict(down=False)),
+                     ("fed no uploads", dict(scene=False, tgt=False)),
+                     ("fed no copies", dict(scene=False, tgt=False, down=False))]:
         fed = Variant(runner, host, htgt, lookahead=True, **kw)
 
         def f():
