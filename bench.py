@@ -51,6 +51,8 @@ def parse():
                     choices=["tiny", "medium", "large", "opaque", "tomography"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--views", type=int, default=0, help="limit the number of views (0 = all)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="fixed-order gradient reductions (the drop-in backward's default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tiles", type=int, default=0, help="tiles in the CPU sample (0 = auto)")
@@ -148,7 +150,7 @@ def run_gpu(args):
     cfg = load_config(args.config, args.views)
     tomo = cfg.tomography
     my_views = shard(len(cfg.cameras), ws, rank)
-    eng = Engine(local)
+    eng = Engine(local, deterministic=args.deterministic)
     ds = eng.upload(cfg.scene)
     cams = cfg.cameras
     H, W = int(cams[0].height), int(cams[0].width)
@@ -233,7 +235,9 @@ def run_gpu(args):
             "config": {"workload": cfg.description,
                        "views_per_step": len(cams), "pixels_per_step": px_step,
                        "gaussians": len(cfg.scene), "parallelism": f"views sharded over {ws} GPU(s)",
-                       "l2_flush": "inputs larger than L2 (scene + SH coefficients > 126 MB)"},
+                       "l2_flush": "inputs larger than L2 (scene + SH coefficients > 126 MB)",
+                       "gradient_reduction": "deterministic (fixed order)" if args.deterministic
+                       else "atomic"},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "kernels": kernels,
             "roofline": roof, "loss": loss_val,
         }

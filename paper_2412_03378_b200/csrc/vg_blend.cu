@@ -367,6 +367,12 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
   v[9] = hsum(h);
 }
 
+// Deterministic mode: slot idx of the per-(entry, warp) partials (the caller
+// numbers them: compact -- running count of visible pairs -- or pos * 4 + warp).
+__device__ __forceinline__ float* det_slot(const BwdIO& io, size_t idx) {
+  return io.det_part + idx * ACC_STRIDE;
+}
+
 // One entry of the backward replay for the lane's two pixels (shared by the
 // staged and the warp-independent kernels): recompute alpha exactly as the
 // forward did, advance T and the running suffix, form dL/de for live pixels,
@@ -374,7 +380,7 @@ __device__ __forceinline__ void pinhole_grad_terms(const Pair2& e, const SRec& s
 template <bool CUT, bool DET>
 __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in0, bool in1,
                                           F2 dcr, F2 dcg, F2 dcb, F2 tot, const BlendParams& p,
-                                          F2& T, F2& P, int lane, const BwdIO& io, uint32_t pos,
+                                          F2& T, F2& P, int lane, const BwdIO& io, size_t pos,
                                           float* wb) {
   // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
   // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
@@ -415,13 +421,12 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
   if (lane == 0 && any_vis) io.visible[gid] = 1;
 #if VG_SMEM_RED
   if (DET)
-    flush_det_smem(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE,
-                   wb);
+    flush_det_smem(v, lane, det_slot(io, pos), wb);
   else
     flush_acc_smem(v, lane, gid, io.acc, wb);
 #else
   if (DET)
-    flush_det(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE);
+    flush_det(v, lane, det_slot(io, pos));
   else
     flush_acc(v, lane, gid, io.acc);
 #endif
@@ -463,13 +468,12 @@ __device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool
 
 template <bool DET>
 __device__ __forceinline__ void bwd_flush(const SRec& s, const Replay& r, float (&v)[16], int lane,
-                                          const BwdIO& io, uint32_t pos, float* wb) {
+                                          const BwdIO& io, size_t pos, float* wb) {
   if (!r.flush) return;
   const uint32_t gid = __float_as_uint(s.c.w);
   if (lane == 0 && r.any_vis) io.visible[gid] = 1;
   if (DET)
-    flush_det_smem(v, lane, io.det_part + ((size_t)pos * (NT / 32) + (threadIdx.x >> 5)) * ACC_STRIDE,
-                   wb);
+    flush_det_smem(v, lane, det_slot(io, pos), wb);
   else
     flush_acc_smem(v, lane, gid, io.acc, wb);
 }
@@ -478,7 +482,7 @@ template <bool CUT, bool DET>
 __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, const SRec& sb,
                                            const Pair2& eb, bool in0, bool in1, F2 dcr, F2 dcg, F2 dcb,
                                            F2 tot, const BlendParams& p, F2& T, F2& P, int lane,
-                                           const BwdIO& io, uint32_t pa, uint32_t pb, float* wb) {
+                                           const BwdIO& io, size_t pa, size_t pb, float* wb) {
   const Replay ra = bwd_replay<CUT>(sa, ea, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   const Replay rb = bwd_replay<CUT>(sb, eb, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   float va[16], vb[16];
@@ -501,9 +505,9 @@ __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, cons
   if (!(lane & 1) && lane < 26) {
     const int q = lane >> 1;
     if (DET) {
-      const size_t w = threadIdx.x >> 5;
-      if (xa != 0.f) io.det_part[((size_t)pa * (NT / 32) + w) * ACC_STRIDE + q] = xa;
-      if (xb != 0.f) io.det_part[((size_t)pb * (NT / 32) + w) * ACC_STRIDE + q] = xb;
+      // every value is stored (compact slots are not pre-zeroed)
+      det_slot(io, pa)[q] = xa;
+      det_slot(io, pb)[q] = xb;
     } else {
       if (xa != 0.f) atomicAdd(io.acc + (size_t)ga * ACC_STRIDE + q, xa);
       if (xb != 0.f) atomicAdd(io.acc + (size_t)gb * ACC_STRIDE + q, xb);
@@ -547,6 +551,17 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   // transmittance (so the same activity and the same early exits)
   F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f), P = f2s(0.f);
   bool done = !(G.in0 || G.in1);
+  // deterministic slots: compact ones are numbered by the running count of this
+  // warp's visible pairs (the backward walks exactly those, in list order)
+  size_t dnext = 0;
+  if (DET && io.det_pref) {
+    const size_t wi = (size_t)warp * io.det_vm_words + (r.x >> 5);
+    dnext = io.det_pref[wi] + __popc(io.det_vm[wi] & ((1u << (r.x & 31u)) - 1u));
+  }
+  auto dslot = [&](uint32_t pos) -> size_t {
+    if (!DET) return 0;
+    return io.det_pref ? dnext++ : (size_t)pos * (NT / 32) + warp;
+  };
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     if (__syncthreads_count(done) == NT) break;
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
@@ -585,15 +600,19 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
 #if VG_BWD_PAIR
+          const size_t ia = dslot(base + k);
+          const size_t ib = dslot(base + kb);
           bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                               base + k, base + kb, wb);
+                               ia, ib, wb);
 #else
-          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k, wb);
-          bwd_entry<CUT, DET>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                              base + kb, wb);
+          const size_t ia = dslot(base + k);
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
+          const size_t ib = dslot(base + kb);
+          bwd_entry<CUT, DET>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ib, wb);
 #endif
         } else {
-          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, base + k, wb);
+          const size_t ia = dslot(base + k);
+          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
         }
       }
       done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);

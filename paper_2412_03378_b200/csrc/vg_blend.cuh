@@ -186,7 +186,7 @@ __device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, u
 
 __device__ __forceinline__ void flush_det_smem(const float (&v)[16], int lane, float* slot, float* wb) {
   const float s = smem_reduce13(v, lane, wb);
-  if (!(lane & 1) && lane < 26 && s != 0.f) slot[lane >> 1] = s;
+  if (!(lane & 1) && lane < 26) slot[lane >> 1] = s;
 }
 
 // Deterministic mode: the warp's 13 sums go to the (entry, warp) slot (no
@@ -194,7 +194,7 @@ __device__ __forceinline__ void flush_det_smem(const float (&v)[16], int lane, f
 __device__ __forceinline__ void flush_det(float (&v)[16], int lane, float* slot) {
   float s = transpose_reduce16(v, lane);
   int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-  if (!(lane & 1) && idx < 13 && s != 0.f) slot[idx] = s;
+  if (!(lane & 1) && idx < 13) slot[idx] = s;
 }
 
 // Block sum of 3 floats + 1 double into global (d_background, loss).

@@ -63,6 +63,7 @@ struct vg_context {
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf tpart;                         // tomography forward: per-split partial images
+  Buf det_pref, det_vcnt, det_vscan;  // deterministic mode: compact slot prefix
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
@@ -215,7 +216,7 @@ void vg_destroy(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -652,7 +653,8 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
 
 // Deterministic mode: the Gaussian -> slot map of the current lists (once per
 // prepare) and zeroed per-(entry, warp) slots for one backward.
-static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cudaStream_t st) {
+static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cudaStream_t st,
+                     BwdIO* compact = nullptr) {
   const int64_t n = c->scene.n, P = c->pairs;
   if (!c->det_ready) {
     VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
@@ -665,7 +667,21 @@ static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cud
     c->det_ready = true;
   }
   VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
-  VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+  if (compact) {
+    // one slot per (entry, warp) pair the forward marked visible; every slot
+    // is written by the backward, so no clearing
+    const int words = c->vm_words;
+    VG_TRY(ensure(c->det_pref, sizeof(uint32_t) * (4 * (size_t)words + 1), st));
+    VG_TRY(ensure(c->det_vcnt, sizeof(uint32_t) * 4 * (size_t)words, st));
+    VG_TRY(ensure(c->det_vscan, det_prefix_scratch_bytes(words), st));
+    VG_CUDA(det_prefix((const uint32_t*)c->vmask.p, words, (uint32_t*)c->det_vcnt.p,
+                       (uint32_t*)c->det_pref.p, c->det_vscan.p, st));
+    compact->det_vm = (const uint32_t*)c->vmask.p;
+    compact->det_pref = (const uint32_t*)c->det_pref.p;
+    compact->det_vm_words = words;
+  } else {
+    VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+  }
   VG_TRY(ensure(c->det_bg, sizeof(float) * 3 * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->det_loss, sizeof(double) * (size_t)c->n_tiles, st));
   VG_CUDA(cudaMemsetAsync(c->det_bg.p, 0, sizeof(float) * 3 * (size_t)c->n_tiles, st));
@@ -701,11 +717,13 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     io.visible = (uint8_t*)c->offset.p;
   }
   const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
-  if (det) VG_TRY(det_setup(c, io.det_part, io.det_bg, io.det_loss, st));
+  const bool vm = c->vmask_valid && c->opt.alpha_cut > 0;
+  if (det)
+    VG_TRY(det_setup(c, io.det_part, io.det_bg, io.det_loss, st,
+                     vm && c->opt.mode != VG_MODE_SPLAT ? &io : nullptr));
   if (c->scene.n > 0) {
     {
       ProfScope ps(c, VG_K_RENDER_BWD, st);
-      const bool vm = c->vmask_valid && c->opt.alpha_cut > 0;
       if (c->opt.mode == VG_MODE_SPLAT)
         launch_splat_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                          (const uint32_t*)c->tord.p, p, target ? 1 : 0, io, st);
@@ -720,7 +738,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                          (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                          (float*)c->acc.p, c->n_tiles, (const float*)c->det_bg.p,
                          target ? (const double*)c->det_loss.p : nullptr, g->d_background,
-                         loss_sum, st));
+                         loss_sum, st, io.det_vm, io.det_pref, io.det_vm_words));
       VG_LAUNCHED(c, 2);
     }
     VG_TRY(finish_view(c, g, st));

@@ -41,31 +41,59 @@ __global__ void k_pair_slots(const uint2* __restrict__ ranges, const uint32_t* _
   }
 }
 
-__global__ void k_det_reduce(int64_t n, const uint32_t* __restrict__ cnt,
-                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ slot,
-                             const float* __restrict__ part, float* __restrict__ acc) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
-  const uint32_t c = cnt[g];
-  if (!c) return;
+// Four lanes per Gaussian: lane w sums warp slot w of each of the Gaussian's
+// tiles in tile order, then the four partials are combined as
+// (w0 + w1) + (w2 + w3) -- a fixed order.  COMPACT: only the (entry, warp)
+// pairs set in the forward's visibility mask have slots (the others
+// contributed nothing).
+template <bool COMPACT>
+__global__ void __launch_bounds__(256) k_det_reduce(int64_t n, const uint32_t* __restrict__ cnt,
+                                                    const uint32_t* __restrict__ off,
+                                                    const uint32_t* __restrict__ slot,
+                                                    const float* __restrict__ part, float* __restrict__ acc,
+                                                    const uint32_t* __restrict__ vm,
+                                                    const uint32_t* __restrict__ pref, int vm_words) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t g = t >> 2;
+  const int w = (int)(t & 3);
+  const uint32_t c = g < n ? cnt[g] : 0u;
   float s[13];
 #pragma unroll
   for (int q = 0; q < 13; ++q) s[q] = 0.f;
-  const uint32_t o = off[g];
+  const uint32_t o = g < n ? off[g] : 0u;
   for (uint32_t k = 0; k < c; ++k) {
-    const float* pp = part + (size_t)slot[o + k] * DET_WARPS * DET_STRIDE;
-    for (int w = 0; w < DET_WARPS; ++w) {
-      const float4* p4 = reinterpret_cast<const float4*>(pp + w * DET_STRIDE);
-      const float4 a = p4[0], b = p4[1], d = p4[2], e = p4[3];
-      s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
-      s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-      s[8] += d.x; s[9] += d.y; s[10] += d.z; s[11] += d.w;
-      s[12] += e.x;
+    const uint32_t p = slot[o + k];
+    size_t idx;
+    if (COMPACT) {
+      const size_t wi = (size_t)w * vm_words + (p >> 5);
+      const uint32_t word = vm[wi];
+      if (!((word >> (p & 31u)) & 1u)) continue;
+      idx = pref[wi] + __popc(word & ((1u << (p & 31u)) - 1u));
+    } else {
+      idx = (size_t)p * DET_WARPS + w;
     }
+    const float4* p4 = reinterpret_cast<const float4*>(part + idx * DET_STRIDE);
+    const float4 a = p4[0], b = p4[1], d = p4[2], e = p4[3];
+    s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w;
+    s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+    s[8] += d.x; s[9] += d.y; s[10] += d.z; s[11] += d.w;
+    s[12] += e.x;
   }
-  float* a = acc + 16 * g;
 #pragma unroll
-  for (int q = 0; q < 13; ++q) a[q] += s[q];
+  for (int q = 0; q < 13; ++q) {
+    s[q] += __shfl_xor_sync(0xffffffffu, s[q], 1);
+    s[q] += __shfl_xor_sync(0xffffffffu, s[q], 2);
+  }
+  if (g < n && w == 0 && c) {
+    float* a = acc + 16 * g;
+#pragma unroll
+    for (int q = 0; q < 13; ++q) a[q] += s[q];
+  }
+}
+
+__global__ void k_vm_popc(int64_t words, const uint32_t* __restrict__ vm, uint32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < words) cnt[i] = __popc(vm[i]);
 }
 
 // Fixed-order sum of the per-tile d_background (3 floats) and loss (double)
@@ -95,6 +123,16 @@ __global__ void __launch_bounds__(256) k_det_tiles(int n_tiles, const float* __r
   }
 }
 
+size_t det_prefix_scratch_bytes(int vm_words) { return scan_u32_scratch_bytes(4 * (int64_t)vm_words) + 16; }
+
+// pref[i] = number of set bits in vm[0 .. i) over the 4 rows (row-major); pref[4 vm_words] = total
+cudaError_t det_prefix(const uint32_t* vm, int vm_words, uint32_t* cnt_tmp, uint32_t* pref,
+                       void* scratch, cudaStream_t st) {
+  const int64_t words = 4 * (int64_t)vm_words;
+  k_vm_popc<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(words, vm, cnt_tmp);
+  return scan_u32(cnt_tmp, pref, scratch, pref + words, words, st);
+}
+
 size_t det_part_bytes(int64_t pairs) {
   return sizeof(float) * (size_t)pairs * DET_WARPS * DET_STRIDE;
 }
@@ -113,8 +151,12 @@ cudaError_t det_prepare(int64_t n, const ushort4* rect, const uint2* ranges, con
 cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, const uint32_t* slot,
                        const float* part, float* acc, int n_tiles, const float* bg_part,
                        const double* loss_part, float* d_background, double* loss_sum,
-                       cudaStream_t st) {
-  if (n > 0) k_det_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, cnt, off, slot, part, acc);
+                       cudaStream_t st, const uint32_t* vm, const uint32_t* pref, int vm_words) {
+  const unsigned blocks = (unsigned)((4 * n + 255) / 256);
+  if (n > 0 && pref)
+    k_det_reduce<true><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, vm, pref, vm_words);
+  else if (n > 0)
+    k_det_reduce<false><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, nullptr, nullptr, 0);
   k_det_tiles<<<1, 256, 0, st>>>(n_tiles, bg_part, loss_part, d_background, loss_sum);
   return cudaGetLastError();
 }

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", default="large")
     ap.add_argument("--views", type=int, default=3)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--deterministic", action="store_true")
     args = ap.parse_args()
     import torch
     from paper_2412_03378_b200 import configs
@@ -22,7 +23,7 @@ def main():
     from paper_2412_03378_b200.multiview import ViewShardedStep
     cfg = configs.BY_NAME[args.config]()
     cams = cfg.cameras[:args.views]
-    eng = Engine()
+    eng = Engine(deterministic=args.deterministic)
     ds = eng.upload(cfg.scene)
     H, W = cams[0].height, cams[0].width
     shape = (H, W) if cfg.tomography else (H, W, 3)
