@@ -38,6 +38,9 @@
 #ifndef VG_FWD_MINB
 #define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
 #endif
+#ifndef VG_SEEN_REDUX
+#define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
+#endif
 #ifndef VG_BWD_MINB
 #define VG_BWD_MINB 6   // <= 80 registers (shared memory also caps it at 6 CTAs)
 #endif
@@ -265,7 +268,12 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         Cg = fma2(w, f2s(s.d.y), Cg);
         Cb = fma2(w, f2s(s.d.z), Cb);
         T = mul2(T, om);
+#if VG_SEEN_REDUX
+        // per-lane bits, OR-reduced over the warp once per chunk
+        if (vmask) seen |= (om0 < 1.f || om1 < 1.f ? 1u : 0u) << (k - c);
+#else
         if (vmask && __any_sync(FULL, om0 < 1.f || om1 < 1.f)) seen |= 1u << (k - c);
+#endif
         if (STATS) {
           st_proc++;
           st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
@@ -289,6 +297,9 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
           composite(k, s, e);
         }
       }
+#if VG_SEEN_REDUX
+      if (vmask) seen = __reduce_or_sync(FULL, seen);
+#endif
       if (vmask && seen && lane == 0) {
         // record (entry, warp) visibility for the backward: bit g of this warp's row
         const uint32_t g = base + c;
@@ -385,9 +396,9 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
   // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
   // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
+  // cut: skipped below alpha_cut (raster.py:363-365) or inactive
   float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
   float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-  // cut: skipped below alpha_cut (raster.py:363-365) or inactive
   const bool cut0 = CUT ? om0 > p.omcut : !act0;
   const bool cut1 = CUT ? om1 > p.omcut : !act1;
   om0 = cut0 ? 1.f : om0;
