@@ -562,16 +562,12 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   // transmittance (so the same activity and the same early exits)
   F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f), P = f2s(0.f);
   bool done = !(G.in0 || G.in1);
-  // deterministic slots: compact ones are numbered by the running count of this
-  // warp's visible pairs (the backward walks exactly those, in list order)
-  size_t dnext = 0;
-  if (DET && io.det_pref) {
-    const size_t wi = (size_t)warp * io.det_vm_words + (r.x >> 5);
-    dnext = io.det_pref[wi] + __popc(io.det_vm[wi] & ((1u << (r.x & 31u)) - 1u));
-  }
-  auto dslot = [&](uint32_t pos) -> size_t {
+  // compact slots: the staging put entry k's slot base in sm[k].d.w and its
+  // four warp bits in smask[k]
+  auto dslot = [&](uint32_t pos, const SRec& s, int k) -> size_t {
     if (!DET) return 0;
-    return io.det_pref ? dnext++ : (size_t)pos * (NT / 32) + warp;
+    if (io.det_pbase) return __float_as_uint(s.d.w) + __popc(smask[k] & ((1u << warp) - 1u));
+    return (size_t)pos * (NT / 32) + warp;
   };
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     if (__syncthreads_count(done) == NT) break;
@@ -580,6 +576,10 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
       if (i < r.y) {
         const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
         if (!vmask) smask[sidx] = (uint8_t)m;
+        if (DET && io.det_pbase) {
+          sm[sidx].d.w = __uint_as_float(io.det_pbase[i]);
+          smask[sidx] = io.det_vis4[i];
+        }
       }
     }
     __syncthreads();
@@ -611,18 +611,18 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
 #if VG_BWD_PAIR
-          const size_t ia = dslot(base + k);
-          const size_t ib = dslot(base + kb);
+          const size_t ia = dslot(base + k, s, k);
+          const size_t ib = dslot(base + kb, sb, kb);
           bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
                                ia, ib, wb);
 #else
-          const size_t ia = dslot(base + k);
+          const size_t ia = dslot(base + k, s, k);
           bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
-          const size_t ib = dslot(base + kb);
+          const size_t ib = dslot(base + kb, sb, kb);
           bwd_entry<CUT, DET>(sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ib, wb);
 #endif
         } else {
-          const size_t ia = dslot(base + k);
+          const size_t ia = dslot(base + k, s, k);
           bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
         }
       }

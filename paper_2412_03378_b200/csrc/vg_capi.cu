@@ -63,7 +63,7 @@ struct vg_context {
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf tpart;                         // tomography forward: per-split partial images
-  Buf det_pref, det_vcnt, det_vscan;  // deterministic mode: compact slot prefix
+  Buf det_pref, det_vcnt, det_vscan, det_vis4;  // deterministic mode: compact pair-major slots
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
@@ -216,7 +216,7 @@ void vg_destroy(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan, &c->det_vis4};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -668,17 +668,16 @@ static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cud
   }
   VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
   if (compact) {
-    // one slot per (entry, warp) pair the forward marked visible; every slot
-    // is written by the backward, so no clearing
-    const int words = c->vm_words;
-    VG_TRY(ensure(c->det_pref, sizeof(uint32_t) * (4 * (size_t)words + 1), st));
-    VG_TRY(ensure(c->det_vcnt, sizeof(uint32_t) * 4 * (size_t)words, st));
-    VG_TRY(ensure(c->det_vscan, det_prefix_scratch_bytes(words), st));
-    VG_CUDA(det_prefix((const uint32_t*)c->vmask.p, words, (uint32_t*)c->det_vcnt.p,
-                       (uint32_t*)c->det_pref.p, c->det_vscan.p, st));
-    compact->det_vm = (const uint32_t*)c->vmask.p;
-    compact->det_pref = (const uint32_t*)c->det_pref.p;
-    compact->det_vm_words = words;
+    // one slot per (entry, warp) pair the forward marked visible, pair-major;
+    // every slot is written by the backward, so no clearing
+    VG_TRY(ensure(c->det_pref, sizeof(uint32_t) * ((size_t)P + 1), st));
+    VG_TRY(ensure(c->det_vcnt, sizeof(uint32_t) * (size_t)P, st));
+    VG_TRY(ensure(c->det_vis4, (size_t)P, st));
+    VG_TRY(ensure(c->det_vscan, det_pairs_scratch_bytes(P), st));
+    VG_CUDA(det_pairs((const uint32_t*)c->vmask.p, c->vm_words, P, (uint8_t*)c->det_vis4.p,
+                      (uint32_t*)c->det_vcnt.p, (uint32_t*)c->det_pref.p, c->det_vscan.p, st));
+    compact->det_pbase = (const uint32_t*)c->det_pref.p;
+    compact->det_vis4 = (const uint8_t*)c->det_vis4.p;
   } else {
     VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
   }
@@ -738,7 +737,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                          (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                          (float*)c->acc.p, c->n_tiles, (const float*)c->det_bg.p,
                          target ? (const double*)c->det_loss.p : nullptr, g->d_background,
-                         loss_sum, st, io.det_vm, io.det_pref, io.det_vm_words));
+                         loss_sum, st, io.det_pbase, io.det_vis4));
       VG_LAUNCHED(c, 2);
     }
     VG_TRY(finish_view(c, g, st));

@@ -44,15 +44,15 @@ __global__ void k_pair_slots(const uint2* __restrict__ ranges, const uint32_t* _
 // Four lanes per Gaussian: lane w sums warp slot w of each of the Gaussian's
 // tiles in tile order, then the four partials are combined as
 // (w0 + w1) + (w2 + w3) -- a fixed order.  COMPACT: only the (entry, warp)
-// pairs set in the forward's visibility mask have slots (the others
-// contributed nothing).
+// pairs set in the forward's visibility mask have slots, numbered pair-major
+// (the others contributed nothing).
 template <bool COMPACT>
 __global__ void __launch_bounds__(256) k_det_reduce(int64_t n, const uint32_t* __restrict__ cnt,
                                                     const uint32_t* __restrict__ off,
                                                     const uint32_t* __restrict__ slot,
                                                     const float* __restrict__ part, float* __restrict__ acc,
-                                                    const uint32_t* __restrict__ vm,
-                                                    const uint32_t* __restrict__ pref, int vm_words) {
+                                                    const uint32_t* __restrict__ pbase,
+                                                    const uint8_t* __restrict__ vis4) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t g = t >> 2;
   const int w = (int)(t & 3);
@@ -65,10 +65,9 @@ __global__ void __launch_bounds__(256) k_det_reduce(int64_t n, const uint32_t* _
     const uint32_t p = slot[o + k];
     size_t idx;
     if (COMPACT) {
-      const size_t wi = (size_t)w * vm_words + (p >> 5);
-      const uint32_t word = vm[wi];
-      if (!((word >> (p & 31u)) & 1u)) continue;
-      idx = pref[wi] + __popc(word & ((1u << (p & 31u)) - 1u));
+      const uint32_t v = vis4[p];
+      if (!((v >> w) & 1u)) continue;
+      idx = pbase[p] + __popc(v & ((1u << w) - 1u));
     } else {
       idx = (size_t)p * DET_WARPS + w;
     }
@@ -91,9 +90,17 @@ __global__ void __launch_bounds__(256) k_det_reduce(int64_t n, const uint32_t* _
   }
 }
 
-__global__ void k_vm_popc(int64_t words, const uint32_t* __restrict__ vm, uint32_t* __restrict__ cnt) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < words) cnt[i] = __popc(vm[i]);
+__global__ void k_pair_vis(int64_t pairs, const uint32_t* __restrict__ vm, int vm_words,
+                           uint8_t* __restrict__ vis4, uint32_t* __restrict__ cnt) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= pairs) return;
+  const size_t wi = (size_t)(p >> 5);
+  const uint32_t sh = (uint32_t)(p & 31);
+  uint32_t v = 0;
+#pragma unroll
+  for (int w = 0; w < DET_WARPS; ++w) v |= ((vm[(size_t)w * vm_words + wi] >> sh) & 1u) << w;
+  vis4[p] = (uint8_t)v;
+  cnt[p] = __popc(v);
 }
 
 // Fixed-order sum of the per-tile d_background (3 floats) and loss (double)
@@ -123,14 +130,12 @@ __global__ void __launch_bounds__(256) k_det_tiles(int n_tiles, const float* __r
   }
 }
 
-size_t det_prefix_scratch_bytes(int vm_words) { return scan_u32_scratch_bytes(4 * (int64_t)vm_words) + 16; }
+size_t det_pairs_scratch_bytes(int64_t pairs) { return scan_u32_scratch_bytes(pairs) + 16; }
 
-// pref[i] = number of set bits in vm[0 .. i) over the 4 rows (row-major); pref[4 vm_words] = total
-cudaError_t det_prefix(const uint32_t* vm, int vm_words, uint32_t* cnt_tmp, uint32_t* pref,
-                       void* scratch, cudaStream_t st) {
-  const int64_t words = 4 * (int64_t)vm_words;
-  k_vm_popc<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(words, vm, cnt_tmp);
-  return scan_u32(cnt_tmp, pref, scratch, pref + words, words, st);
+cudaError_t det_pairs(const uint32_t* vm, int vm_words, int64_t pairs, uint8_t* vis4, uint32_t* cnt_tmp,
+                      uint32_t* pbase, void* scratch, cudaStream_t st) {
+  k_pair_vis<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(pairs, vm, vm_words, vis4, cnt_tmp);
+  return scan_u32(cnt_tmp, pbase, scratch, pbase + pairs, pairs, st);
 }
 
 size_t det_part_bytes(int64_t pairs) {
@@ -151,12 +156,12 @@ cudaError_t det_prepare(int64_t n, const ushort4* rect, const uint2* ranges, con
 cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, const uint32_t* slot,
                        const float* part, float* acc, int n_tiles, const float* bg_part,
                        const double* loss_part, float* d_background, double* loss_sum,
-                       cudaStream_t st, const uint32_t* vm, const uint32_t* pref, int vm_words) {
+                       cudaStream_t st, const uint32_t* pbase, const uint8_t* vis4) {
   const unsigned blocks = (unsigned)((4 * n + 255) / 256);
-  if (n > 0 && pref)
-    k_det_reduce<true><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, vm, pref, vm_words);
+  if (n > 0 && pbase)
+    k_det_reduce<true><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, pbase, vis4);
   else if (n > 0)
-    k_det_reduce<false><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, nullptr, nullptr, 0);
+    k_det_reduce<false><<<blocks, 256, 0, st>>>(n, cnt, off, slot, part, acc, nullptr, nullptr);
   k_det_tiles<<<1, 256, 0, st>>>(n_tiles, bg_part, loss_part, d_background, loss_sum);
   return cudaGetLastError();
 }

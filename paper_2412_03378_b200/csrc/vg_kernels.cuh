@@ -36,10 +36,10 @@ struct BwdIO {
   float* det_bg = nullptr;
   double* det_loss = nullptr;
   // compact slots (render backward with a forward visibility mask): one slot per
-  // visible (entry, warp) pair, index = det_pref[word] + popcount below the bit
-  const uint32_t* det_vm = nullptr;
-  const uint32_t* det_pref = nullptr;
-  int det_vm_words = 0;
+  // visible (entry, warp) pair, pair-major: slot of (entry p, warp w) =
+  // det_pbase[p] + popcount(det_vis4[p] & ((1 << w) - 1))
+  const uint32_t* det_pbase = nullptr;
+  const uint8_t* det_vis4 = nullptr;
 };
 
 // gm (nullable): per binned Gaussian M and M (mean - centre) in float64, for sort_by="gamma"
@@ -65,12 +65,12 @@ cudaError_t det_prepare(int64_t n, const ushort4* rect, const uint2* ranges, con
 cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, const uint32_t* slot,
                        const float* part, float* acc, int n_tiles, const float* bg_part,
                        const double* loss_part, float* d_background, double* loss_sum,
-                       cudaStream_t st, const uint32_t* vm = nullptr, const uint32_t* pref = nullptr,
-                       int vm_words = 0);
-// compact-slot prefix of a visibility mask of 4 rows x vm_words words
-cudaError_t det_prefix(const uint32_t* vm, int vm_words, uint32_t* cnt_tmp, uint32_t* pref,
-                       void* scratch, cudaStream_t st);
-size_t det_prefix_scratch_bytes(int vm_words);
+                       cudaStream_t st, const uint32_t* pbase = nullptr, const uint8_t* vis4 = nullptr);
+// compact pair-major slots from a visibility mask of 4 rows x vm_words words:
+// vis4[p] = the 4 warp bits of entry p, pbase[p] = slots before entry p (pbase[P] = total)
+cudaError_t det_pairs(const uint32_t* vm, int vm_words, int64_t pairs, uint8_t* vis4, uint32_t* cnt_tmp,
+                      uint32_t* pbase, void* scratch, cudaStream_t st);
+size_t det_pairs_scratch_bytes(int64_t pairs);
 // sort_by="gamma" re-sort of every tile list (vg_gamma.cu)
 size_t gamma_scratch_bytes(int64_t pairs);
 void launch_gamma_sort(int n_tiles, const uint2* ranges, uint32_t* vals, const double* gm,
