@@ -588,12 +588,14 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
       unsigned bits;
       if (vmask) {
         // exact: the entries where the forward saw a visible pixel in this block
-        const uint32_t g = base + c;
-        const uint32_t* row = vmask + (size_t)warp * vm_words + (g >> 5);
-        const uint32_t sh = g & 31u;
-        bits = __ldg(row) >> sh;
-        if (sh) bits |= __ldg(row + 1) << (32u - sh);
-        if (nb - c < 32) bits &= (1u << (nb - c)) - 1u;
+        // lane l tests entry base + c + l; the ballot makes the mask
+        // warp-uniform for the compiler (uniform bit scan and loop, no
+        // divergence bookkeeping: backward -6 % on config 3, -12 % on config 4
+        // against extracting the 32 bits from the mask words per lane)
+        const uint32_t g = base + c + lane;
+        const bool vb = (c + lane < nb) &&
+                        ((__ldg(vmask + (size_t)warp * vm_words + (g >> 5)) >> (g & 31u)) & 1u);
+        bits = __ballot_sync(FULL, vb);
       } else {
         const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
         bits = __ballot_sync(FULL, vb);
