@@ -520,8 +520,9 @@ __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, cons
       det_slot(io, pa)[q] = xa;
       det_slot(io, pb)[q] = xb;
     } else {
-      if (xa != 0.f) atomicAdd(io.acc + (size_t)ga * ACC_STRIDE + q, xa);
-      if (xb != 0.f) atomicAdd(io.acc + (size_t)gb * ACC_STRIDE + q, xb);
+      // unconditional: a zero test per value costs more than the rare zero add
+      atomicAdd(io.acc + (size_t)ga * ACC_STRIDE + q, xa);
+      atomicAdd(io.acc + (size_t)gb * ACC_STRIDE + q, xb);
     }
   }
 #else

@@ -181,7 +181,7 @@ __device__ __forceinline__ void smem_reduce13x2(const float (&va)[16], const flo
 __device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, uint32_t gid, float* acc,
                                                float* wb) {
   const float s = smem_reduce13(v, lane, wb);
-  if (!(lane & 1) && lane < 26 && s != 0.f) atomicAdd(acc + (size_t)gid * ACC_STRIDE + (lane >> 1), s);
+  if (!(lane & 1) && lane < 26) atomicAdd(acc + (size_t)gid * ACC_STRIDE + (lane >> 1), s);
 }
 
 __device__ __forceinline__ void flush_det_smem(const float (&v)[16], int lane, float* slot, float* wb) {
