@@ -30,7 +30,7 @@
 //   dL/de_i = dL/dalpha_i (1 - alpha_i) = dot_i T_after_i - suffix_i.
 // Per-Gaussian accumulators (13 floats, whitened e-frame, see vg_finalize.cu)
 // are summed over the lane's two pixels, warp-reduced through shared memory
-// (smem_reduce13x2: two entries per pass) and added with one 13-lane
+// (smem_reduce13x2p: two entries per pass, packed) and added with one 13-lane
 // red.global.add per warp and entry.
 #include "vg_blend.cuh"
 
@@ -46,8 +46,9 @@
 #endif
 #ifndef VG_BWD_PAIR
 // two visible entries per step: 1 = both replays, then both entries' gradient
-// terms, two reductions; 2 = the same with one shared-memory pass for both
-// (A/B on config 3, 16 views: backward 21.1 -> 20.0 -> 18.9 ms)
+// terms, two reductions; 2 = the same with one shared-memory pass for both,
+// packed 8-byte stores (A/B on config 3, 16 views: backward 21.1 -> 20.0 ->
+// 18.9 ms; packed pass 17.65 -> 17.28 ms)
 #define VG_BWD_PAIR 2
 #endif
 #ifndef VG_SMEM_RED
@@ -511,10 +512,10 @@ __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, cons
   const uint32_t ga = __float_as_uint(sa.c.w), gb = __float_as_uint(sb.c.w);
   if (lane == 0 && ra.any_vis) io.visible[ga] = 1;
   if (lane == 0 && rb.any_vis) io.visible[gb] = 1;
-  float xa, xb;
-  smem_reduce13x2(va, vb, lane, wb, xa, xb);
-  if (!(lane & 1) && lane < 26) {
-    const int q = lane >> 1;
+  const F2 xs = smem_reduce13x2p(va, vb, lane, wb);
+  const float xa = lo(xs), xb = hi(xs);
+  if (lane < 13) {
+    const int q = lane;
     if (DET) {
       // every value is stored (compact slots are not pre-zeroed)
       det_slot(io, pa)[q] = xa;
@@ -544,7 +545,8 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
                                                    int vm_words) {
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
-  __shared__ __align__(16) float sred[NT / 32][VG_SMEM_RED ? (VG_BWD_PAIR == 2 ? 2 : 1) * RED_WORDS : 4];
+  __shared__ __align__(16) float sred[NT / 32][VG_BWD_PAIR == 2 ? (REDP_WORDS > RED_WORDS ? REDP_WORDS : RED_WORDS)
+                                               : VG_SMEM_RED ? RED_WORDS : 4];
   const int tile = order[blockIdx.x];
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

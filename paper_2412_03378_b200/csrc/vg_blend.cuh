@@ -151,31 +151,37 @@ __device__ __forceinline__ float smem_reduce13(const float (&v)[16], int lane, f
   return s;
 }
 
-// The same for two entries at once (wb: 2 * RED_WORDS floats): lane 2q
-// returns the sums of value q of entry a (sa) and entry b (sb).
-__device__ __forceinline__ void smem_reduce13x2(const float (&va)[16], const float (&vb)[16], int lane,
-                                                float* wb, float& sa, float& sb) {
+// Packed variant for two entries: value q of both entries is stored as one
+// 8-byte pair per lane in row q (68 floats: 64 data + 4 pad, so that the 8
+// rows a quarter-warp reads start in distinct bank groups); lanes 0..12 sum
+// the lower half row of q = lane, lanes 16..28 the upper half of q = lane-16,
+// both entries at once in packed FP32x2 adds, and one exchange joins the
+// halves: lane q (< 13) returns (sum_a[q], sum_b[q]).  13 STS.64 instead of
+// 26 STS.32.
+constexpr int REDP_ROW = 68;
+constexpr int REDP_WORDS = 13 * REDP_ROW;
+__device__ __forceinline__ F2 smem_reduce13x2p(const float (&va)[16], const float (&vb)[16], int lane,
+                                               float* wb) {
 #pragma unroll
-  for (int q = 0; q < 13; ++q) {
-    wb[q * RED_ROW + lane] = va[q];
-    wb[(13 + q) * RED_ROW + lane] = vb[q];
-  }
+  for (int q = 0; q < 13; ++q)
+    *reinterpret_cast<unsigned long long*>(wb + q * REDP_ROW + 2 * lane) = f2(va[q], vb[q]).v;
   __syncwarp();
-  sa = sb = 0.f;
-  if (lane < 26) {
+  F2 acc = f2s(0.f);
+  const int q = lane & 15;
+  if (q < 13) {
+    const float4* src = reinterpret_cast<const float4*>(wb + q * REDP_ROW + (lane & 16) * 2);
+    F2 t[8];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const float4* src =
-          reinterpret_cast<const float4*>(wb + (13 * t + (lane >> 1)) * RED_ROW + (lane & 1) * 16);
-      const float4 x0 = src[0], x1 = src[1], x2 = src[2], x3 = src[3];
-      const F2 a = add2(add2(f2(x0.x, x0.y), f2(x1.x, x1.y)), add2(f2(x2.x, x2.y), f2(x3.x, x3.y)));
-      const F2 b = add2(add2(f2(x0.z, x0.w), f2(x1.z, x1.w)), add2(f2(x2.z, x2.w), f2(x3.z, x3.w)));
-      (t ? sb : sa) = hsum(add2(a, b));
+    for (int k = 0; k < 8; ++k) {
+      const float4 x = src[k];
+      t[k] = add2(f2(x.x, x.y), f2(x.z, x.w));
     }
+    acc = add2(add2(add2(t[0], t[1]), add2(t[2], t[3])), add2(add2(t[4], t[5]), add2(t[6], t[7])));
   }
-  sa += __shfl_xor_sync(FULL, sa, 1);
-  sb += __shfl_xor_sync(FULL, sb, 1);
+  F2 o;
+  o.v = __shfl_xor_sync(FULL, acc.v, 16);
   __syncwarp();
+  return add2(acc, o);
 }
 
 __device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, uint32_t gid, float* acc,
