@@ -100,14 +100,16 @@ static cudaEvent_t pool_event(vg_context* c) {
 }
 
 // Bracket a launch with events when profiling is on.  Outside profiling, the
-// launches of large views are still bracketed by timing events ("fences"):
-// measured on B200, bracketing both the side-stream binning and the
-// main-stream blend launches this way cuts the pipelined step 6% on 1080p
-// views (149.0 -> 139.8 ms on config 3, opaque 66.3 -> 63.2, tomography
-// 423.9 -> 413.9) -- it keeps the binning kernels from co-running with the
-// blend kernels in a way that slows the blends more than it hides -- while
-// at 640x480 the extra records cost 2.6%.  VG_FENCE overrides: bit 0 = binning
-// launches, bit 1 = blend launches, bit 2 = timing-free events (no gain).
+// launches of large views of a deterministic context are still bracketed by
+// timing events ("fences").  Measured on B200 with the blends of consecutive
+// views serialised on one stream (what the deterministic multi-view step
+// does): bracketing both the side-stream binning and the main-stream blend
+// launches this way cut config 3 from 149.0 to 139.8 ms per step -- it keeps
+// the binning kernels from co-running with the blends in a way that slowed
+// the blends more than it hid.  With the two alternating blend streams of the
+// atomic step they cost 0.5-5 % instead, and small views never gain, so they
+// are off there.  VG_FENCE overrides: bit 0 = binning launches, bit 1 = blend
+// launches, bit 2 = timing-free events (no gain).
 constexpr int FENCE_MIN_TILES = 4096;
 static int fence_mode(const vg_context* c) {
   static int m = -2;
@@ -116,7 +118,7 @@ static int fence_mode(const vg_context* c) {
     m = e ? atoi(e) : -1;
   }
   if (m >= 0) return m;
-  return c->n_tiles >= FENCE_MIN_TILES ? 3 : 0;
+  return c->opt.deterministic && c->n_tiles >= FENCE_MIN_TILES ? 3 : 0;
 }
 
 struct ProfScope {
