@@ -51,6 +51,9 @@
 // 18.9 ms; packed pass 17.65 -> 17.28 ms)
 #define VG_BWD_PAIR 2
 #endif
+#ifndef VG_TOMO_REC
+#define VG_TOMO_REC 1   // parallel-beam projector: row recurrence (k_tomo_fwd_rec), -21 % on config 5
+#endif
 #ifndef VG_SMEM_RED
 #define VG_SMEM_RED 1   // backward warp sums through shared memory (smem_reduce13)
 #endif
@@ -689,6 +692,110 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
   }
 }
 
+// Parallel-beam projector with a row recurrence (VG_TOMO_REC; the default --
+// config 5 projector 20.3 -> 16.0 ms over 45 views).  For parallel
+// rays the exponent along a tile column is a quadratic in the row index y,
+//   e(y) = -C (q1^2 + (A + B y)^2),  C = log2(e) / 2,
+// so h(y) = 2^e(y) obeys h(y+1) = h(y) r(y), r(y+1) = r(y) k with
+// k = 2^(-2 C B^2): four exp2 per entry and column (two anchors at rows 7 and
+// 8, one ratio each way, k) instead of sixteen, each sweep running from the
+// middle outwards.  An anchor far in the tail (e < -100) while the column
+// still reaches 2^-100 falls back to exp2 per pixel (narrow Gaussians, sub-
+// pixel scale); columns that never reach 2^-100 are skipped (< 1e-30).
+// Thread t owns column t & 15 for list entries = t >> 4 (mod 8); the eight
+// partial columns are summed in a fixed order at the end.
+__global__ void __launch_bounds__(NT) k_tomo_fwd_rec(const GRec* __restrict__ rec,
+                                                     const uint32_t* __restrict__ vals,
+                                                     const uint2* __restrict__ ranges,
+                                                     const uint32_t* __restrict__ order,
+                                                     BlendParams p, float* __restrict__ image,
+                                                     float* __restrict__ intensity,
+                                                     float* __restrict__ part) {
+  __shared__ SRec sm[BATCH];
+  __shared__ float sacc[NT / TILE][TILE_PIX];
+  const int tile = order[blockIdx.x];
+  const int split = blockIdx.y, S = gridDim.y;
+  const int tx = tile % p.ntx, ty = tile / p.ntx;
+  const int col = threadIdx.x & (TILE - 1), slice = threadIdx.x / TILE;
+  constexpr int NSL = NT / TILE;  // 8 entry slices
+  const float x = (float)col;
+  const uint2 r = ranges[tile];
+  F2 acc2[TILE / 2];
+#pragma unroll
+  for (int i = 0; i < TILE / 2; ++i) acc2[i] = f2s(0.f);
+  for (uint32_t base = r.x + split * BATCH; base < r.y; base += BATCH * S) {
+    __syncthreads();
+    for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
+      uint32_t i = base + sidx;
+      if (i < r.y) stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, false, 0.f);
+    }
+    __syncthreads();
+    const int nb = min((uint32_t)BATCH, r.y - base);
+    for (int k = slice; k < nb; k += NSL) {
+      const SRec s = sm[k];
+      const float q1 = fmaf(s.b.x, x, s.a.x);
+      const float A = fmaf(s.b.y, x, s.a.y);
+      const float B = s.b.z;
+      const float amp = s.c.z * s.b.w;  // E2 = amp * 2^e
+      const float q11 = q1 * q1;
+      // column maximum of e: (A + B y)^2 smallest at y* = -A / B, clamped to the column
+      const float ys = B != 0.f ? fminf(fmaxf(__fdividef(-A, B), 0.f), (float)(TILE - 1)) : 0.f;
+      const float zs = fmaf(B, ys, A);
+      const float emax = -C_HALF_LOG2E * fmaf(zs, zs, q11);
+      if (!(emax > -100.f)) continue;  // < 2^-100 everywhere in this column
+      const float z7 = fmaf(B, 7.f, A), z8 = fmaf(B, 8.f, A);
+      const float e7 = -C_HALF_LOG2E * fmaf(z7, z7, q11);
+      const float e8 = -C_HALF_LOG2E * fmaf(z8, z8, q11);
+      if (e7 < -100.f || e8 < -100.f) {
+        // anchors in the tail of a narrow Gaussian: direct evaluation
+#pragma unroll
+        for (int i = 0; i < TILE / 2; ++i) {
+          const float zu = fmaf(B, (float)(8 + i), A), zd = fmaf(B, (float)(7 - i), A);
+          acc2[i] = fma2(f2s(amp), f2(ex2f(-C_HALF_LOG2E * fmaf(zu, zu, q11)),
+                                      ex2f(-C_HALF_LOG2E * fmaf(zd, zd, q11))), acc2[i]);
+        }
+        continue;
+      }
+      const float kk = ex2f(-2.f * C_HALF_LOG2E * B * B);
+      // both sweeps at once in packed FP32x2: lo walks rows 8..15 from
+      // h(8) with h(9)/h(8) = 2^(-C B (2 z8 + B)), hi walks rows 7..0 from
+      // h(7) with h(6)/h(7) = 2^(C B (2 z7 - B)); accumulator pair i holds
+      // rows (8 + i, 7 - i)
+      F2 h = f2(ex2f(e8), ex2f(e7));
+      F2 rr = f2(ex2f(-C_HALF_LOG2E * B * fmaf(2.f, z8, B)), ex2f(C_HALF_LOG2E * B * fmaf(2.f, z7, -B)));
+      const F2 k2 = f2s(kk), a2 = f2s(amp);
+#pragma unroll
+      for (int i = 0; i < TILE / 2; ++i) {
+        acc2[i] = fma2(a2, h, acc2[i]);
+        h = mul2(h, rr);
+        rr = mul2(rr, k2);
+      }
+    }
+  }
+  // fixed-order sum of the eight slices
+#pragma unroll
+  for (int i = 0; i < TILE / 2; ++i) {
+    sacc[slice][(8 + i) * TILE + col] = lo(acc2[i]);
+    sacc[slice][(7 - i) * TILE + col] = hi(acc2[i]);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < TILE_PIX; q += NT) {
+    float sum = 0.f;
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) sum += sacc[sl][q];
+    const int c = tx * TILE + (q & (TILE - 1)), rw = ty * TILE + q / TILE;
+    if (c >= p.width || rw >= p.height) continue;
+    const int pix = rw * p.width + c;
+    if (S > 1) {
+      part[(size_t)split * p.width * p.height + pix] = sum;
+      continue;
+    }
+    const float I = sum * (float)LN2;
+    image[pix] = I;
+    if (intensity) intensity[pix] = __expf(-I);
+  }
+}
+
 // Sum of the per-split partial images in split order (deterministic).
 __global__ void k_tomo_combine(int npix, int S, const float* __restrict__ part, float* __restrict__ image,
                                float* __restrict__ intensity) {
@@ -884,6 +991,8 @@ void launch_tomo_fwd(int n_tiles, int ray, const GRec* rec, const uint32_t* vals
   const dim3 grid(n_tiles, splits);
   if (ray == VG_PINHOLE)
     k_tomo_fwd<VG_PINHOLE><<<grid, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity, part);
+  else if (VG_TOMO_REC)
+    k_tomo_fwd_rec<<<grid, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity, part);
   else
     k_tomo_fwd<VG_PARALLEL><<<grid, NT, 0, st>>>(rec, vals, ranges, order, p, image, intensity, part);
   if (splits > 1) {
