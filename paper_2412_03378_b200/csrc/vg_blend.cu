@@ -51,6 +51,13 @@
 // 18.9 ms; packed pass 17.65 -> 17.28 ms)
 #define VG_BWD_PAIR 2
 #endif
+#ifndef VG_TOMO_SKIP
+// projector: (entry, column) pairs whose peak in the column is below 2^-60 of
+// the Gaussian's peak (< 1e-18 relative; far below float32 resolution) are not
+// summed (-40: another 3.5 %, but that is the size of the reference's own
+// binning cut and is left alone)
+#define VG_TOMO_SKIP -60.f
+#endif
 #ifndef VG_TOMO_REC
 #define VG_TOMO_REC 1   // parallel-beam projector: row recurrence (k_tomo_fwd_rec), -21 % on config 5
 #endif
@@ -700,8 +707,8 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd(const GRec* __restrict__ rec,
 // k = 2^(-2 C B^2): four exp2 per entry and column (two anchors at rows 7 and
 // 8, one ratio each way, k) instead of sixteen, each sweep running from the
 // middle outwards.  An anchor far in the tail (e < -100) while the column
-// still reaches 2^-100 falls back to exp2 per pixel (narrow Gaussians, sub-
-// pixel scale); columns that never reach 2^-100 are skipped (< 1e-30).
+// still reaches 2^-60 falls back to exp2 per pixel (narrow Gaussians); columns
+// that never reach 2^VG_TOMO_SKIP = 2^-60 of the peak are skipped.
 // Thread t owns column t & 15 for list entries = t >> 4 (mod 8); the eight
 // partial columns are summed in a fixed order at the end.
 __global__ void __launch_bounds__(NT) k_tomo_fwd_rec(const GRec* __restrict__ rec,
@@ -742,7 +749,7 @@ __global__ void __launch_bounds__(NT) k_tomo_fwd_rec(const GRec* __restrict__ re
       const float ys = B != 0.f ? fminf(fmaxf(__fdividef(-A, B), 0.f), (float)(TILE - 1)) : 0.f;
       const float zs = fmaf(B, ys, A);
       const float emax = -C_HALF_LOG2E * fmaf(zs, zs, q11);
-      if (!(emax > -100.f)) continue;  // < 2^-100 everywhere in this column
+      if (!(emax > VG_TOMO_SKIP)) continue;  // below 2^VG_TOMO_SKIP of the peak everywhere here
       const float z7 = fmaf(B, 7.f, A), z8 = fmaf(B, 8.f, A);
       const float e7 = -C_HALF_LOG2E * fmaf(z7, z7, q11);
       const float e8 = -C_HALF_LOG2E * fmaf(z8, z8, q11);
