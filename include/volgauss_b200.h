@@ -212,6 +212,12 @@ int vg_tomo_backward(vg_context* ctx, const float* d_image, vg_grads* grads, voi
 int vg_tomo_backward_l2(vg_context* ctx, const float* image, const float* target,
                         double* loss_sum, vg_grads* grads, void* stream);
 
+/* Move the VG_DEFER accumulators of `src` (same scene, same device) into `dst`
+ * (src is left empty), so one vg_finalize_grads on dst covers the views of
+ * both contexts: one parameter-chain pass per step instead of one per
+ * context.  Ordered on `stream`. */
+int vg_merge_deferred(vg_context* dst, vg_context* src, void* stream);
+
 /* Write the geometry gradients accumulated by VG_DEFER backward calls
  * (analytic_param_chain, grad.py:242-259) into grads (overwrite when
  * grads->accumulate == VG_OVERWRITE, else add) and reset the accumulator. */

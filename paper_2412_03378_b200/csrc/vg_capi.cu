@@ -643,6 +643,34 @@ static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
   return VG_OK;
 }
 
+int vg_merge_deferred(vg_context* dst, vg_context* src, void* stream) {
+  if (!dst || !src) return fail(VG_EINVAL, "vg_merge_deferred: NULL context");
+  if (dst == src) return VG_OK;
+  if (!dst->prepared || !src->prepared) return fail(VG_EINVAL, "vg_merge_deferred: no scene on a context");
+  if (dst->scene.n != src->scene.n || (dst->scene.sh == nullptr) != (src->scene.sh == nullptr))
+    return fail(VG_EINVAL, "vg_merge_deferred: contexts hold different scenes");
+  if (dst->device != src->device) return fail(VG_EINVAL, "vg_merge_deferred: contexts on different devices");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = dst->scene.n;
+  if (n <= 0) return VG_OK;
+  VG_CUDA(cudaSetDevice(dst->device));
+  if (src->lacc.p && dst->lacc.p) launch_merge_acc(12 * n, (float*)dst->lacc.p, (float*)src->lacc.p, st);
+  if (src->cacc.p && dst->cacc.p) launch_merge_acc(3 * n, (float*)dst->cacc.p, (float*)src->cacc.p, st);
+  if (dst->scene.sh && src->sh_views > 0) {
+    const int v0 = dst->sh_views, v1 = src->sh_views;
+    VG_TRY(grow_keep(dst->dcol, sizeof(float) * 3 * (size_t)n * (size_t)(v0 + v1), st));
+    VG_TRY(grow_keep(dst->centers, sizeof(double) * 3 * (size_t)(v0 + v1), st));
+    VG_CUDA(cudaMemcpyAsync((float*)dst->dcol.p + (size_t)v0 * 3 * (size_t)n, src->dcol.p,
+                            sizeof(float) * 3 * (size_t)n * (size_t)v1, cudaMemcpyDeviceToDevice, st));
+    VG_CUDA(cudaMemcpyAsync((double*)dst->centers.p + 3 * (size_t)v0, src->centers.p,
+                            sizeof(double) * 3 * (size_t)v1, cudaMemcpyDeviceToDevice, st));
+    dst->sh_views = v0 + v1;
+    src->sh_views = 0;
+  }
+  VG_LAUNCHED(dst, 2);
+  return cudaGetLastError() == cudaSuccess ? VG_OK : fail(VG_ECUDA, "vg_merge_deferred: launch failed");
+}
+
 int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   if (!c || !g) return fail(VG_EINVAL, "vg_finalize_grads: NULL argument");
   if (!c->prepared) return fail(VG_EINVAL, "vg_finalize_grads: no scene on this context");

@@ -467,6 +467,37 @@ void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const f
   k_view_accumulate<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, c);
 }
 
+// dst += src, src = 0 (merging the deferred accumulators of two contexts)
+__global__ void __launch_bounds__(256) k_merge_acc(int64_t n4, float4* __restrict__ dst,
+                                                   float4* __restrict__ src) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 a = src[i];
+  float4 b = dst[i];
+  b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
+  dst[i] = b;
+  src[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void k_merge_acc_tail(int64_t n, float* __restrict__ dst, float* __restrict__ src) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dst[i] += src[i];
+  src[i] = 0.f;
+}
+
+void launch_merge_acc(int64_t n, float* dst, float* src, cudaStream_t st) {
+  if (n <= 0) return;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  const int64_t n4 = aligned ? n / 4 : 0;
+  if (n4)
+    k_merge_acc<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(n4, reinterpret_cast<float4*>(dst),
+                                                             reinterpret_cast<float4*>(src));
+  const int64_t rest = n - 4 * n4;
+  if (rest)
+    k_merge_acc_tail<<<(unsigned)((rest + 255) / 256), 256, 0, st>>>(rest, dst + 4 * n4, src + 4 * n4);
+}
+
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const float* dcol, const double* centers, int sh_views,
                            const vg_grads& g, bool splat, cudaStream_t st) {

@@ -106,6 +106,7 @@ void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const f
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,
                             bool splat, cudaStream_t st);
 // returns the number of kernels launched; SH scenes fold the sh_views slabs of dcol
+void launch_merge_acc(int64_t n, float* dst, float* src, cudaStream_t st);
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,
                            const float* dcol, const double* centers, int sh_views,
                            const vg_grads& g, bool splat, cudaStream_t st);

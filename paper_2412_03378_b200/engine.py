@@ -128,6 +128,12 @@ class Engine:
             return out / color.numel()
         return out
 
+    def merge_deferred(self, other):
+        """Move `other`'s deferred (VG_DEFER) accumulators into this engine's,
+        so that one finalize covers both (same scene, same device)."""
+        _lib.check(self.lib.vg_merge_deferred(self.ctx.handle, other.ctx.handle, self.stream()),
+                   "vg_merge_deferred")
+
     def finalize(self, grads, accumulate=True):
         """Write the geometry gradients of all VG_DEFER backward calls since
         the last finalize into `grads` (added unless accumulate=False)."""

@@ -184,8 +184,15 @@ class ViewShardedStep:
             self.torch.cuda.current_stream(self.eng.device).wait_stream(self.blend2)
 
     def _finish(self):
-        for i in sorted(getattr(self, "_used", ())):
-            self.engines[i].finalize(self.grads, accumulate=True)
+        used = sorted(getattr(self, "_used", ()))
+        if not used:
+            return
+        # one parameter-chain pass per step: the other contexts' deferred
+        # accumulators are merged into the first one (in context order)
+        first = self.engines[used[0]]
+        for i in used[1:]:
+            first.merge_deferred(self.engines[i])
+        first.finalize(self.grads, accumulate=True)
 
     def __call__(self, dscene=None, targets=None, ready=None, grads=None, loss=None):
         """Run the step.  `ready` optionally maps view -> CUDA event that the
