@@ -212,6 +212,12 @@ int vg_tomo_backward(vg_context* ctx, const float* d_image, vg_grads* grads, voi
 int vg_tomo_backward_l2(vg_context* ctx, const float* image, const float* target,
                         double* loss_sum, vg_grads* grads, void* stream);
 
+/* Copy `bytes` between device memory and pinned host memory (a mapped
+ * pointer) with `ctas` CTAs of a streaming kernel (evict-first cache hints:
+ * the transfer does not flush the L2 working set of concurrent kernels).
+ * Either pointer may be device or mapped host memory. */
+int vg_copy_streaming(void* dst, const void* src, size_t bytes, int32_t ctas, void* stream);
+
 /* Move the VG_DEFER accumulators of `src` (same scene, same device) into `dst`
  * (src is left empty), so one vg_finalize_grads on dst covers the views of
  * both contexts: one parameter-chain pass per step instead of one per

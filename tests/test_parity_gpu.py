@@ -725,3 +725,33 @@ def test_tomography_split_lists_pinhole():
     for f in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_kappas"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
         check_field(getattr(a, f), getattr(rg, f), f"split tomo {f}")
+
+
+def test_host_fed_step_kernel_download():
+    """HostFedStep with the streaming-kernel gradient download (vg_copy_streaming)
+    delivers the same bytes as the copy-engine download."""
+    import torch
+    from paper_2412_03378_b200 import configs
+    from paper_2412_03378_b200.engine import Engine
+    from paper_2412_03378_b200.multiview import HostFedStep, ViewShardedStep
+    cfg = configs.large(n=2000, width=96, height=64, n_views=3)
+    s = cfg.scene
+    eng = Engine(deterministic=True)
+    ds = eng.upload(s)
+    targets = {v: torch.from_numpy(cfg.target(v, (64, 96, 3))).cuda() for v in range(3)}
+    step = ViewShardedStep(eng, ds, cfg.cameras, targets)
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(s, k))).float().pin_memory()
+            for k in ("means", "scales", "rotations", "thetas", "colors")}
+    if s.sh is not None:
+        host["sh"] = torch.from_numpy(np.ascontiguousarray(s.sh)).float().pin_memory()
+    htgt = {v: t.cpu().pin_memory() for v, t in targets.items()}
+    out = []
+    for ctas in (0, 8):
+        fed = HostFedStep(step, host, htgt, lookahead=True, download_ctas=ctas)
+        for _ in range(3):
+            fed.step()
+        fed.drain()
+        torch.cuda.synchronize()
+        out.append((fed.grads_host.numpy().copy(), float(fed.loss_host)))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]

@@ -90,7 +90,9 @@ def main():
     print("device step        %.2f ms" % timed(lambda: runner(ds, targets)))
     for name, kw in [("fed lookahead", {}), ("fed no downloads", dict(down=False)),
                      ("fed no uploads", dict(scene=False, tgt=False)),
-                     ("fed no copies", dict(scene=False, tgt=False, down=False))]:
+                     ("fed no copies", dict(scene=False, tgt=False, down=False)),
+                     ("fed kernel dl 8", dict(download_ctas=8)),
+                     ("fed kernel dl 4", dict(download_ctas=4))]:
         fed = Variant(runner, host, htgt, lookahead=True, **kw)
 
         def f():
