@@ -755,3 +755,28 @@ def test_host_fed_step_kernel_download():
         out.append((fed.grads_host.numpy().copy(), float(fed.loss_host)))
     np.testing.assert_array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1]
+
+
+def test_integration_md_ctypes_stub_runs():
+    """The ctypes binding shown in INTEGRATION.md section 3 (what a maintainer
+    adds to the reference) runs as written and renders what render() renders."""
+    import os
+    import torch
+    from paper_2412_03378_b200 import configs
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = configs.tiny()
+    scene, cam = cfg.scene, cfg.cameras[0]
+    src = open(os.path.join(root, "INTEGRATION.md")).read()
+    body = src[src.index("## 3. The ctypes binding"):]
+    body = body[body.index("```python") + len("```python"):]
+    body = body[:body.index("```")]
+    cwd = os.getcwd()
+    os.chdir(root)
+    try:
+        ns = {"scene": scene, "cam": cam}
+        exec(compile(body, "INTEGRATION.md#3", "exec"), ns)
+    finally:
+        os.chdir(cwd)
+    torch.cuda.synchronize()
+    ref = vg().render(scene, cam)
+    np.testing.assert_allclose(ns["color"].cpu().numpy(), ref.color, rtol=1e-6, atol=1e-6)
