@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .camera import Camera, look_at
+from .camera import look_at
 
 SH_C = None  # filled lazily by sh_basis
 

@@ -13,7 +13,6 @@ import ctypes
 import math
 from dataclasses import dataclass
 
-import numpy as np
 
 from . import _lib
 from .raster import DeviceScene, _out, _stream
