@@ -108,7 +108,11 @@ typedef struct {
  *   VG_DEFER      multi-view accumulation: colour/SH gradients, d_background
  *                 and visible are added now, the per-Gaussian geometry chain
  *                 (means/scales/rotations/thetas/kappas) is summed over views
- *                 inside the context and written by vg_finalize_grads. */
+ *                 inside the context and written by vg_finalize_grads.  With
+ *                 vg_options.deterministic, d_background and the fused-L2 loss
+ *                 are also summed inside the context (in view order) and added
+ *                 by vg_finalize_grads, so deferred views on different
+ *                 contexts may run concurrently and stay bitwise reproducible. */
 #define VG_OVERWRITE 0
 #define VG_ADD 1
 #define VG_DEFER 2

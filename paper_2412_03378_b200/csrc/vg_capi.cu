@@ -64,6 +64,11 @@ struct vg_context {
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf tpart;                         // tomography forward: per-split partial images
   Buf det_pref, det_vcnt, det_vscan, det_vis4;  // deterministic mode: compact pair-major slots
+  // deterministic VG_DEFER: d_background (3 floats) and loss (double at +16 B)
+  // partials summed per context in view order, added by vg_finalize_grads
+  Buf det_sums;
+  double* defer_loss = nullptr;
+  float* defer_bg = nullptr;
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
   int vm_words = 0;
   bool vmask_valid = false;
@@ -118,7 +123,7 @@ static int fence_mode(const vg_context* c) {
     m = e ? atoi(e) : -1;
   }
   if (m >= 0) return m;
-  return c->opt.deterministic && c->n_tiles >= FENCE_MIN_TILES ? 3 : 0;
+  return 0;
 }
 
 struct ProfScope {
@@ -218,7 +223,7 @@ void vg_destroy(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan, &c->det_vis4};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan, &c->det_vis4, &c->det_sums};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -667,6 +672,16 @@ int vg_merge_deferred(vg_context* dst, vg_context* src, void* stream) {
     dst->sh_views = v0 + v1;
     src->sh_views = 0;
   }
+  if (src->det_sums.p && (src->defer_bg || src->defer_loss)) {
+    if (!dst->det_sums.p) VG_TRY(ensure(dst->det_sums, 64, st, true));
+    launch_det_flush((float*)src->det_sums.p, (double*)((char*)src->det_sums.p + 16),
+                     src->defer_bg ? (float*)dst->det_sums.p : nullptr,
+                     src->defer_loss ? (double*)((char*)dst->det_sums.p + 16) : nullptr, st);
+    if (src->defer_bg) dst->defer_bg = src->defer_bg;
+    if (src->defer_loss) dst->defer_loss = src->defer_loss;
+    src->defer_bg = nullptr;
+    src->defer_loss = nullptr;
+  }
   VG_LAUNCHED(dst, 2);
   return cudaGetLastError() == cudaSuccess ? VG_OK : fail(VG_ECUDA, "vg_merge_deferred: launch failed");
 }
@@ -678,6 +693,14 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   gg.accumulate = g->accumulate == VG_OVERWRITE ? VG_OVERWRITE : VG_ADD;
   cudaStream_t st = (cudaStream_t)stream;
   if (c->scene.n > 0) VG_TRY(run_param_chain(c, gg, st));
+  if (c->det_sums.p && (c->defer_bg || c->defer_loss)) {
+    // the deterministic mode's deferred d_background / loss sums
+    launch_det_flush((float*)c->det_sums.p, (double*)((char*)c->det_sums.p + 16), c->defer_bg,
+                     c->defer_loss, st);
+    VG_LAUNCHED(c, 1);
+    c->defer_bg = nullptr;
+    c->defer_loss = nullptr;
+  }
   return VG_OK;
 }
 
@@ -717,6 +740,27 @@ static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cud
   part = (float*)c->det_part.p;
   bg = (float*)c->det_bg.p;
   loss = (double*)c->det_loss.p;
+  return VG_OK;
+}
+
+// Deterministic mode: where the per-view tile-order d_background / loss sums
+// go.  Deferred backward calls add them into the context's own sums (summed in
+// view order; vg_merge_deferred / vg_finalize_grads add the contexts in a
+// fixed order), so the views of different contexts may run concurrently.
+static int det_targets(vg_context* c, const vg_grads* g, double* loss_sum, float*& bg,
+                       double*& loss, cudaStream_t st) {
+  bg = g->d_background;
+  loss = loss_sum;
+  if (g->accumulate != VG_DEFER) return VG_OK;
+  if (!c->det_sums.p) VG_TRY(ensure(c->det_sums, 64, st, true));
+  if (bg) {
+    c->defer_bg = bg;
+    bg = (float*)c->det_sums.p;
+  }
+  if (loss) {
+    c->defer_loss = loss;
+    loss = (double*)((char*)c->det_sums.p + 16);
+  }
   return VG_OK;
 }
 
@@ -763,11 +807,14 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     }
     VG_LAUNCHED(c, 1);
     if (det) {
+      float* bg_out;
+      double* loss_out;
+      VG_TRY(det_targets(c, g, loss_sum, bg_out, loss_out, st));
       VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
                          (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                          (float*)c->acc.p, c->n_tiles, (const float*)c->det_bg.p,
-                         target ? (const double*)c->det_loss.p : nullptr, g->d_background,
-                         loss_sum, st, io.det_pbase, io.det_vis4));
+                         target ? (const double*)c->det_loss.p : nullptr, bg_out,
+                         loss_out, st, io.det_pbase, io.det_vis4));
       VG_LAUNCHED(c, 2);
     }
     VG_TRY(finish_view(c, g, st));
@@ -859,10 +906,15 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
   VG_LAUNCHED(c, 1);
   if (det) {
     // tile loss partials exist only with the fused L2 (target); no d_background in tomography
+    float* bg_out;
+    double* loss_out;
+    vg_grads gn = *g;
+    gn.d_background = nullptr;
+    VG_TRY(det_targets(c, &gn, loss_sum, bg_out, loss_out, st));
     VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
                        (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                        (float*)c->acc.p, c->n_tiles, dbg, target ? dloss : nullptr, nullptr,
-                       loss_sum, st));
+                       loss_out, st));
     VG_LAUNCHED(c, 2);
   }
   VG_TRY(finish_view(c, g, st));

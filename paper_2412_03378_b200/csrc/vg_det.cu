@@ -130,6 +130,20 @@ __global__ void __launch_bounds__(256) k_det_tiles(int n_tiles, const float* __r
   }
 }
 
+// out += the deferred sums (when out is given); the sums are cleared
+__global__ void k_det_flush(float* __restrict__ bg, double* __restrict__ loss, float* __restrict__ bg_out,
+                            double* __restrict__ loss_out) {
+  if (threadIdx.x != 0) return;
+  if (bg_out) { bg_out[0] += bg[0]; bg_out[1] += bg[1]; bg_out[2] += bg[2]; }
+  if (loss_out) *loss_out += *loss;
+  bg[0] = bg[1] = bg[2] = 0.f;
+  *loss = 0.0;
+}
+
+void launch_det_flush(float* bg, double* loss, float* bg_out, double* loss_out, cudaStream_t st) {
+  k_det_flush<<<1, 32, 0, st>>>(bg, loss, bg_out, loss_out);
+}
+
 size_t det_pairs_scratch_bytes(int64_t pairs) { return scan_u32_scratch_bytes(pairs) + 16; }
 
 cudaError_t det_pairs(const uint32_t* vm, int vm_words, int64_t pairs, uint8_t* vis4, uint32_t* cnt_tmp,

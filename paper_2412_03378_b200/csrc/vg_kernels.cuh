@@ -71,6 +71,8 @@ cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, cons
 cudaError_t det_pairs(const uint32_t* vm, int vm_words, int64_t pairs, uint8_t* vis4, uint32_t* cnt_tmp,
                       uint32_t* pbase, void* scratch, cudaStream_t st);
 size_t det_pairs_scratch_bytes(int64_t pairs);
+// deterministic VG_DEFER: out += (bg[3], loss); the sums are cleared
+void launch_det_flush(float* bg, double* loss, float* bg_out, double* loss_out, cudaStream_t st);
 // sort_by="gamma" re-sort of every tile list (vg_gamma.cu)
 size_t gamma_scratch_bytes(int64_t pairs);
 void launch_gamma_sort(int n_tiles, const uint2* ranges, uint32_t* vals, const double* gm,

@@ -102,11 +102,12 @@ class ViewShardedStep:
         # overlap: a tile CTA whose warps finish at different depths (early
         # termination) or a short grid's tail no longer idles SMs.  Measured
         # (3 contexts): config 4 49.6 -> 34.5 ms/step, config 2 -5 %, config 5
-        # -2.3 %, config 3 -0.4 %.  Not with deterministic sums, whose per-view
-        # tile-order partials must be added in view order (VG_DUAL_BLEND=0: off).
+        # -2.3 %, config 3 -0.4 %.  Deterministic contexts defer their per-view
+        # d_background / loss sums per context (summed in view order, contexts
+        # added in a fixed order), so they overlap too (VG_DUAL_BLEND=0: off).
         self.blend2 = (torch.cuda.Stream(device=dev)
-                       if self.side is not None and not engine.deterministic
-                       and os.environ.get("VG_DUAL_BLEND", "1") != "0" else None)
+                       if self.side is not None and os.environ.get("VG_DUAL_BLEND", "1") != "0"
+                       else None)
 
     def _blend_stream(self, j):
         """Blend stream of the j-th view of the step: alternating when dual."""
