@@ -104,26 +104,22 @@ static cudaEvent_t pool_event(vg_context* c) {
   return c->pool[c->pool_used++];
 }
 
-// Bracket a launch with events when profiling is on.  Outside profiling, the
-// launches of large views of a deterministic context are still bracketed by
-// timing events ("fences").  Measured on B200 with the blends of consecutive
-// views serialised on one stream (what the deterministic multi-view step
-// does): bracketing both the side-stream binning and the main-stream blend
-// launches this way cut config 3 from 149.0 to 139.8 ms per step -- it keeps
-// the binning kernels from co-running with the blends in a way that slowed
-// the blends more than it hid.  With the two alternating blend streams of the
-// atomic step they cost 0.5-5 % instead, and small views never gain, so they
-// are off there.  VG_FENCE overrides: bit 0 = binning launches, bit 1 = blend
-// launches, bit 2 = timing-free events (no gain).
-constexpr int FENCE_MIN_TILES = 4096;
-static int fence_mode(const vg_context* c) {
+// Bracket a launch with events when profiling is on.  VG_FENCE brackets
+// launches with timing events outside profiling too ("fences"): with the
+// blends of consecutive views serialised on one stream, bracketing both the
+// side-stream binning and the blend launches cut config 3 from 149.0 to 139.8
+// ms per step (it kept the binning kernels from co-running with the blends in a
+// way that slowed the blends more than it hid); with the two alternating blend
+// streams of the multi-view step they cost 0.5-5 %, so they are off by
+// default.  Bits: 0 = binning launches, 1 = blend launches, 2 = timing-free
+// events (no gain).
+static int fence_mode(const vg_context*) {
   static int m = -2;
   if (m == -2) {
     const char* e = getenv("VG_FENCE");
-    m = e ? atoi(e) : -1;
+    m = e ? atoi(e) : 0;
   }
-  if (m >= 0) return m;
-  return 0;
+  return m;
 }
 
 struct ProfScope {
