@@ -216,6 +216,13 @@ int vg_tomo_backward(vg_context* ctx, const float* d_image, vg_grads* grads, voi
 int vg_tomo_backward_l2(vg_context* ctx, const float* image, const float* target,
                         double* loss_sum, vg_grads* grads, void* stream);
 
+/* tomo.voxelize (tomo.py:345-389): the mixture density sum_i kappa_i
+ * exp(-q_i/2) at the cell centres of a shape[0] x shape[1] x shape[2] grid over
+ * [bbox_min, bbox_max] (C order, float64, device `out`), each primitive culled
+ * to a box of 5 largest standard deviations and q <= 25 like the reference. */
+int vg_voxelize(const vg_scene* scene, const double* bbox_min, const double* bbox_max,
+                const int32_t* shape, double* out, void* stream);
+
 /* Copy `bytes` between device memory and pinned host memory (a mapped
  * pointer) with `ctas` CTAs of a streaming kernel (evict-first cache hints:
  * the transfer does not flush the L2 working set of concurrent kernels).

@@ -92,6 +92,8 @@ EXPORTS = {
     "vg_visible_pairs": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "vg_merge_deferred": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vg_copy_streaming": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p]),
+    "vg_voxelize": (C.c_int, [C.POINTER(VgScene), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                              C.POINTER(C.c_int32), C.c_void_p, C.c_void_p]),
     "vg_tomo_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vg_tomo_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(VgGrads), C.c_void_p]),
     "vg_tomo_backward_l2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
