@@ -11,7 +11,8 @@ L2 TrainConfig with 16 initial primitives and 24 iterations (no densify
 before iteration 24), seed 0.  Stored: the projections and cameras, the loss
 of every iteration, the final scene, its voxel grid at resolution 20, the
 psnr_3d / ssim_3d against the phantom grid, and a separate voxelize case
-(anisotropic rotated primitives, anisotropic resolution, box partly outside).
+(anisotropic rotated primitives, anisotropic resolution, box partly outside),
+and a density grid written by tomo.save_density_grid (io_grid.raw / .txt).
 """
 
 from __future__ import annotations
@@ -63,6 +64,13 @@ def main():
     out.update(vox_means=vs.means, vox_scales=vs.scales, vox_rotations=vs.rotations,
                vox_thetas=vs.thetas, vox_bmin=bmin, vox_bmax=bmax, vox_values=vg.values)
     np.savez_compressed(os.path.join(HERE, "recon.npz"), **out)
+    # density grid I/O (tomo.save_density_grid): a 5x6x7 grid with negative and
+    # awkward values and an asymmetric box -> io_grid.raw / io_grid.txt
+    gv = rng.normal(size=(5, 6, 7)) / 3.0
+    tomo.save_density_grid(os.path.join(HERE, "io_grid"),
+                           tomo.DensityGrid(values=gv, bbox_min=np.array([-1.0, -0.5, -2.0 / 3.0]),
+                                            bbox_max=np.array([1.25, 0.1, 0.7])))
+    np.save(os.path.join(HERE, "io_grid_values.npy"), gv)
     print(f"recon.npz: losses {rep['losses'][0]:.4g} -> {rep['losses'][-1]:.4g}, "
           f"psnr_3d {rep['psnr_3d']:.3f}, ssim_3d {rep['ssim_3d']:.4f}, vox max {vg.values.max():.4g}")
 

@@ -59,3 +59,23 @@ def test_format_errors_name_line_and_field(tmp_path):
         sceneio.load_scene(bad)
     with pytest.raises(ValueError):
         sceneio.write_pfm(tmp_path / "x.pfm", np.zeros((2, 2, 2)))
+
+
+def test_density_grid_files_match_reference(tmp_path):
+    """save_density_grid writes the reference's bytes (tests/golden/io_grid.*,
+    written by tomo.save_density_grid); load_density_grid reads them back."""
+    from paper_2412_03378_b200 import sceneio
+    from paper_2412_03378_b200.tomo import DensityGrid
+    gold = os.path.join(G, "io_grid")
+    values = np.load(os.path.join(G, "io_grid_values.npy"))
+    g = sceneio.load_density_grid(gold)
+    assert g.values.shape == (5, 6, 7)
+    assert np.array_equal(g.values, values.astype(np.float32).astype(np.float64))
+    base = str(tmp_path / "grid")
+    sceneio.save_density_grid(base, DensityGrid(values, g.bbox_min, g.bbox_max))
+    for ext in (".raw", ".txt"):
+        assert open(base + ext, "rb").read() == open(gold + ext, "rb").read(), ext
+    with open(base + ".txt", "w") as f:
+        f.write("something else\n")
+    with pytest.raises(ValueError):
+        sceneio.load_density_grid(base)
