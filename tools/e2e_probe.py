@@ -72,7 +72,7 @@ class Variant(HostFedStep):
 
 
 def main():
-    cfg = load_config("large", None)
+    cfg = load_config(sys.argv[1] if len(sys.argv) > 1 else "large", None)
     dev = torch.device("cuda", 0)
     eng = Engine(0)
     ds = eng.upload(cfg.scene)
@@ -92,7 +92,8 @@ def main():
                      ("fed no uploads", dict(scene=False, tgt=False)),
                      ("fed no copies", dict(scene=False, tgt=False, down=False)),
                      ("fed kernel dl 8", dict(download_ctas=8)),
-                     ("fed kernel dl 4", dict(download_ctas=4))]:
+                     ("fed kernel dl 4", dict(download_ctas=4)),
+                     ("fed kernel dl 2", dict(download_ctas=2))]:
         fed = Variant(runner, host, htgt, lookahead=True, **kw)
 
         def f():
