@@ -135,7 +135,8 @@ def medium(seed=2, n=100_000, size=800, n_views=8):
 
 
 def sh_basis(dirs):
-    """Real spherical-harmonic basis up to degree 3 for unit dirs (K,3) -> (K,16).
+    """Real spherical-harmonic basis up to degree 3 for unit dirs (K,3) -> (K,16)
+    (numpy arrays or torch tensors).
     Band 0 is the constant 1 so the DC coefficient is the view-independent RGB;
     bands 1-3 use the standard real-SH normalisation constants."""
     x, y, z = dirs[:, 0], dirs[:, 1], dirs[:, 2]
@@ -145,12 +146,15 @@ def sh_basis(dirs):
     c3 = (-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
           0.3731763325901154, -0.4570457994644658, 1.445305721320277, -0.5900435899266435)
     xx, yy, zz = x * x, y * y, z * z
-    cols = [np.ones_like(x),
+    cols = [x * 0 + 1,
             -c1 * y, c1 * z, -c1 * x,
             c2[0] * x * y, c2[1] * y * z, c2[2] * (2 * zz - xx - yy), c2[3] * x * z, c2[4] * (xx - yy),
             c3[0] * y * (3 * xx - yy), c3[1] * x * y * z, c3[2] * y * (4 * zz - xx - yy),
             c3[3] * z * (2 * zz - 3 * xx - 3 * yy), c3[4] * x * (4 * zz - xx - yy),
             c3[5] * z * (xx - yy), c3[6] * x * (xx - 3 * yy)]
+    if not isinstance(dirs, np.ndarray):  # torch tensors (autograd in the tests)
+        import torch
+        return torch.stack(cols, dim=1)
     return np.stack(cols, axis=1)
 
 

@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         }
         float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
         if (CUT) {
-          const bool c0 = om0 > p.omcut, c1 = om1 > p.omcut;
+          // cut iff alpha_raw < alpha_cut, decided on e itself (E2 = e log2 e
+          // has full float32 relative precision; exp(-e) ~ 0.996 there would
+          // quantise alpha to 1.5e-5 relative), or inactive (floor 1)
+          const bool c0 = lo(e.E2) < p.e2cut || fl0 == 1.f, c1 = hi(e.E2) < p.e2cut || fl1 == 1.f;
           om0 = c0 ? 1.f : om0;
           om1 = c1 ? 1.f : om1;
           if (COUNTS) {
@@ -413,8 +416,8 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
   // cut: skipped below alpha_cut (raster.py:363-365) or inactive
   float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
   float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-  const bool cut0 = CUT ? om0 > p.omcut : !act0;
-  const bool cut1 = CUT ? om1 > p.omcut : !act1;
+  const bool cut0 = !act0 || (CUT && lo(e.E2) < p.e2cut);
+  const bool cut1 = !act1 || (CUT && hi(e.E2) < p.e2cut);
   om0 = cut0 ? 1.f : om0;
   om1 = cut1 ? 1.f : om1;
   const F2 om = f2(om0, om1);
@@ -472,8 +475,8 @@ __device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
   float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
   float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-  const bool cut0 = CUT ? om0 > p.omcut : !act0;
-  const bool cut1 = CUT ? om1 > p.omcut : !act1;
+  const bool cut0 = !act0 || (CUT && lo(e.E2) < p.e2cut);
+  const bool cut1 = !act1 || (CUT && hi(e.E2) < p.e2cut);
   om0 = cut0 ? 1.f : om0;
   om1 = cut1 ? 1.f : om1;
   const F2 om = f2(om0, om1);

@@ -502,6 +502,8 @@ static BlendParams blend_params(const vg_context* c) {
   p.clamp = (float)c->opt.alpha_clamp;
   p.cc = (float)(1.0 - c->opt.alpha_clamp);
   p.omcut = (float)(1.0 - c->opt.alpha_cut);
+  // alpha_raw = 1 - exp(-e) < cut  <=>  e log2(e) < -log1p(-cut) log2(e)
+  p.e2cut = (float)(-log1p(-c->opt.alpha_cut) * 1.4426950408889634);
   p.ecut = c->opt.alpha_cut > 0 ? (float)(-log1p(-c->opt.alpha_cut) * (1.0 - 1e-3)) : 0.f;
   for (int i = 0; i < 3; ++i) p.bg[i] = (float)c->scene.background[i];
   return p;

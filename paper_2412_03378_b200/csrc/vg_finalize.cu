@@ -298,20 +298,49 @@ __global__ void __launch_bounds__(128) k_finalize_splat(FinalIn in, vg_grads g) 
 #undef VG_PUT
 }
 
-// SH pull-back of the step's views: d_sh[i][l][ch] (+)= sum_v b_l(d_v) dRGB_v[ch]
-// with d_v = normalize(mean_i - centre_v) and the real SH basis of
-// vg_common.cuh (DC band basis = 1).  One thread per Gaussian, 48 register
+// SH pull-back of the step's views, with d_v = (mean_i - centre_v) / |.| and
+// the real SH basis of vg_common.cuh (DC band basis = 1):
+//   d_sh[i][l][ch] (+)= sum_v b_l(d_v) dRGB_v[ch]
+//   d_means[i]     +=  sum_v (I - d_v d_v^T) / |mean_i - centre_v|
+//                          * sum_l grad b_l(d_v) (sum_ch sh[i][l][ch] dRGB_v[ch])
+// (the colour's dependence on the view direction; RGB = sum_l b_l sh_l is
+// linear, unclamped, as in preprocess).  One thread per Gaussian, 48 register
 // accumulators, the per-view slabs read coalesced.
+__device__ __forceinline__ void sh_basis_vjp(const float x, const float y, const float z,
+                                             const float (&g)[16], float (&o)[3]) {
+  const float c1 = 0.4886025119029199f, C4 = 1.0925484305920792f, C6 = 0.31539156525252005f,
+              C8 = 0.5462742152960396f, C9 = -0.5900435899266435f, C10 = 2.890611442640554f,
+              C11 = -0.4570457994644658f, C12 = 0.3731763325901154f, C13 = -0.4570457994644658f,
+              C14 = 1.445305721320277f, C15 = -0.5900435899266435f;
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  // d b_l / d(x, y, z) for the polynomial basis, contracted with g_l
+  o[0] = -c1 * g[3] + C4 * y * g[4] - 2.f * C6 * x * g[6] - C4 * z * g[7] + 2.f * C8 * x * g[8] +
+         6.f * C9 * xy * g[9] + C10 * yz * g[10] - 2.f * C11 * xy * g[11] - 6.f * C12 * xz * g[12] +
+         C13 * (4.f * zz - 3.f * xx - yy) * g[13] + 2.f * C14 * xz * g[14] +
+         3.f * C15 * (xx - yy) * g[15];
+  o[1] = -c1 * g[1] + C4 * x * g[4] - C4 * z * g[5] - 2.f * C6 * y * g[6] - 2.f * C8 * y * g[8] +
+         3.f * C9 * (xx - yy) * g[9] + C10 * xz * g[10] + C11 * (4.f * zz - xx - 3.f * yy) * g[11] -
+         6.f * C12 * yz * g[12] - 2.f * C13 * xy * g[13] - 2.f * C14 * yz * g[14] -
+         6.f * C15 * xy * g[15];
+  o[2] = c1 * g[2] - C4 * y * g[5] + 4.f * C6 * z * g[6] - C4 * x * g[7] + C10 * xy * g[10] +
+         8.f * C11 * yz * g[11] + C12 * (6.f * zz - 3.f * xx - 3.f * yy) * g[12] +
+         8.f * C13 * xz * g[13] + C14 * (xx - yy) * g[14];
+}
+
 __global__ void __launch_bounds__(128) k_sh_pull(int64_t n, const float* __restrict__ means,
+                                                 const float* __restrict__ sh,
                                                  const float* __restrict__ dcol,
                                                  const double* __restrict__ centers, int nviews,
-                                                 float* __restrict__ d_sh, int add) {
+                                                 float* __restrict__ d_sh, float* __restrict__ d_means,
+                                                 int add) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float acc[48];
 #pragma unroll
   for (int k = 0; k < 48; ++k) acc[k] = 0.f;
+  float dm[3] = {0.f, 0.f, 0.f};
   const double m[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+  const float4* sh4 = reinterpret_cast<const float4*>(sh + 48 * i);
   bool any = false;
   for (int v = 0; v < nviews; ++v) {
     const float* sl = dcol + (size_t)v * 3 * n;
@@ -329,8 +358,35 @@ __global__ void __launch_bounds__(128) k_sh_pull(int64_t n, const float* __restr
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) acc[3 * l + ch] = fmaf(bl, dc[ch], acc[3 * l + ch]);
     }
+    if (d_means) {
+      // g_l = sum_ch sh[l][ch] dRGB[ch] (the coefficients re-read from L1/L2)
+      float g[16];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        const float4 c = __ldg(sh4 + k);
+        const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = 4 * k + e, l = idx / 3, ch = idx % 3;
+          g[l] = (ch == 0 ? 0.f : g[l]) + cv[e] * dc[ch];
+        }
+      }
+      const float x = (float)d[0], y = (float)d[1], z = (float)d[2];
+      float gd[3];
+      sh_basis_vjp(x, y, z, g, gd);
+      // through d = u / |u|: (I - d d^T) gd / |u|
+      const float r = gd[0] * x + gd[1] * y + gd[2] * z;
+      const float inv = (float)(1.0 / dn);
+      dm[0] += (gd[0] - r * x) * inv;
+      dm[1] += (gd[1] - r * y) * inv;
+      dm[2] += (gd[2] - r * z) * inv;
+    }
   }
-  if (!any && add) return;
+  if (any && d_means) {
+    // k_finalize_params has already written (or added) this step's geometric term
+    for (int k = 0; k < 3; ++k) d_means[3 * i + k] += dm[k];
+  }
+  if (!d_sh || (!any && add)) return;
   float4* o = reinterpret_cast<float4*>(d_sh + 48 * i);
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
@@ -512,9 +568,9 @@ int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cac
   const unsigned blocks = (unsigned)((n + 31) / 32);
   const int add = g.accumulate != 0;
   if (s.sh) {
-    if (g.d_sh)
-      k_sh_pull<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, s.means, dcol, centers, sh_views,
-                                                            g.d_sh, add);
+    if (g.d_sh || g.d_means)
+      k_sh_pull<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, s.means, s.sh, dcol, centers, sh_views,
+                                                            g.d_sh, g.d_means, add);
     // d_colors (dL/d evaluated RGB) is not tracked separately for SH scenes
     if (g.d_colors && !add) cudaMemsetAsync(g.d_colors, 0, sizeof(float) * 3 * (size_t)n, st);
   } else {

@@ -15,7 +15,8 @@ struct BlendParams {
   float cut;       // alpha_cut
   float clamp;     // alpha_clamp
   float cc;        // 1 - alpha_clamp (rounded once from float64): clamped transmittance factor
-  float omcut;     // 1 - alpha_cut: factor above which an entry is cut
+  float omcut;     // 1 - alpha_cut
+  float e2cut;     // -log1p(-alpha_cut) log2(e): entries with e log2(e) below it are cut
   float ecut;      // culling threshold on e: -log1p(-alpha_cut) * (1 - 1e-3)
   float bg[3];
 };

@@ -215,6 +215,20 @@ class Prep:
         _lib.check(_lib.load().vg_pair_count(self.ctx.handle, ctypes.byref(out)), "vg_pair_count")
         return int(out.value)
 
+    def n_active(self):
+        """Per-pixel count of active entries (transmittance in front >=
+        early_stop, raster.py:384-385) of the last render on this prep, as an
+        int32 (H, W) array on the host (diagnostic: the parity tests use it to
+        find early-stop decisions float32 took differently from float64)."""
+        torch = _lib._require_cuda()
+        if self.fwd is None:
+            raise ValueError("n_active: render on this prep first")
+        H, W = int(self.camera.height), int(self.camera.width)
+        out = torch.empty((H, W), dtype=torch.int32, device=self.dscene.device)
+        _lib.check(_lib.load().vg_n_active(self.ctx.handle, _lib.ptr(out), _stream(self.dscene.device)),
+                   "vg_n_active")
+        return out.cpu().numpy()
+
     def tile_lists_device(self):
         """(prims int32[P], offsets int32[n_tiles+1]) on the device."""
         torch = _lib._require_cuda()

@@ -10,12 +10,15 @@ flip.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
 from conftest import RASTER_CASES, TOMO_CASES, case_flags, cuda_available, golden_lists, load_case
 from oracle import volgauss_oracle as O
-from parity import check_field, check_image, knife_edge_mask
+from parity import (check_field, check_image, device_knife_mask, image_mismatch, knife_cap,
+                    near_threshold)
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
@@ -59,14 +62,18 @@ def test_tile_lists_bit_exact(name):
 def test_render_matches_reference(name):
     scene, cam, d = load_case(name)
     flags = case_flags(d)
-    out = vg().render(scene, cam, **flags)
+    dprep = vg().prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    out = vg().render(scene, cam, **flags, prep=dprep)
     prep = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"])
-    check_image(out.color, d["color"], prep, scene, flags, f"{name} color")
-    check_image(out.final_transmittance, d["final_transmittance"], prep, scene, flags, f"{name} T")
+    # pixels whose float32 counts differ from the oracle's (each explained by
+    # an entry at a threshold), plus alpha-clamp edges
+    knife = device_knife_mask(prep, scene, flags, out.n_contrib, dprep.n_active())
+    check_image(out.color, d["color"], prep, scene, flags, f"{name} color", knife=knife)
+    check_image(out.final_transmittance, d["final_transmittance"], prep, scene, flags, f"{name} T",
+                knife=knife)
     if flags["alpha_cut"] > 0:
         diff = np.argwhere(out.n_contrib != d["n_contrib"])
-        from parity import pixel_is_flip
-        bad = [tuple(x) for x in diff if not pixel_is_flip(prep, scene, x[0], x[1], flags)]
+        bad = [tuple(x) for x in diff if not knife[x[0], x[1]]]
         assert not bad, f"n_contrib differs at {bad[:5]}"
 
 
@@ -79,16 +86,18 @@ def test_backward_matches_reference(name):
     dc, dt = d["d_color"], d.get("d_transmittance")
     ref = {f: d[f"bwd_{f}"] for f in GRAD_FIELDS + ["d_background", "visible"]}
     prep = O.prepare(scene, cam, alpha_cut=flags["alpha_cut"])
-    knife = knife_edge_mask(prep, scene, flags)
+    dprep = vg().prepare(scene, cam, alpha_cut=flags["alpha_cut"])
+    out = vg().render(scene, cam, **flags, prep=dprep)
+    knife = device_knife_mask(prep, scene, flags, out.n_contrib, dprep.n_active())
+    knife_cap(int(knife.sum()), knife.size, f"{name} backward")
     if knife.any():
         # float32/float64 threshold flips: take those pixels out of the
         # upstream gradient on both sides (oracle is pinned to the reference)
-        assert knife.mean() < 0.02, f"{knife.sum()} knife-edge pixels"
         dc = dc * ~knife[..., None]
         dt = None if dt is None else dt * ~knife
         g64 = O.backward(scene, cam, dc, d_transmittance=dt, prep=prep, **flags)
         ref = {f: getattr(g64, f) for f in ref}
-    g = vg().backward(scene, cam, dc, d_transmittance=dt, **flags)
+    g = vg().backward(scene, cam, dc, d_transmittance=dt, **flags, prep=dprep)
     for f in GRAD_FIELDS:
         check_field(getattr(g, f), ref[f], f"{name} {f}")
     check_field(g.d_background, ref["d_background"], f"{name} d_background")
@@ -214,7 +223,7 @@ def _tile_mask(oprep, tiles, H, W):
     return mask
 
 
-def _full_size_check(scene, cam, n_random=5, seed=5):
+def _full_size_check(scene, cam, n_random=5, seed=5, n_busy=3):
     """Every tile list bit-exact against the oracle's float32-key order; a
     seeded sample of tiles (incl. the three heaviest) rendered and
     back-propagated against the float64 oracle (d_color vanishes outside the
@@ -227,16 +236,18 @@ def _full_size_check(scene, cam, n_random=5, seed=5):
     assert np.array_equal(prims.cpu().numpy(), oprep.pair_prim)
     out = vg().render(scene, cam, prep=prep)
     rng = np.random.default_rng(seed)
-    busy = np.argsort(np.diff(oprep.tile_start))[-3:]
+    busy = np.argsort(np.diff(oprep.tile_start))[len(oprep.tile_start) - 1 - n_busy:]
     tiles = sorted(set(busy.tolist()) |
                    set(rng.integers(0, oprep.tiles_x * oprep.tiles_y, n_random).tolist()))
     ref = O.render(scene, cam, prep=oprep, tiles=tiles)
     mask = _tile_mask(oprep, tiles, cam.height, cam.width)
+    npx = int(mask.sum())
+    knife = device_knife_mask(oprep, scene, {}, out.n_contrib, prep.n_active(), tiles=tiles)
     check_image(np.where(mask[..., None], out.color, 0), np.where(mask[..., None], ref.color, 0),
-                oprep, scene, {}, "color")
+                oprep, scene, {}, "color", n_px=npx, knife=knife)
     check_image(np.where(mask, out.final_transmittance, 0), np.where(mask, ref.final_transmittance, 0),
-                oprep, scene, {}, "T")
-    knife = knife_edge_mask(oprep, scene, {}, tiles=tiles)
+                oprep, scene, {}, "T", n_px=npx, knife=knife)
+    knife_cap(int(knife.sum()), npx, "sampled tiles backward")
     dc = rng.uniform(-1, 1, (cam.height, cam.width, 3)) * (mask & ~knife)[..., None]
     g = vg().backward(scene, cam, dc, prep=prep)
     rg = O.backward(scene, cam, dc, prep=oprep, tiles=tiles)
@@ -249,6 +260,19 @@ def test_full_size_large_view_tiles_and_sampled_pixels():
     from paper_2412_03378_b200 import configs
     cfg = configs.large()
     _full_size_check(_f64_scene(cfg.scene), cfg.cameras[0])
+
+
+def test_full_size_medium_all_views():
+    """Config 2 (BASELINE configs[1]: N=100k, 8 views at 800x800) at full
+    size: every view's tile lists bit-exact, and per view the heaviest tile
+    plus two seeded tiles rendered and back-propagated against the float64
+    oracle (raster.py:410-439, grad.py:107-259)."""
+    from paper_2412_03378_b200 import configs
+    cfg = configs.medium()
+    assert len(cfg.cameras) == 8 and cfg.cameras[0].width == 800
+    scene = _f64_scene(cfg.scene)
+    for v, cam in enumerate(cfg.cameras):
+        _full_size_check(scene, cam, n_random=2, seed=100 + v, n_busy=1)
 
 
 def test_full_size_opaque_view():
@@ -328,11 +352,12 @@ def test_degenerate_inputs():
     ref_lists = O.prepare(scene, cam, key_dtype=np.float32).lists()
     for gl, rl in zip(prep.grid.tiles, ref_lists):
         assert np.array_equal(gl, rl)
-    out = vg().render(scene, cam)
+    out = vg().render(scene, cam, prep=prep)
     ref = O.render(scene, cam)
     oprep = O.prepare(scene, cam)
-    check_image(out.color, ref.color, oprep, scene, {}, "degenerate color")
-    knife = knife_edge_mask(oprep, scene, {})
+    knife = device_knife_mask(oprep, scene, {}, out.n_contrib, prep.n_active())
+    check_image(out.color, ref.color, oprep, scene, {}, "degenerate color", knife=knife)
+    knife_cap(int(knife.sum()), knife.size, "degenerate backward")
     dc = rng.uniform(-1, 1, (34, 50, 3)) * ~knife[..., None]
     g = vg().backward(scene, cam, dc)
     rg = O.backward(scene, cam, dc)
@@ -359,6 +384,21 @@ def test_depth_sort_and_span_lists(name):
     prims, offs = prep.tile_lists_device()
     assert np.array_equal(offs.cpu().numpy(), oprep.tile_start)
     assert np.array_equal(prims.cpu().numpy(), oprep.pair_prim)
+
+
+def sh_direction_grad(means, centre, sh, d_rgb):
+    """d/dmeans of sum(d_rgb * RGB(dir)), RGB = sum_l b_l(dir) sh_l, dir =
+    (mean - centre)/|.|: float64 torch autograd through configs.sh_basis's
+    polynomial (an independent check of k_sh_pull's hand-written VJP)."""
+    import torch
+    from paper_2412_03378_b200 import configs
+    m = torch.tensor(means, dtype=torch.float64, requires_grad=True)
+    d = m - torch.tensor(np.asarray(centre, dtype=np.float64))
+    d = d / d.norm(dim=1, keepdim=True)
+    b = configs.sh_basis(d)
+    rgb = torch.einsum("nl,nlc->nc", b, torch.tensor(sh, dtype=torch.float64))
+    (rgb * torch.tensor(d_rgb, dtype=torch.float64)).sum().backward()
+    return m.grad.numpy()
 
 
 def test_sh_colour_and_deferred_pullback():
@@ -403,6 +443,8 @@ def test_sh_colour_and_deferred_pullback():
         for f in tot:
             tot[f] = tot[f] + getattr(rg, f)
         d_sh += basis[:, :, None] * rg.d_colors[:, None, :]
+        # the colour's view-direction dependence (torch float64 autograd)
+        tot["d_means"] = tot["d_means"] + sh_direction_grad(means, c, sh, rg.d_colors)
     assert abs(loss - ref_loss) <= 1e-4 * ref_loss
     for f in tot:
         check_field(getattr(g, f), tot[f], f"sh step {f}")
@@ -437,15 +479,15 @@ def test_gamma_sort_lists_render_and_backward(name):
         assert np.all(np.abs(ga - gb) <= 1e-12 * np.abs(gb) + 1e-300), f"tile {t}"
     out = vg().render(scene, cam, sort_by="gamma", prep=prep)
     gprep = O.prepare(scene, cam, sort_by="gamma")
-    check_image(out.color, g[f"{name}_color"], gprep, scene, {}, f"{name} gamma color")
+    knife = device_knife_mask(gprep, scene, {}, out.n_contrib, prep.n_active())
+    check_image(out.color, g[f"{name}_color"], gprep, scene, {}, f"{name} gamma color", knife=knife)
     fields = ("d_means", "d_scales", "d_rotations", "d_thetas", "d_colors", "d_background")
     dc = g[f"{name}_dcolor"]
     ref = {f: g[f"{name}_{f}"] for f in fields}
-    knife = knife_edge_mask(gprep, scene, {})
+    knife_cap(int(knife.sum()), knife.size, f"{name} gamma backward")
     if knife.any():
         # threshold flips out of the upstream gradient on both sides (the
         # oracle is pinned to the reference's gamma render/backward)
-        assert knife.mean() < 0.02
         dc = dc * ~knife[..., None]
         g64 = O.backward(scene, cam, dc, prep=gprep)
         ref = {f: getattr(g64, f) for f in fields}
@@ -535,28 +577,21 @@ def test_splat_mode_matches_reference(name):
     sprep = SO.prepare(scene, cam, key_dtype=np.float32)
     assert np.array_equal(prims.cpu().numpy(), sprep.pair_prim)
     out = vg().render(scene, cam, mode="splat", prep=prep)
-    err = np.abs(out.color - g[f"{name}_color"])
-    assert np.mean(err > 1e-4 + 1e-3 * np.abs(g[f"{name}_color"])) < 2e-3, err.max()
-    np.testing.assert_allclose(out.color, g[f"{name}_color"], rtol=1e-3, atol=5e-3)
-    # knife edges of the splat alphas
-    knife = np.zeros((cam.height, cam.width), dtype=bool)
-    for t in range(sprep.tiles_x * sprep.tiles_y):
-        ids = sprep.tile_ids(t)
-        if ids.size == 0:
-            continue
-        from oracle.volgauss_oracle import _tile_box, front_to_back
-        r0, c0, h, w, rows, cols = _tile_box(sprep, t)
-        raw, alpha, _, _, _, _, _ = SO._alphas(sprep, scene, ids, rows, cols, O.ALPHA_CUT, O.ALPHA_CLAMP)
-        before, active, _, _, n_act = front_to_back(alpha, O.EARLY_STOP_T)
-        near = (np.abs(raw - O.ALPHA_CUT) < 1e-6) | (np.abs(raw - O.ALPHA_CLAMP) < 1e-6) | \
-            (np.abs(before - O.EARLY_STOP_T) < 1e-6 * O.EARLY_STOP_T + 1e-9)
-        rel = np.arange(len(ids))[:, None] <= n_act[None, :]
-        knife[r0:r0 + h, c0:c0 + w] = (near & rel).any(axis=0).reshape(h, w)
+    # pixels whose float32 counts differ from the oracle's (each explained by
+    # an entry at a threshold), plus alpha-clamp edges, with the splat alphas
+    def splat_alphas(p, ids, rows, cols):
+        raw, alpha, _, _, _, _, _ = SO._alphas(p, scene, ids, rows, cols, O.ALPHA_CUT, O.ALPHA_CLAMP)
+        return raw, alpha
+    knife = device_knife_mask(sprep, scene, {}, out.n_contrib, prep.n_active(), alphas=splat_alphas)
+    knife_cap(int(knife.sum()), knife.size, f"{name} splat")
+    # the image contract (1e-4 + 1e-3 |ref|) everywhere but on knife edges
+    bad = image_mismatch(out.color, g[f"{name}_color"])
+    assert not (bad & ~knife).any(), (np.argwhere(bad & ~knife)[:5],
+                                      float(np.abs(out.color - g[f"{name}_color"]).max()))
     dc = g[f"{name}_dcolor"]
     fields = ("d_means", "d_scales", "d_rotations", "d_colors", "d_background", "d_splat_opacities")
     ref = {f: g[f"{name}_{f}"] for f in fields}
     if knife.any():
-        assert knife.mean() < 0.02
         dc = dc * ~knife[..., None]
         r64 = SO.backward(scene, cam, dc, prep=sprep)
         ref = {f: getattr(r64, f) for f in fields}
@@ -896,3 +931,221 @@ def test_pipelined_step_is_stable_across_steps():
             else:
                 torch.testing.assert_close(g, grads[0], rtol=1e-4, atol=1e-7)
         assert max(losses) - min(losses) <= 1e-12 * abs(losses[0])
+
+
+def test_sh_gradient_matches_float64_central_differences():
+    """SH-3 colour gradients against float64 central differences (the FD
+    semantics of grad.fd_check, grad.py:420-467): L = sum_px w . colour over
+    two views of the float64 oracle fed each view's SH-evaluated RGB, the
+    analytic gradient from the device backward of w (d_means includes the
+    colour's view-direction term, d_sh the per-view basis pull-back).  Smooth
+    flags (no cut, no early stop, no clamp) so the differences see no
+    threshold."""
+    from types import SimpleNamespace
+    from paper_2412_03378_b200 import configs
+    rng = np.random.default_rng(31)
+    n = 24
+    f32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+    means = f32(rng.uniform(-0.5, 0.5, (n, 3)))
+    scales = f32(np.exp(rng.uniform(np.log(0.08), np.log(0.22), (n, 3))))
+    q = rng.normal(size=(n, 4))
+    rots = f32(q / np.linalg.norm(q, axis=1, keepdims=True))
+    thetas = f32(rng.uniform(0.2, 0.8, n))
+    sh = rng.normal(0.0, 0.3, (n, 16, 3))
+    sh[:, 0, :] = rng.uniform(0.2, 0.9, (n, 3))
+    sh = f32(sh)
+    flags = dict(alpha_cut=0.0, early_stop=None, alpha_clamp=1.0)
+    cams = [vg().look_at([0.4, 0.6, -3.0], [0, 0, 0], width=40, height=32, fov_x_deg=50.0),
+            vg().look_at([-2.5, 0.3, -1.8], [0, 0, 0], width=40, height=32, fov_x_deg=50.0)]
+    ws = [rng.uniform(-1, 1, (32, 40, 3)) for _ in cams]
+
+    def oracle_loss(m, coef):
+        tot = 0.0
+        for cam, w in zip(cams, ws):
+            d = m - O.cam_center(cam)
+            d /= np.linalg.norm(d, axis=1, keepdims=True)
+            rgb = np.einsum("nl,nlc->nc", configs.sh_basis(d), coef)
+            sc = SimpleNamespace(means=m, scales=scales, rotations=rots, thetas=thetas, colors=rgb,
+                                 background=np.zeros(3))
+            tot += float(np.sum(O.render(sc, cam, **flags).color * w))
+        return tot
+
+    dev_scene = SimpleNamespace(means=means, scales=scales, rotations=rots, thetas=thetas, sh=sh,
+                                colors=None, background=np.zeros(3))
+    gm = np.zeros((n, 3))
+    gsh = np.zeros((n, 16, 3))
+    for cam, w in zip(cams, ws):
+        g = vg().backward(dev_scene, cam, w, **flags)
+        gm += np.asarray(g.d_means)
+        gsh += np.asarray(g.d_sh).reshape(n, 16, 3)
+    eps = 1e-5
+    picks = rng.choice(n, 6, replace=False)
+    for i in picks:
+        for k in range(3):
+            a, b = means.copy(), means.copy()
+            a[i, k] += eps
+            b[i, k] -= eps
+            fd = (oracle_loss(a, sh) - oracle_loss(b, sh)) / (2 * eps)
+            assert abs(gm[i, k] - fd) <= 1e-4 * np.abs(gm).max() + 1e-3 * abs(fd), (i, k, gm[i, k], fd)
+        for l, ch in ((0, 0), (3, 1), (8, 2), (15, 0)):
+            a, b = sh.copy(), sh.copy()
+            a[i, l, ch] += eps
+            b[i, l, ch] -= eps
+            fd = (oracle_loss(means, a) - oracle_loss(means, b)) / (2 * eps)
+            assert abs(gsh[i, l, ch] - fd) <= 1e-4 * np.abs(gsh).max() + 1e-3 * abs(fd), (i, l, ch, gsh[i, l, ch], fd)
+    # the direction term matters at this scale: without it d_means misses
+    # sum_v (I - d d^T)/|u| grad_b . (sh dRGB)
+    assert np.abs(gm).max() > 0
+
+
+# --- config 3: the full 64-view step against the per-view oracle ------------
+
+_STEP64 = {}
+
+
+def _oracle_view_job(v):
+    """Worker (forked): view v of config 3 on the float64 oracle -- its
+    seeded tile, the knife-edge pixels there (the device's counts against
+    the oracle's), and the backward of the L2 residual against the seeded
+    tile target (knife pixels excluded), as sparse rows.  Runs in a child
+    process: numpy only."""
+    from types import SimpleNamespace
+    from paper_2412_03378_b200 import configs
+    s, cams, means, sh = _STEP64["scene"], _STEP64["cams"], _STEP64["means"], _STEP64["sh"]
+    t, dev_nc, dev_na = _STEP64["dev"][v]
+    cam = cams[v]
+    c = O.cam_center(cam)
+    d = means - c
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    basis = configs.sh_basis(d)
+    rgb = np.einsum("nl,nlc->nc", basis, sh)
+    scene = SimpleNamespace(means=means, scales=s.scales.astype(np.float64),
+                            rotations=s.rotations.astype(np.float64), thetas=s.thetas.astype(np.float64),
+                            colors=rgb, background=np.zeros(3))
+    prep = O.prepare(scene, cam, key_dtype=np.float32)
+    ref = O.render(scene, cam, prep=prep, tiles=[t])
+    ty, tx = divmod(t, prep.tiles_x)
+    r0, c0 = ty * 16, tx * 16
+    h, w = dev_nc.shape
+    full_nc = np.zeros((cam.height, cam.width), dtype=np.int64)
+    full_na = np.zeros((cam.height, cam.width), dtype=np.int64)
+    full_nc[r0:r0 + h, c0:c0 + w] = dev_nc
+    full_na[r0:r0 + h, c0:c0 + w] = dev_na
+    knife = device_knife_mask(prep, scene, {}, full_nc, full_na, tiles=[t])
+    rng = np.random.default_rng(1000 + v)
+    tgt = rng.uniform(0.0, 1.0, (h, w, 3))
+    keep = ~knife[r0:r0 + h, c0:c0 + w]
+    r = (ref.color[r0:r0 + h, c0:c0 + w] - tgt) * keep[..., None]
+    dc = np.zeros((cam.height, cam.width, 3))
+    dc[r0:r0 + h, c0:c0 + w] = 2.0 * r / (3.0 * cam.width * cam.height)
+    g = O.backward(scene, cam, dc, prep=prep, tiles=[t])
+    rows = np.flatnonzero(g.visible | np.any(g.d_colors != 0, axis=1))
+    out = {f: getattr(g, f)[rows] for f in ("d_means", "d_scales", "d_rotations", "d_thetas",
+                                           "d_kappas", "d_colors")}
+    out["d_means"] = out["d_means"] + _sh_dir_rows(means[rows], c, sh[rows], out["d_colors"])
+    out["d_sh"] = basis[rows][:, :, None] * out["d_colors"][:, None, :]
+    return dict(v=v, tile=t, knife=int((~keep).sum()), tgt=tgt, keep=keep, rows=rows, g=out,
+                d_background=g.d_background, loss=float(np.sum(r * r)))
+
+
+def _sh_dir_rows(means, centre, sh, d_rgb):
+    """Numpy restatement of sh_direction_grad for the worker (no torch in a
+    forked child): central differences of the float64 basis along each axis
+    are not needed -- the basis is polynomial, so use its exact derivative by
+    complex-step differentiation."""
+    from paper_2412_03378_b200 import configs
+    out = np.zeros_like(means)
+    for k in range(3):
+        m = means.astype(np.complex128)
+        m[:, k] += 1e-30j
+        d = m - centre
+        d = d / np.sqrt(np.sum(d * d, axis=1, keepdims=True))
+        rgb = np.einsum("nl,nlc->nc", configs.sh_basis(d), sh)
+        out[:, k] = np.sum(rgb.imag * d_rgb, axis=1) / 1e-30
+    return out
+
+
+def _engine_lists(eng):
+    """Tile offsets of an engine's last prepare (host int64)."""
+    import torch
+    from paper_2412_03378_b200 import _lib
+    nt = ((eng.cam.width + 15) // 16) * ((eng.cam.height + 15) // 16)
+    P = eng.pair_count()
+    prims = torch.empty(max(P, 1), dtype=torch.int32, device=eng.device)
+    offs = torch.empty(nt + 1, dtype=torch.int32, device=eng.device)
+    _lib.check(eng.lib.vg_tile_lists(eng.ctx.handle, _lib.ptr(prims), _lib.ptr(offs), eng.stream()),
+               "vg_tile_lists")
+    return prims[:P].cpu().numpy(), offs.cpu().numpy().astype(np.int64)
+
+
+def test_full_size_large_64_view_step_equals_sum_of_oracle_views():
+    """BASELINE config 3 at full size: N=1M SH-3 Gaussians, all 64 views at
+    1920x1080 through the production multi-view step (pipelined contexts,
+    dual blend streams, fused L2, deferred float64 parameter chain, SH
+    pull-back incl. the view-direction term).  Each view's target equals the
+    device's own render except on one seeded tile per view (seeded values;
+    knife-edge pixels keep the device colour), so the L2 gradient is zero
+    outside those 64 tiles and the step's flat gradient must equal the sum of
+    64 per-view float64 oracle backwards (raster.py:410-439, grad.py:107-259)
+    on those tiles."""
+    import multiprocessing as mp
+    import torch
+    from paper_2412_03378_b200 import configs
+    from paper_2412_03378_b200.engine import Engine
+    from paper_2412_03378_b200.multiview import ViewShardedStep
+    cfg = configs.large()
+    s = cfg.scene
+    _STEP64.update(scene=s, cams=cfg.cameras, means=s.means.astype(np.float64), sh=s.sh.astype(np.float64))
+    V = len(cfg.cameras)
+    assert V == 64
+    eng = Engine()
+    ds = eng.upload(s)
+    # the device forward of every view: its colour (the target outside the
+    # sampled tile) and its counts on one seeded tile of at least median
+    # list length
+    colors, dev = [], {}
+    for v, cam in enumerate(cfg.cameras):
+        eng.prepare(ds, cam)
+        color, _, ncon = eng.forward()
+        nact = eng.n_active()
+        _, offs = _engine_lists(eng)
+        lens = np.diff(offs)
+        cand = np.flatnonzero(lens >= np.median(lens[lens > 0]))
+        t = int(np.random.default_rng(1000 + v).choice(cand))
+        ty, tx = divmod(t, (cam.width + 15) // 16)
+        blk = (slice(ty * 16, min(ty * 16 + 16, cam.height)), slice(tx * 16, min(tx * 16 + 16, cam.width)))
+        dev[v] = (t, ncon[blk].cpu().numpy(), nact[blk].cpu().numpy())
+        colors.append(color.clone())
+    _STEP64["dev"] = dev
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(8, os.cpu_count() or 1)) as pool:
+        res = pool.map(_oracle_view_job, range(V))
+    targets = {}
+    for v, cam in enumerate(cfg.cameras):
+        tg = colors[v]
+        r = res[v]
+        ty, tx = divmod(r["tile"], (cam.width + 15) // 16)
+        h, w = r["tgt"].shape[:2]
+        blk = tg[ty * 16:ty * 16 + h, tx * 16:tx * 16 + w]
+        keep = torch.from_numpy(r["keep"]).cuda()[..., None]
+        blk.copy_(torch.where(keep, torch.from_numpy(r["tgt"]).float().cuda(), blk))
+        targets[v] = tg
+    step = ViewShardedStep(eng, ds, cfg.cameras, targets)
+    loss = float(step())
+    g = step.grads.to_scene_grads("analytic", torch_out=False)
+    n = len(s.means)
+    tot = {f: np.zeros((n,) + np.shape(res[0]["g"][f])[1:]) for f in res[0]["g"]}
+    bg = np.zeros(3)
+    ref_loss = 0.0
+    for r in res:
+        for f, a in r["g"].items():
+            np.add.at(tot[f], r["rows"], a)
+        bg += r["d_background"]
+        ref_loss += r["loss"]
+    knives = sum(r["knife"] for r in res)
+    knife_cap(knives, 256 * V, "64-view step")
+    assert abs(loss - ref_loss) <= 1e-4 * ref_loss
+    for f in ("d_means", "d_scales", "d_rotations", "d_thetas", "d_kappas"):
+        check_field(getattr(g, f), tot[f], f"64-view step {f}")
+    check_field(np.asarray(g.d_sh).reshape(n, 48), tot["d_sh"].reshape(n, 48), "64-view step d_sh")
+    check_field(g.d_background, bg, "64-view step d_background")
