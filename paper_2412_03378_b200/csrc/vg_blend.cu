@@ -42,7 +42,10 @@
 #define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
 #endif
 #ifndef VG_BWD_MINB
-#define VG_BWD_MINB 6   // <= 80 registers (shared memory also caps it at 6 CTAs)
+// 5: <= 96 registers.  With the cut decided on e (eval_pinhole2) the 80-register
+// budget of 6 CTAs spilled: config 3, 16 views, serial: 6 -> 19.26 ms,
+// 5 -> 18.01 ms, 4 -> 19.26 ms
+#define VG_BWD_MINB 5
 #endif
 #ifndef VG_BWD_PAIR
 // two visible entries per step: 1 = both replays, then both entries' gradient
@@ -159,7 +162,15 @@ struct Pair2 {
 
 // Pinhole rays, two pixels (same column lx, rows ly.x / ly.y).  The single
 // shared evaluation for forward and backward (identical rounding).
-__device__ __forceinline__ Pair2 eval_pinhole2(const SRec& s, float lx, F2 ly, F2 Lp) {
+// CUT: entries with alpha_raw < alpha_cut get the transmittance factor
+// ex = 1 exactly, so the callers need no separate cut test: om = max(ex,
+// floor) is 1 for cut and inactive entries alike, and every other factor is
+// exp(-e) < 1 in float32 (alpha_cut >= 6e-8).  The decision is taken on E2 = e log2(e),
+// which carries full float32 relative precision: testing exp(-e) ~ 0.996
+// against 1 - cut would quantise alpha to 1.5e-5 relative and flip ~0.3 %
+// of the pixels of a dense view against the float64 reference.
+template <bool CUT = false>
+__device__ __forceinline__ Pair2 eval_pinhole2(const SRec& s, float lx, F2 ly, F2 Lp, float e2cut = 0.f) {
   Pair2 o;
   o.q1 = fmaf(s.b.x, lx, s.a.x);
   const float t2 = fmaf(s.b.y, lx, s.a.y);
@@ -174,6 +185,7 @@ __device__ __forceinline__ Pair2 eval_pinhole2(const SRec& s, float lx, F2 ly, F
   o.G = mul2(o.rs, ex2_2(arg));
   o.E2 = mul2(f2s(s.b.w), o.G);
   o.ex = ex2_2(neg2(o.E2));
+  if (CUT) o.ex = sel2(lo(o.E2) < e2cut, hi(o.E2) < e2cut, f2s(1.f), o.ex);
   return o;
 }
 
@@ -263,19 +275,10 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
             na1 = a1 ? jb + k : na1;
           }
         }
-        float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
-        if (CUT) {
-          // cut iff alpha_raw < alpha_cut, decided on e itself (E2 = e log2 e
-          // has full float32 relative precision; exp(-e) ~ 0.996 there would
-          // quantise alpha to 1.5e-5 relative), or inactive (floor 1)
-          const bool c0 = lo(e.E2) < p.e2cut || fl0 == 1.f, c1 = hi(e.E2) < p.e2cut || fl1 == 1.f;
-          om0 = c0 ? 1.f : om0;
-          om1 = c1 ? 1.f : om1;
-          if (COUNTS) {
-            nc0 += c0 ? 0 : 1;
-            nc1 += c1 ? 0 : 1;
-          }
-        } else if (COUNTS) {
+        // cut entries carry the factor 1 (eval_pinhole2), inactive ones the
+        // floor 1: either way om = 1, no contribution, no count
+        const float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
+        if (COUNTS) {
           nc0 += om0 < 1.f;
           nc1 += om1 < 1.f;
         }
@@ -302,12 +305,12 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
         const SRec s = sm[k];
-        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
         if (bits) {
           const int kb = c + __ffs(bits) - 1;
           bits &= bits - 1;
           const SRec sb = sm[kb];
-          const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
+          const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
           composite(k, s, e);
           composite(kb, sb, eb);
         } else {
@@ -411,24 +414,22 @@ __device__ __forceinline__ void bwd_entry(const SRec& s, const Pair2& e, bool in
                                           F2& T, F2& P, int lane, const BwdIO& io, size_t pos,
                                           float* wb) {
   // active iff the replayed transmittance in front is >= stop (raster.py:384-385),
-  // bit-identical to the forward's; inactive entries get a floor of 1 (no change)
+  // bit-identical to the forward's; inactive entries get a floor of 1 (no
+  // change), cut ones (raster.py:363-365) the factor 1 from eval_pinhole2
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
-  // cut: skipped below alpha_cut (raster.py:363-365) or inactive
-  float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
-  float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-  const bool cut0 = !act0 || (CUT && lo(e.E2) < p.e2cut);
-  const bool cut1 = !act1 || (CUT && hi(e.E2) < p.e2cut);
-  om0 = cut0 ? 1.f : om0;
-  om1 = cut1 ? 1.f : om1;
+  const float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
+  const float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
   const F2 om = f2(om0, om1);
   const F2 contrib = mul2(sub2(f2s(1.f), om), T);
   const F2 Tn = mul2(T, om);
   const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
   P = fma2(dot, contrib, P);
   T = Tn;
-  // live: active, not cut, not clamped (alpha_raw < clamp <=> exp(-e) > 1 - clamp)
-  const bool live0 = !cut0 && lo(e.ex) > p.cc;
-  const bool live1 = !cut1 && hi(e.ex) > p.cc;
+  // live: active, not cut (CUT: om < 1), not clamped (alpha_raw < clamp <=>
+  // exp(-e) > 1 - clamp); without a cut an active alpha = 0 entry is live
+  // (theta = 0 still has a kappa gradient, grad.py:150-160)
+  const bool live0 = (CUT ? om0 < 1.f : act0) && lo(e.ex) > p.cc;
+  const bool live1 = (CUT ? om1 < 1.f : act1) && hi(e.ex) > p.cc;
   const bool vis = om0 < 1.f || om1 < 1.f;
   const bool any_live = __any_sync(FULL, live0 || live1);
   const bool any_vis = __any_sync(FULL, vis);
@@ -473,12 +474,8 @@ __device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool
                                              F2 dcg, F2 dcb, F2 tot, const BlendParams& p, F2& T,
                                              F2& P) {
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
-  float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
-  float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
-  const bool cut0 = !act0 || (CUT && lo(e.E2) < p.e2cut);
-  const bool cut1 = !act1 || (CUT && hi(e.E2) < p.e2cut);
-  om0 = cut0 ? 1.f : om0;
-  om1 = cut1 ? 1.f : om1;
+  const float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
+  const float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
   const F2 om = f2(om0, om1);
   Replay r;
   r.contrib = mul2(sub2(f2s(1.f), om), T);
@@ -486,8 +483,8 @@ __device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool
   const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
   P = fma2(dot, r.contrib, P);
   T = Tn;
-  const bool live0 = !cut0 && lo(e.ex) > p.cc;
-  const bool live1 = !cut1 && hi(e.ex) > p.cc;
+  const bool live0 = (CUT ? om0 < 1.f : act0) && lo(e.ex) > p.cc;
+  const bool live1 = (CUT ? om1 < 1.f : act1) && hi(e.ex) > p.cc;
   r.h = mul2(sel2(live0, live1, fma2(dot, Tn, sub2(P, tot)), f2s(0.f)), e.G);
   r.any_vis = __any_sync(FULL, om0 < 1.f || om1 < 1.f);
   r.flush = r.any_vis || __any_sync(FULL, live0 || live1);
@@ -625,12 +622,12 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
         const SRec s = sm[k];
-        const Pair2 e = eval_pinhole2(s, lx, ly, Lp);
+        const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
         if (bits) {
           const int kb = c + __ffs(bits) - 1;
           bits &= bits - 1;
           const SRec sb = sm[kb];
-          const Pair2 eb = eval_pinhole2(sb, lx, ly, Lp);
+          const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
 #if VG_BWD_PAIR
           const size_t ia = dslot(base + k, s, k);
           const size_t ib = dslot(base + kb, sb, kb);

@@ -501,8 +501,10 @@ static BlendParams blend_params(const vg_context* c) {
   p.cut = (float)c->opt.alpha_cut;
   p.clamp = (float)c->opt.alpha_clamp;
   p.cc = (float)(1.0 - c->opt.alpha_clamp);
-  p.omcut = (float)(1.0 - c->opt.alpha_cut);
-  // alpha_raw = 1 - exp(-e) < cut  <=>  e log2(e) < -log1p(-cut) log2(e)
+  // alpha_raw = 1 - exp(-e) < cut  <=>  e log2(e) < -log1p(-cut) log2(e):
+  // cut entries get the factor 1 (eval_pinhole2), every other factor is
+  // exp(-e) < 1 in float32 for cut >= 6e-8, so "cut" is om > nextafter(1, 0)
+  p.omcut = 0.99999994f;
   p.e2cut = (float)(-log1p(-c->opt.alpha_cut) * 1.4426950408889634);
   p.ecut = c->opt.alpha_cut > 0 ? (float)(-log1p(-c->opt.alpha_cut) * (1.0 - 1e-3)) : 0.f;
   for (int i = 0; i < 3; ++i) p.bg[i] = (float)c->scene.background[i];

@@ -15,7 +15,7 @@ struct BlendParams {
   float cut;       // alpha_cut
   float clamp;     // alpha_clamp
   float cc;        // 1 - alpha_clamp (rounded once from float64): clamped transmittance factor
-  float omcut;     // 1 - alpha_cut
+  float omcut;     // largest float below 1: a factor above it is a cut (or inactive) entry
   float e2cut;     // -log1p(-alpha_cut) log2(e): entries with e log2(e) below it are cut
   float ecut;      // culling threshold on e: -log1p(-alpha_cut) * (1 - 1e-3)
   float bg[3];
