@@ -3,6 +3,12 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config large]
                     [--impl ours|reference] [--views V] [--no-e2e] [--no-cpu]
 
+`--gpus N` (N > 1) outside torchrun re-runs itself as N ranks under
+torch.distributed.run (127.0.0.1); under torchrun the ranks come from
+RANK / LOCAL_RANK / WORLD_SIZE.  Each rank renders its share of the views
+and one NCCL group per step (vg_allreduce_grads through the C ABI) sums the
+gradients, ORs `visible` and sums the loss.
+
 Workload (default `--config large`, BASELINE.json configs[2], the config the
 north-star 1000x target is quoted on): N=1M Gaussians with SH-3 colour,
 64 cameras at 1920x1080.  One step = every view of the config rendered
@@ -14,9 +20,12 @@ Views are sharded round-robin over ranks, so total work is fixed ("strong").
 `value` is device-timed with CUDA events (inputs resident in HBM), max over
 ranks.  `e2e` runs the same step through the public engine API with the
 scene and targets copied from pinned host memory and the gradients + loss
-copied back inside the timed region.  `roofline` is for the dominant kernel
-(measured live with CUDA events on the launch stream); its denominator is
-the FP32 / MUFU throughput probed on this GPU at its live clock.
+copied back inside the timed region.  `roofline` is for the dominant kernel:
+its SURVEY 8(d) algorithmic FP32 / MUFU work (counted per step: evaluated
+and live pair-pixels x the canonical per-unit costs) over its time in an
+isolated serial pass (CUDA events on the launch stream), against the FP32 /
+MUFU throughput probed on this GPU at its live clock; `roofline.issue` keeps
+the issue-slot view (ncu warp instructions per unit).
 `cpu_baseline` is the float64 numpy oracle (a port of the reference path,
 oracle/) on a bounded, seeded sample of tiles of view 0, all host cores.
 `--impl reference` prints that CPU arm as the line itself.
@@ -151,13 +160,17 @@ def run_gpu(args):
 
     from paper_2412_03378_b200 import _lib
     from paper_2412_03378_b200.engine import Engine
-    from paper_2412_03378_b200.multiview import ViewShardedStep, shard
+    from paper_2412_03378_b200.multiview import NcclComm, ViewShardedStep, shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
+        # the step's gradient exchange: one NCCL group through the C ABI
+        # (vg_allreduce_grads) on the step's stream
+        comm = NcclComm(dev)
     cfg = load_config(args.config, args.views)
     tomo = cfg.tomography
     my_views = shard(len(cfg.cameras), ws, rank)
@@ -168,7 +181,7 @@ def run_gpu(args):
     tshape = (H, W) if tomo else (H, W, 3)
     targets = {v: torch.from_numpy(cfg.target(v, tshape)).to(dev) for v in my_views}
     runner = ViewShardedStep(eng, ds, cams, targets, world=ws, rank=rank, tomography=tomo,
-                             parallel=cfg.parallel, extent=cfg.extent)
+                             parallel=cfg.parallel, extent=cfg.extent, comm=comm)
     grads = runner.grads
     loss = runner.loss
 
@@ -203,23 +216,21 @@ def run_gpu(args):
     ms_total = e0.elapsed_time(e1)
     launches = sum(e.launches() for e in runner.engines) - l0
     clk = clocks.stop()
-    # per-kernel breakdown: a separate pass with per-launch events (vg_profile),
-    # outside the timed region; consecutive views' blends run on one stream
-    # here, so each launch's event interval is its own (in the timed steps
-    # they alternate over two streams and overlap)
-    blend2, runner.blend2 = runner.blend2, None
-    for e in runner.engines:
-        e.ctx.profile(True)
-    for _ in range(args.steps):
-        step(ds, targets, grads)
+    # per-kernel breakdown: a separate, fully serial pass (one context, one
+    # stream, no side-stream binning: VG_OVERLAP=0) with per-launch events
+    # (vg_profile), outside the timed region, so every launch's event interval
+    # is that kernel alone; in the timed steps binning and consecutive views'
+    # blends overlap, so these times sum to more than the step
+    serial = ViewShardedStep(eng, ds, cams, targets, world=ws, rank=rank, tomography=tomo,
+                             parallel=cfg.parallel, extent=cfg.extent, pipeline=False)
+    serial()
     torch.cuda.synchronize()
-    runner.blend2 = blend2
-    prof = {}
-    for e in runner.engines:
-        for k, (ms, cnt) in e.ctx.profile_read().items():
-            a, b = prof.get(k, (0.0, 0))
-            prof[k] = (a + ms, b + cnt)
-        e.ctx.profile(False)
+    eng.ctx.profile(True)
+    for _ in range(args.steps):
+        serial()
+    torch.cuda.synchronize()
+    prof = dict(eng.ctx.profile_read())
+    eng.ctx.profile(False)
     loss_val = float(loss) / (len(cams) * math.prod(tshape))
     if ws > 1:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -240,12 +251,17 @@ def run_gpu(args):
     if rank == 0:
         kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                    for k, v in prof.items() if v[1]}
+        kernels["_note"] = ("isolated: a serial pass (one context, one stream, VG_OVERLAP=0 equivalent) "
+                            "timed per launch with CUDA events; the timed steps overlap binning and "
+                            "consecutive views' blends, so these sum to more than ms_per_step")
         roof = build_roofline(prof, args.steps, eng, ds, cams, my_views, tomo, cfg,
                               fp32_peak, mufu_peak, args.config)
         result = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mpixels/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "collective": ("NCCL all-reduce of the flat gradient buffer + visible OR + loss, one group "
+                           "per step via vg_allreduce_grads") if ws > 1 else None,
             "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
             "config": {"workload": cfg.description,
                        "views_per_step": len(cams), "pixels_per_step": px_step,
@@ -299,60 +315,106 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
             "api": "multiview.HostFedStep(lookahead=True): every step uploads its scene + targets and downloads grads + loss, double-buffered and overlapped with compute (gradient buffers >= 64 MB by an 8-CTA streaming kernel); the timed region holds K uploads and K downloads"}
 
 
-def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak, cfg_name):
-    """Roofline of the dominant blend kernel from this run's CUDA-event times.
+# SURVEY 8(d) / BASELINE.md section 4: canonical FP32 instructions and MUFU ops
+# per unit of the blend kernels.  Render: per evaluated pair-pixel E (an entry
+# evaluated at a pixel: 64 per (entry, 8x8 warp block) pair the kernel walks)
+# plus extra FP32 per live pair-pixel L (sum of n_contrib).  Tomography: per
+# binned pair-pixel B (pairs x 256); the parallel-beam adjoint has no 8(d)
+# figure, the cone-beam one is used.
+COSTS = {"render_fwd": {"fp32_per_E": 21, "mufu_per_E": 3, "fp32_per_L": 5},
+         "render_bwd": {"fp32_per_E": 24, "mufu_per_E": 4, "fp32_per_L": 46},
+         "tomo_fwd": {"fp32_per_E": 9, "mufu_per_E": 1, "fp32_per_L": 0},
+         "tomo_bwd": {"fp32_per_E": 45, "mufu_per_E": 2, "fp32_per_L": 0}}
 
-    The blend kernels are neither HBM- nor tensor-core-bound (ncu: DRAM
-    throughput ~3%, no MMA); they are instruction-issue-bound (no single pipe
-    saturated), so the roofline is the SM issue rate, 148 SMs x 4 schedulers
-    x 1 warp-instruction / clock at the live clock.
-    Algorithmic units, counted in an untimed pass over this rank's views:
-    render -- V = visible (entry, 64-pixel warp block) pairs, what the
-    backward walks (one warp iteration each), plus A = active pair-pixels
-    and L = live pair-pixels; tomography -- the binned
-    (tile, Gaussian) pairs, one thread walking the tile's 256 pixels each.
-    achieved = (ncu warp instructions per unit of the profiled view of this
-    config, profiles/traffic.json) x units per step / the kernel's CUDA-event
-    time per step."""
+
+def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak, cfg_name):
+    """Roofline of the blend kernels (the dominant one first).
+
+    Algorithmic: the kernels are FP32-issue / SFU bound (no
+    tensor cores: a per-pixel exponential chain; ncu DRAM throughput ~3 %).
+    Work per step is counted in an untimed pass over this rank's views:
+    E = evaluated pair-pixels (64 x the (entry, warp block) pairs each kernel
+    walks: the forward's culled set from a counting forward, the backward's
+    forward-visible set), L = live pair-pixels (sum n_contrib), A = active
+    pair-pixels (sum n_active); tomography: B = 256 x binned pairs.  FP32 =
+    fp32_per_E E + fp32_per_L L, MUFU = mufu_per_E E (COSTS); the peaks are
+    probed on this GPU at its live clock (vg_probe_peaks: scalar FFMA lane
+    ops/s = 148 x 128 x f, MUFU ex2/s = 148 x 16 x f); t* = max(FP32 /
+    P_fp32, MUFU / P_mufu) and frac = t* / t, t the kernel's time per step
+    in the isolated (serial) pass.  `issue` keeps the issue-slot view (ncu
+    warp instructions per unit of the profiled view, profiles/traffic.json).
+    """
     import torch
     kinds = ("tomo_fwd", "tomo_bwd") if tomo else ("render_fwd", "render_bwd")
     dom = max(kinds, key=lambda k: prof.get(k, (0, 0))[0])
-    ms, cnt = prof.get(dom, (0.0, 0))
-    if not cnt:
+    if not prof.get(dom, (0, 0))[1]:
         return None
-    tr = load_traffic(cfg_name, dom) or {}
-    pv = tr.get("view", 0)
-    A = L = U = 0.0
+    tr_all = {k: load_traffic(cfg_name, k) or {} for k in kinds}
+    pv = tr_all[dom].get("view", 0)
+    A = L = 0.0
+    U = {"fwd": 0.0, "bwd": 0.0}
     U_prof = None
     for v in my_views if pv in my_views else list(my_views) + [pv]:
         if tomo:
             eng.prepare(ds, cams[v], tomo=True, parallel=cfg.parallel, extent=cfg.extent)
-            u = eng.pair_count()
+            uf = ub = float(eng.pair_count())
         else:
             eng.prepare(ds, cams[v])
             _, _, nc = eng.forward()
-            u = eng.visible_pairs()
+            ub = float(eng.visible_pairs())
+            na = eng.n_active()
+            a_v, l_v = float(na.double().sum()), float(nc.double().sum())
+            uf = float(eng.forward_stats()[0])
         if v == pv:
-            U_prof = u
+            U_prof = ub
         if v in my_views:
-            U += u
+            U["fwd"] += uf
+            U["bwd"] += ub
             if not tomo:
-                A += float(eng.n_active().double().sum())
-                L += float(nc.double().sum())
+                A += a_v
+                L += l_v
     torch.cuda.synchronize()
-    t = ms * 1e-3 / steps                       # seconds per step in this kernel
-    launch_s = t / max(cnt / steps, 1.0)        # average duration of one launch
-    unit = "binned pairs" if tomo else "visible pairs"
-    out = {"kernel": dom, "unit_of_work": unit, "units_per_step": U,
-           "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
-           "ns_per_unit": t / U * 1e9 if U else None,
+    px_per_unit = 256.0 if tomo else 64.0
+    clock_mhz = mufu_peak / (148 * 16) / 1e6 if mufu_peak else None
+    blend = {}
+    for k in kinds:
+        ms, cnt = prof.get(k, (0.0, 0))
+        if not cnt:
+            continue
+        t = ms * 1e-3 / steps
+        units = U["fwd" if k.endswith("fwd") else "bwd"]
+        E = px_per_unit * units
+        c = COSTS[k]
+        fp32 = c["fp32_per_E"] * E + c["fp32_per_L"] * (0.0 if tomo else L)
+        mufu = c["mufu_per_E"] * E
+        alg = {"kernel": k, "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
+               "unit": "binned pair-pixels B (256 x binned pairs)" if tomo else
+                       "evaluated pair-pixels E (64 x walked (entry, 8x8 block) pairs)",
+               "E_per_step": E, "L_per_step": None if tomo else L,
+               "fp32_per_E": c["fp32_per_E"], "fp32_per_L": c["fp32_per_L"], "mufu_per_E": c["mufu_per_E"],
+               "fp32_instr_per_step": fp32, "mufu_ops_per_step": mufu,
+               "p_fp32_per_s": fp32_peak, "p_mufu_per_s": mufu_peak, "sm_clock_mhz_probed": clock_mhz}
+        if fp32_peak and mufu_peak:
+            t_fp, t_mu = fp32 / fp32_peak, mufu / mufu_peak
+            t_star = max(t_fp, t_mu)
+            alg.update(t_fp32_ms=t_fp * 1e3, t_mufu_ms=t_mu * 1e3, t_star_ms=t_star * 1e3,
+                       bound="fp32" if t_fp >= t_mu else "mufu", frac=t_star / t)
+        blend[k] = alg
+    dalg = blend[dom]
+    tr = tr_all[dom]
+    ms, cnt = prof[dom]
+    t = ms * 1e-3 / steps
+    launch_s = t / max(cnt / steps, 1.0)
+    out = {"kernel": dom, "bound": dalg.get("bound"), "frac": dalg.get("frac"),
+           "achieved": (dalg["fp32_instr_per_step"] if dalg.get("bound") == "fp32" else dalg["mufu_ops_per_step"]) / t / 1e12
+           if dalg.get("bound") else None,
+           "peak": ((fp32_peak if dalg.get("bound") == "fp32" else mufu_peak) or 0) / 1e12,
+           "unit": "T FP32 lane-instr/s" if dalg.get("bound") == "fp32" else "T MUFU ops/s",
            "traffic": tr.get("bytes_per_launch"),
            "traffic_source": f"profiles/traffic.json[{cfg_name}] (ncu --set full, dram read + write per launch)",
-           "timing_note": "kernel time from a profiling pass with the blends of consecutive views on one "
-                          "stream (in the timed steps they alternate over two streams and overlap)"}
-    if not tomo:
-        out.update(visible_pair_pixels_per_step=64.0 * U, active_pair_pixels_per_step=A,
-                   live_pair_pixels_per_step=L)
+           "timing": "isolated serial pass (VG_OVERLAP=0 equivalent), CUDA events on the launch stream",
+           "algorithmic": dalg, "blend_kernels": blend,
+           "A_active_pair_pixels_per_step": None if tomo else A}
     if tr.get("bytes_per_launch"):
         hbm = measured_hbm_gbs()
         gbs = tr["bytes_per_launch"] / launch_s / 1e9
@@ -362,27 +424,14 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
         f_clk = mufu_peak / (148 * 16)          # live SM clock from the MUFU probe (16 ex2/clk/SM)
         issue_peak = 148 * 4 * f_clk
         ipu = tr["warp_instructions_per_launch"] / U_prof
-        ach = ipu * U / t
-        f_issue = ach / issue_peak
-        out.update(bound="issue", achieved=ach / 1e9, peak=issue_peak / 1e9,
-                   unit="G warp-instructions/s", frac=f_issue,
-                   warp_instructions_per_unit=ipu,
-                   peak_source="148 SMs x 4 issue/clk at the live clock (vg_probe_peaks MUFU loop / 16)",
-                   ncu_pipes_pct={k: tr.get(k) for k in ("issue_active_pct", "xu_pipe_pct", "fma_pipe_pct",
-                                                          "alu_pipe_pct", "lsu_pipe_pct", "occupancy_pct")})
-        # the busiest pipe: ncu's pipe / issue utilisation ratio scaled to the live issue rate
-        ia = tr.get("issue_active_pct") or 0.0
-        if ia > 0:
-            fr = {"issue": f_issue}
-            for name, key in (("fma pipe", "fma_pipe_pct"), ("xu (MUFU) pipe", "xu_pipe_pct"),
-                              ("alu pipe", "alu_pipe_pct")):
-                if tr.get(key) is not None:
-                    fr[name] = f_issue * tr[key] / ia
-            out["pipe_fracs"] = fr
-            top = max(fr, key=fr.get)
-            if top != "issue":
-                out.update(bound=top, frac=fr[top],
-                           frac_note=f"{top} utilisation = live issue fraction x ncu {top} / issue-active")
+        ach = ipu * U["fwd" if dom.endswith("fwd") else "bwd"] / t
+        out["issue"] = {"achieved": ach / 1e9, "peak": issue_peak / 1e9, "unit": "G warp-instructions/s",
+                        "frac": ach / issue_peak, "warp_instructions_per_unit": ipu,
+                        "unit_of_work": "binned pairs" if tomo else "visible (entry, 8x8 block) pairs",
+                        "peak_source": "148 SMs x 4 issue/clk at the live clock",
+                        "ncu_pipes_pct": {k: tr.get(k) for k in ("issue_active_pct", "xu_pipe_pct",
+                                                                  "fma_pipe_pct", "alu_pipe_pct",
+                                                                  "lsu_pipe_pct", "occupancy_pct")}}
     return out
 
 
@@ -457,7 +506,11 @@ def cpu_sample(cfg, n_tiles_target, seed=0, budget_s=25.0):
             "sample": (f"{len(used)} seeded-random 16x16 tiles ({done_px} px) of view 0 of "
                        f"{cfg.name}, fwd+bwd, float64 numpy oracle/ (port of raster/grad"
                        f"{'/tomo' if cfg.tomography else ''}.py); per-view prepare "
-                       f"{t_prep:.1f}s prorated by pixel fraction"),
+                       f"{t_prep:.1f}s prorated by pixel fraction"
+                       + ("; SH-3 colour replaced by its DC band (the reference has RGB colour only; "
+                          "the SH evaluation is < 0.1 % of the CPU work)" if getattr(s, "sh", None) is not None
+                          else "")),
+            "host_cpu": cpu_model(),
             "seconds": round(t_eff, 2)}
 
 
@@ -474,6 +527,17 @@ def _tile_mask(prep, tiles, H, W):
     return m
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return f"{line.split(':', 1)[1].strip()} ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"unknown ({os.cpu_count()} logical CPUs)"
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -487,20 +551,49 @@ def run_reference(args):
         if not warm:
             samples.append(r)
     val = statistics.mean(r["value"] for r in samples)
+    # NOT timed: the whole step would take hours on the CPU; this is the step's
+    # pixel count at the sampled rate
     ms_step = len(cfg.cameras) * cfg.cameras[0].height * cfg.cameras[0].width / (val * 1e6) * 1e3
     return {"metric": METRIC, "value": round(val, 6), "unit": "Mpixels/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 1),
+            "ms_per_step_extrapolated": True,
+            "ms_per_step_note": ("extrapolated: the step's pixels at the rate measured on the sampled tiles "
+                                 "(cpu_baseline.sample); a full config-3 step would take hours on the host"),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox, BASELINE.json config shapes/distributions)",
-            "impl": "reference",
+            "impl": "reference", "host_cpu": cpu_model(),
             "config": {"workload": cfg.description, "views_per_step": len(cfg.cameras)},
             "cpu_baseline": {k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": round(val, 6)},
             "e2e": {"value": round(val, 6), "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
+def launch_ranks(n):
+    """`--gpus N` (N > 1) outside torchrun: re-run this command as N ranks
+    under torch.distributed.run on this node (one process per GPU, NCCL);
+    rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA device(s) visible"}))
+            sys.exit(2)
+        launch_ranks(args.gpus)
+    ws, _, _ = dist_env()
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; running {ws} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         res = run_reference(args)
         if res is not None:

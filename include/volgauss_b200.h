@@ -349,6 +349,40 @@ int vg_raymarch(const vg_scene* scene, const vg_camera* cam, int32_t n_steps,
                 double support_sigmas, double t_min, double t_max, float* color, float* final_t,
                 void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU gradient exchange (SURVEY 8(b) vg_allreduce_grads, 8(e)).  The
+ * reference sums per-view gradients one view per iteration
+ * (optim.py:367-378); the view-sharded step renders each rank's views into
+ * one flat float32 gradient buffer, then one NCCL group sums it over the
+ * ranks.  NCCL is resolved at run time (the libnccl.so.2 already loaded in
+ * the process, else VG_NCCL_LIB, else the loader path), so this library has
+ * no link-time NCCL dependency.  Communicators are plain `ncclComm_t`
+ * handles passed as void*: one from vg_nccl_comm_init, or any the caller
+ * built with NCCL itself. */
+
+/* 1 if NCCL could be resolved in this process, else 0 (vg_last_error says why). */
+int vg_nccl_available(void);
+/* ncclGetUniqueId: 128 bytes for rank 0 to broadcast to the other ranks. */
+int vg_nccl_unique_id(void* out128);
+/* ncclCommInitRank on `device` (collective over the nranks processes). */
+int vg_nccl_comm_init(void** comm, int32_t nranks, const void* id128, int32_t rank, int32_t device);
+int vg_nccl_comm_destroy(void* comm);
+/* Stream-ordered, in place, in one NCCL group: flat[0..count) summed
+ * (float32), visible[0..n_visible) OR-ed (uint8 max; NULL/0 to skip), *loss
+ * summed (float64; NULL to skip).  Afterwards every rank holds the gradient
+ * of all views, equal to the sum of the per-view reference SceneGrads. */
+int vg_allreduce_grads(vg_context* ctx, void* nccl_comm, float* flat, int64_t count, uint8_t* visible,
+                       int64_t n_visible, double* loss, void* stream);
+
+/* Diagnostic (roofline counts, not on the hot path): re-run the forward of
+ * the prepared view with counters and return out4 = {evaluated (list entry,
+ * 8x8 warp block) pairs -- the pairs whose block the culling could not
+ * exclude, each evaluated at 64 pixels --, of which any pixel was visible,
+ * list entries walked per warp, 0}.  Writes color / final_t / n_contrib like
+ * vg_render_forward.  Synchronises the stream. */
+int vg_debug_forward_stats(vg_context* ctx, float* color, float* final_t, int32_t* n_contrib,
+                           unsigned long long* out4, void* stream);
+
 /* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and
  * MUFU ex2 ops/s over all SMs of `device`. */
 int vg_probe_peaks(int32_t device, double* fp32_per_s, double* mufu_per_s);

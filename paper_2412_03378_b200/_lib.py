@@ -105,6 +105,14 @@ EXPORTS = {
     "vg_probe_peaks": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "vg_raymarch": (C.c_int, [C.POINTER(VgScene), C.POINTER(VgCamera), C.c_int32, C.c_double,
                               C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vg_debug_forward_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]),
+    "vg_nccl_available": (C.c_int, []),
+    "vg_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "vg_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.c_int32]),
+    "vg_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "vg_allreduce_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                     C.c_void_p, C.c_void_p]),
     "vg_adam_step": (C.c_int, [C.POINTER(VgTrainState), C.POINTER(VgGrads), C.POINTER(VgAdamHparams),
                                C.c_void_p, C.c_void_p]),
     "vg_densify_scratch_bytes": (C.c_size_t, [C.c_int64]),

@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-r
 # per-file extra flags: preprocess rounds like numpy float64 (no FMA contraction)
 EXTRA = {"vg_preprocess.cu": ["-fmad=false"]}
 SOURCES = ["vg_preprocess.cu", "vg_radix.cu", "vg_span.cu", "vg_gamma.cu", "vg_blend.cu", "vg_splat.cu", "vg_finalize.cu",
-           "vg_capi.cu", "vg_probe.cu", "vg_optim.cu", "vg_det.cu", "vg_raymarch.cu", "vg_voxel.cu"]
+           "vg_capi.cu", "vg_probe.cu", "vg_optim.cu", "vg_det.cu", "vg_raymarch.cu", "vg_voxel.cu", "vg_comm.cu"]
 
 
 def nvcc():
@@ -74,7 +74,7 @@ def build(verbose=False, force=False, ptxas_verbose=False):
     objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
     if force or jobs or _newer(LIB, objs):
         tmp = LIB + ".tmp"
-        cmd = [cc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs
+        cmd = [cc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -109,6 +109,21 @@ class Engine:
         _lib.check(self.lib.vg_visible_pairs(self.ctx.handle, ctypes.byref(out)), "vg_visible_pairs")
         return int(out.value)
 
+    def forward_stats(self):
+        """Roofline counts of the prepared view (diagnostic, synchronises):
+        (evaluated forward (entry, warp-block) pairs, of which visible, list
+        entries walked per warp); runs an extra counting forward."""
+        H, W = int(self.cam.height), int(self.cam.width)
+        t = self.torch
+        color = self._buf(("color", "stats"), (H, W, 3), t.float32)
+        tfin = self._buf(("T", "stats"), (H, W), t.float32)
+        ncon = self._buf(("nc", "stats"), (H, W), t.int32)
+        out = (ctypes.c_ulonglong * 4)()
+        _lib.check(self.lib.vg_debug_forward_stats(self.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),
+                                                   _lib.ptr(ncon), out, self.stream()),
+                   "vg_debug_forward_stats")
+        return int(out[0]), int(out[1]), int(out[2])
+
     def backward(self, color, tfin, d_color, grads, d_t=None, accumulate=False):
         g = grads.struct(accumulate)
         _lib.check(self.lib.vg_render_backward(self.ctx.handle, _lib.ptr(color), _lib.ptr(tfin),

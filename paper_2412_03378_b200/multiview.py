@@ -22,31 +22,82 @@ def shard(n_views, world, rank):
     return list(range(rank, n_views, world))
 
 
-def reduce_across_ranks(flat, loss=None, group=None):
-    """Sum the flat gradient buffer (and the loss scalar) over all ranks with
-    one collective each; a no-op outside an initialised process group."""
+def reduce_across_ranks(flat, loss=None, group=None, visible=None, comm=None):
+    """Sum the flat gradient buffer (and the loss scalar) over all ranks and
+    OR the per-primitive `visible` flags (max of uint8), so every rank holds
+    the gradient of all views and the same GradAccum / densify inputs.  With
+    an NcclComm the three reductions run as one NCCL group through the C ABI
+    (vg_allreduce_grads); otherwise through torch.distributed (any backend:
+    gloo on CPU tests).  A no-op for one rank."""
+    if comm is not None:
+        comm.allreduce(flat, visible, loss)
+        return
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return
     if dist.get_world_size(group) == 1:
         return
     dist.all_reduce(flat, group=group)
+    if visible is not None:
+        dist.all_reduce(visible, op=dist.ReduceOp.MAX, group=group)
     if loss is not None:
         dist.all_reduce(loss, group=group)
 
 
-def sharded_step(views, view_fn, flat, loss, group=None, finish=None):
+class NcclComm:
+    """An NCCL communicator over the ranks of a torch.distributed group, owned
+    by the C ABI (vg_nccl_comm_init); rank 0's unique id travels over the
+    group (any backend).  allreduce() runs vg_allreduce_grads on the current
+    CUDA stream: the step's only data exchange."""
+
+    def __init__(self, device, group=None):
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import _lib
+        self.torch = torch
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(self.lib.vg_nccl_unique_id(uid), "vg_nccl_unique_id")
+        if self.world > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        self.handle = ctypes.c_void_p()
+        _lib.check(self.lib.vg_nccl_comm_init(ctypes.byref(self.handle), self.world, uid, self.rank,
+                                              self.device.index or 0), "vg_nccl_comm_init")
+
+    def allreduce(self, flat, visible=None, loss=None):
+        from . import _lib
+        st = self.torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self.lib.vg_allreduce_grads(
+            None, self.handle, _lib.ptr(flat), flat.numel(), _lib.ptr(visible),
+            visible.numel() if visible is not None else 0, _lib.ptr(loss), st), "vg_allreduce_grads")
+
+    def close(self):
+        if self.handle:
+            self.lib.vg_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+def sharded_step(views, view_fn, flat, loss, group=None, finish=None, visible=None):
     """Run view_fn(view, accumulate) for this rank's views (the first one
     overwrites, the rest accumulate into `flat`), call finish() once (the
     deferred per-Gaussian parameter chain, if any), then all-reduce."""
     loss.zero_()
     if not views:
         flat.zero_()
+        if visible is not None:
+            visible.zero_()
     for j, v in enumerate(views):
         view_fn(v, j > 0)
     if finish is not None:
         finish()
-    reduce_across_ranks(flat, loss, group)
+    reduce_across_ranks(flat, loss, group, visible=visible)
     return loss
 
 
@@ -66,7 +117,7 @@ class ViewShardedStep:
     buffer)."""
 
     def __init__(self, engine, dscene, cameras, targets, *, world=1, rank=0, tomography=False,
-                 parallel=False, extent=1.6, group=None, pipeline=True, contexts=None):
+                 parallel=False, extent=1.6, group=None, pipeline=True, contexts=None, comm=None):
         import torch
         from .engine import Engine
         self.torch = torch
@@ -87,6 +138,7 @@ class ViewShardedStep:
         self.parallel = parallel
         self.extent = extent
         self.group = group
+        self.comm = comm                            # NcclComm: the exchange through the C ABI
         self.grads = engine.new_grads(dscene)
         self.loss = torch.zeros((), dtype=torch.float64, device=engine.device)
         self.ready = None
@@ -211,7 +263,8 @@ class ViewShardedStep:
         self.loss.zero_()
         self._run_views()
         self._finish()
-        reduce_across_ranks(self.grads.flat, self.loss, self.group)
+        reduce_across_ranks(self.grads.flat, self.loss, self.group, visible=self.grads.visible,
+                            comm=self.comm)
         return self.loss
 
 

@@ -23,7 +23,8 @@ def declared_symbols():
 def test_header_declares_the_boundary():
     syms = declared_symbols()
     for name in ["vg_prepare", "vg_render_forward", "vg_render_backward", "vg_tomo_forward",
-                 "vg_tomo_backward", "vg_tile_lists", "vg_create", "vg_destroy", "vg_last_error"]:
+                 "vg_tomo_backward", "vg_tile_lists", "vg_create", "vg_destroy", "vg_last_error",
+                 "vg_allreduce_grads"]:
         assert name in syms
 
 

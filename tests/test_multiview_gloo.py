@@ -1,7 +1,9 @@
 """The N>1 path on CPU: two gloo ranks shard the views of a small scene,
 each computes its views' gradients (float64 oracle standing in for the GPU
 engine), accumulates them into one flat buffer and all-reduces it.  The
-reduced buffer on every rank must equal the serial sum over all views."""
+reduced buffer on every rank must equal the serial sum over all views, and
+the per-primitive `visible` flags the OR over all views (so every rank's
+GradAccum / densify inputs agree)."""
 
 from __future__ import annotations
 
@@ -43,7 +45,7 @@ def _view_grads(cfg, scene, v):
     flat = np.concatenate([g.d_means.ravel(), g.d_scales.ravel(), g.d_rotations.ravel(),
                            g.d_thetas.ravel(), g.d_colors.ravel(), g.d_kappas.ravel(),
                            g.d_background.ravel()])
-    return flat, loss * img.color.size
+    return flat, loss * img.color.size, np.asarray(g.visible, dtype=np.uint8)
 
 
 def _worker(rank, world, port, out_dir):
@@ -57,17 +59,21 @@ def _worker(rank, world, port, out_dir):
     size = len(_view_grads(cfg, scene, 0)[0])
     flat = torch.zeros(size, dtype=torch.float64)
     loss = torch.zeros((), dtype=torch.float64)
+    visible = torch.zeros(len(scene.means), dtype=torch.uint8)
 
     def view_fn(v, accumulate):
-        g, l = _view_grads(cfg, scene, v)
+        g, l, vis = _view_grads(cfg, scene, v)
         if accumulate:
             flat.add_(torch.from_numpy(g))
+            visible.copy_(torch.maximum(visible, torch.from_numpy(vis)))
         else:
             flat.copy_(torch.from_numpy(g))
+            visible.copy_(torch.from_numpy(vis))
         loss.add_(l)
 
-    sharded_step(views, view_fn, flat, loss)
+    sharded_step(views, view_fn, flat, loss, visible=visible)
     np.save(os.path.join(out_dir, f"rank{rank}.npy"), np.append(flat.numpy(), float(loss)))
+    np.save(os.path.join(out_dir, f"rank{rank}_visible.npy"), visible.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -89,14 +95,18 @@ def test_shard_covers_every_view_once():
         shard(4, 2, 2)
 
 
-def test_two_rank_gloo_allreduce_equals_serial_sum(tmp_path):
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_allreduce_equals_serial_sum(tmp_path, world):
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        start_method="spawn", join=True)
     cfg, scene = _scene_and_cams()
-    serial = sum(_view_grads(cfg, scene, v)[0] for v in range(N_VIEWS))
-    serial_loss = sum(_view_grads(cfg, scene, v)[1] for v in range(N_VIEWS))
+    per_view = [_view_grads(cfg, scene, v) for v in range(N_VIEWS)]
+    serial = sum(p[0] for p in per_view)
+    serial_loss = sum(p[1] for p in per_view)
+    serial_vis = np.max([p[2] for p in per_view], axis=0)
+    assert 0 < serial_vis.sum() < len(serial_vis) or serial_vis.all()
     for r in range(world):
         got = np.load(tmp_path / f"rank{r}.npy")
         np.testing.assert_allclose(got[:-1], serial, rtol=1e-12, atol=1e-14)
         assert got[-1] == pytest.approx(serial_loss, rel=1e-12)
+        np.testing.assert_array_equal(np.load(tmp_path / f"rank{r}_visible.npy"), serial_vis)
