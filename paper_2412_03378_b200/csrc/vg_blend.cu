@@ -54,6 +54,13 @@
 // 18.9 ms; packed pass 17.65 -> 17.28 ms)
 #define VG_BWD_PAIR 2
 #endif
+#ifndef VG_BWD_PREF
+// backward: load the next batch's list entries and the next chunk's
+// visibility words one step ahead.  A/B (serial, 16 views of config 3):
+// 17.98 -> 18.41 ms (+2.4 %; config 4 -0.8 %): the two extra live registers
+// cost more than the hidden L2 latency, so off
+#define VG_BWD_PREF 0
+#endif
 #ifndef VG_TOMO_SKIP
 // projector: (entry, column) pairs whose peak in the column is below 2^-60 of
 // the Gaussian's peak (< 1e-18 relative; far below float32 resolution) are not
@@ -585,12 +592,31 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
     if (io.det_pbase) return __float_as_uint(s.d.w) + __popc(smask[k] & ((1u << warp) - 1u));
     return (size_t)pos * (NT / 32) + warp;
   };
+#if VG_BWD_PREF
+  constexpr int PER = BATCH / NT;
+  uint32_t pv[PER];  // this thread's list entries of the next batch to stage
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const uint32_t i = r.x + threadIdx.x + j * NT;
+    pv[j] = i < r.y ? vals[i] : 0u;
+  }
+#endif
+  const uint32_t* vrow = vmask ? vmask + (size_t)warp * vm_words : nullptr;
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     if (__syncthreads_count(done) == NT) break;
+#if VG_BWD_PREF
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int sidx = threadIdx.x + j * NT;
+      const uint32_t i = base + sidx;
+      if (i < r.y) {
+        const uint32_t m = stage(sm, sidx, rec, pv[j], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
+#else
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
-      uint32_t i = base + sidx;
+      const uint32_t i = base + sidx;
       if (i < r.y) {
         const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
+#endif
         if (!vmask) smask[sidx] = (uint8_t)m;
         if (DET && io.det_pbase) {
           sm[sidx].d.w = __uint_as_float(io.det_pbase[i]);
@@ -598,8 +624,17 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         }
       }
     }
+#if VG_BWD_PREF
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const uint32_t i = base + BATCH + threadIdx.x + j * NT;
+      pv[j] = i < r.y ? vals[i] : 0u;
+    }
+#endif
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);
+    // visibility word of the first chunk (lane l: entry base + l)
+    uint32_t vwn = (vrow && lane < nb) ? __ldg(vrow + ((base + lane) >> 5)) : 0u;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
       unsigned bits;
       if (vmask) {
@@ -609,8 +644,13 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         // divergence bookkeeping: backward -6 % on config 3, -12 % on config 4
         // against extracting the 32 bits from the mask words per lane)
         const uint32_t g = base + c + lane;
-        const bool vb = (c + lane < nb) &&
-                        ((__ldg(vmask + (size_t)warp * vm_words + (g >> 5)) >> (g & 31u)) & 1u);
+#if VG_BWD_PREF
+        const uint32_t vw = vwn;
+        if (c + 32 + lane < nb) vwn = __ldg(vrow + ((g + 32) >> 5));
+#else
+        const uint32_t vw = __ldg(vrow + (g >> 5));
+#endif
+        const bool vb = (c + lane < nb) && ((vw >> (g & 31u)) & 1u);
         bits = __ballot_sync(FULL, vb);
       } else {
         const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
