@@ -534,13 +534,16 @@ __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, cons
   if (lane == 0 && rb.any_vis) io.visible[gb] = 1;
   const F2 xs = smem_reduce13x2p(va, vb, lane, wb);
   const float xa = lo(xs), xb = hi(xs);
-  if (lane < 13) {
+  if (DET) {
+    // every value is stored (slots are not pre-zeroed), the 3 pad floats too:
+    // whole 32-byte sectors, so L2 never holds partially written slot lines
+    if (lane < ACC_STRIDE) {
+      det_slot(io, pa)[lane] = lane < 13 ? xa : 0.f;
+      det_slot(io, pb)[lane] = lane < 13 ? xb : 0.f;
+    }
+  } else if (lane < 13) {
     const int q = lane;
-    if (DET) {
-      // every value is stored (compact slots are not pre-zeroed)
-      det_slot(io, pa)[q] = xa;
-      det_slot(io, pb)[q] = xb;
-    } else {
+    {
       // unconditional: a zero test per value costs more than the rare zero add
       atomicAdd(io.acc + (size_t)ga * ACC_STRIDE + q, xa);
       atomicAdd(io.acc + (size_t)gb * ACC_STRIDE + q, xb);
@@ -585,11 +588,10 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   // transmittance (so the same activity and the same early exits)
   F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f), P = f2s(0.f);
   bool done = !(G.in0 || G.in1);
-  // compact slots: the staging put entry k's slot base in sm[k].d.w and its
-  // four warp bits in smask[k]
+  // Gaussian-major slots: the staging put entry k's (Gaussian, tile) index in sm[k].d.w
   auto dslot = [&](uint32_t pos, const SRec& s, int k) -> size_t {
     if (!DET) return 0;
-    if (io.det_pbase) return __float_as_uint(s.d.w) + __popc(smask[k] & ((1u << warp) - 1u));
+    if (io.det_gvis4) return (size_t)__float_as_uint(s.d.w) * (NT / 32) + warp;
     return (size_t)pos * (NT / 32) + warp;
   };
 #if VG_BWD_PREF
@@ -618,9 +620,19 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
 #endif
         if (!vmask) smask[sidx] = (uint8_t)m;
-        if (DET && io.det_pbase) {
-          sm[sidx].d.w = __uint_as_float(io.det_pbase[i]);
-          smask[sidx] = io.det_vis4[i];
+        if (DET && io.det_gvis4) {
+          // this entry's (Gaussian, tile) index within the Gaussian's tile
+          // rectangle (row-major) and its four warp-visibility bits
+          const uint32_t gid = __float_as_uint(sm[sidx].c.w);
+          const ushort4 q = io.det_rect[gid];
+          const uint32_t ps = io.det_off[gid] + (uint32_t)(ty - q.y) * (uint32_t)(q.z - q.x + 1) +
+                              (uint32_t)(tx - q.x);
+          sm[sidx].d.w = __uint_as_float(ps);
+          uint32_t v = 0;
+#pragma unroll
+          for (int w = 0; w < NT / 32; ++w)
+            v |= ((__ldg(vmask + (size_t)w * vm_words + (i >> 5)) >> (i & 31u)) & 1u) << w;
+          io.det_gvis4[ps] = (uint8_t)v;
         }
       }
     }

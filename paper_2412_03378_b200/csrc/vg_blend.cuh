@@ -192,7 +192,8 @@ __device__ __forceinline__ void flush_acc_smem(const float (&v)[16], int lane, u
 
 __device__ __forceinline__ void flush_det_smem(const float (&v)[16], int lane, float* slot, float* wb) {
   const float s = smem_reduce13(v, lane, wb);
-  if (!(lane & 1) && lane < 26) slot[lane >> 1] = s;
+  // all 16 floats of the slot (3 zero pads): whole sectors
+  if (!(lane & 1)) slot[lane >> 1] = lane < 26 ? s : 0.f;
 }
 
 // Deterministic mode: the warp's 13 sums go to the (entry, warp) slot (no

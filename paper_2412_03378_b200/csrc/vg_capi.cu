@@ -59,11 +59,12 @@ struct vg_context {
   Buf cacc;                          // RGB gradient accumulators, SoA [3][N]
   Buf gm, gscratch;                  // sort_by="gamma": per-Gaussian M, M delta; merge scratch
   Buf det_part, det_cnt, det_off, det_slot, det_bg, det_loss, det_scan;  // deterministic mode
-  bool det_ready = false;            // det_slot maps the lists of the last prepare
+  bool det_ready = false;            // det_cnt / det_off describe the lists of the last prepare
+  bool det_slots_ready = false;      // ... and det_slot maps them (pair-major slots)
   Buf dcol, centers;                 // SH scenes: per-view dL/dRGB slabs [V][3][N] + centres
   int sh_views = 0;                  // views in dcol since the last parameter chain
   Buf tpart;                         // tomography forward: per-split partial images
-  Buf det_pref, det_vcnt, det_vscan, det_vis4;  // deterministic mode: compact pair-major slots
+  Buf det_gvis4, det_big;             // deterministic mode: warp bits per (Gaussian, tile); large-Gaussian queue
   // deterministic VG_DEFER: d_background (3 floats) and loss (double at +16 B)
   // partials summed per context in view order, added by vg_finalize_grads
   Buf det_sums;
@@ -219,7 +220,7 @@ void vg_destroy(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_pref, &c->det_vcnt, &c->det_vscan, &c->det_vis4, &c->det_sums};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_gvis4, &c->det_big, &c->det_sums};
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->total_host) cudaFreeHost(c->total_host);
@@ -310,6 +311,7 @@ int vg_prepare_async(vg_context* c, const vg_scene* s, const vg_camera* cam,
   c->prepared = false;
   c->have_fwd = false;
   c->det_ready = false;
+  c->det_slots_ready = false;
   const int64_t npix = (int64_t)k.width * k.height;
   VG_TRY(ensure(c->ranges, sizeof(uint2) * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->n_act, sizeof(int) * (size_t)npix, st));
@@ -704,35 +706,44 @@ int vg_finalize_grads(vg_context* c, vg_grads* g, void* stream) {
   return VG_OK;
 }
 
-// Deterministic mode: the Gaussian -> slot map of the current lists (once per
-// prepare) and zeroed per-(entry, warp) slots for one backward.
+// Deterministic mode: the per-Gaussian tile counts / offsets of the current
+// lists (once per prepare; plus the pair-major slot map unless `gmajor`), the
+// slot array for one backward, and zeroed per-tile partials.  gmajor (render
+// backward with a forward visibility mask): Gaussian-major slots, their warp
+// bytes cleared (entries past a tile's early stop are never staged, so their
+// bytes must read as "no warp visible").  Without list entries there are no
+// slots, but the per-tile d_background / loss partials still take the
+// fixed-order route (the blend selects it on det_part).
 static int det_setup(vg_context* c, float*& part, float*& bg, double*& loss, cudaStream_t st,
-                     BwdIO* compact = nullptr) {
+                     BwdIO* gmajor = nullptr) {
   const int64_t n = c->scene.n, P = c->pairs;
-  if (!c->det_ready) {
-    VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
-    VG_TRY(ensure(c->det_off, sizeof(uint32_t) * ((size_t)n + 1), st));
-    VG_TRY(ensure(c->det_slot, sizeof(uint32_t) * (size_t)P, st));
-    VG_TRY(ensure(c->det_scan, scan_u32_scratch_bytes(n) + 16, st));
-    VG_CUDA(det_prepare(n, (const ushort4*)c->rect.p, (const uint2*)c->ranges.p, c->vals,
-                        c->n_tiles, c->cam.ntx, (uint32_t*)c->det_cnt.p, (uint32_t*)c->det_off.p,
-                        (uint32_t*)c->det_slot.p, c->det_scan.p, (uint32_t*)c->det_off.p + n, st));
-    c->det_ready = true;
-  }
-  VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
-  if (compact) {
-    // one slot per (entry, warp) pair the forward marked visible, pair-major;
-    // every slot is written by the backward, so no clearing
-    VG_TRY(ensure(c->det_pref, sizeof(uint32_t) * ((size_t)P + 1), st));
-    VG_TRY(ensure(c->det_vcnt, sizeof(uint32_t) * (size_t)P, st));
-    VG_TRY(ensure(c->det_vis4, (size_t)P, st));
-    VG_TRY(ensure(c->det_vscan, det_pairs_scratch_bytes(P), st));
-    VG_CUDA(det_pairs((const uint32_t*)c->vmask.p, c->vm_words, P, (uint8_t*)c->det_vis4.p,
-                      (uint32_t*)c->det_vcnt.p, (uint32_t*)c->det_pref.p, c->det_vscan.p, st));
-    compact->det_pbase = (const uint32_t*)c->det_pref.p;
-    compact->det_vis4 = (const uint8_t*)c->det_vis4.p;
+  if (n > 0 && P > 0) {
+    const bool need_slots = gmajor == nullptr;
+    if (!c->det_ready || (need_slots && !c->det_slots_ready)) {
+      VG_TRY(ensure(c->det_cnt, sizeof(uint32_t) * (size_t)n, st));
+      VG_TRY(ensure(c->det_off, sizeof(uint32_t) * ((size_t)n + 1), st));
+      VG_TRY(ensure(c->det_scan, scan_u32_scratch_bytes(n) + 16, st));
+      if (need_slots) VG_TRY(ensure(c->det_slot, sizeof(uint32_t) * (size_t)P, st));
+      VG_CUDA(det_prepare(n, (const ushort4*)c->rect.p, (const uint2*)c->ranges.p, c->vals,
+                          c->n_tiles, c->cam.ntx, (uint32_t*)c->det_cnt.p, (uint32_t*)c->det_off.p,
+                          need_slots ? (uint32_t*)c->det_slot.p : nullptr, c->det_scan.p,
+                          (uint32_t*)c->det_off.p + n, st));
+      c->det_ready = true;
+      c->det_slots_ready = c->det_slots_ready || need_slots;
+    }
+    VG_TRY(ensure(c->det_part, det_part_bytes(P), st));
+    if (gmajor) {
+      VG_TRY(ensure(c->det_gvis4, (size_t)P, st));
+      VG_TRY(ensure(c->det_big, sizeof(uint32_t) * ((size_t)n + 1), st));
+      VG_CUDA(cudaMemsetAsync(c->det_gvis4.p, 0, (size_t)P, st));
+      gmajor->det_off = (const uint32_t*)c->det_off.p;
+      gmajor->det_rect = (const ushort4*)c->rect.p;
+      gmajor->det_gvis4 = (uint8_t*)c->det_gvis4.p;
+    } else {
+      VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+    }
   } else {
-    VG_CUDA(cudaMemsetAsync(c->det_part.p, 0, det_part_bytes(P), st));
+    VG_TRY(ensure(c->det_part, 64, st));
   }
   VG_TRY(ensure(c->det_bg, sizeof(float) * 3 * (size_t)c->n_tiles, st));
   VG_TRY(ensure(c->det_loss, sizeof(double) * (size_t)c->n_tiles, st));
@@ -789,7 +800,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     VG_TRY(ensure(c->offset, sizeof(uint32_t) * (size_t)(c->scene.n > 0 ? c->scene.n : 1), st));
     io.visible = (uint8_t*)c->offset.p;
   }
-  const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
+  const bool det = c->opt.deterministic != 0;
   const bool vm = c->vmask_valid && c->opt.alpha_cut > 0;
   if (det)
     VG_TRY(det_setup(c, io.det_part, io.det_bg, io.det_loss, st,
@@ -810,11 +821,11 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
       float* bg_out;
       double* loss_out;
       VG_TRY(det_targets(c, g, loss_sum, bg_out, loss_out, st));
-      VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
-                         (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
+      VG_CUDA(det_reduce(c->pairs > 0 ? c->scene.n : 0, (const uint32_t*)c->det_cnt.p,
+                         (const uint32_t*)c->det_off.p, (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                          (float*)c->acc.p, c->n_tiles, (const float*)c->det_bg.p,
                          target ? (const double*)c->det_loss.p : nullptr, bg_out,
-                         loss_out, st, io.det_pbase, io.det_vis4));
+                         loss_out, st, io.det_gvis4, (uint32_t*)c->det_big.p));
       VG_LAUNCHED(c, 2);
     }
     VG_TRY(finish_view(c, g, st));
@@ -824,6 +835,15 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
     launch_render_bwd(c->n_tiles, nullptr, nullptr, (const uint2*)c->ranges.p,
                       (const uint32_t*)c->tord.p, p, false, target ? 1 : 0, io, nullptr, 0, st);
     VG_LAUNCHED(c, 1);
+    if (det) {
+      float* bg_out;
+      double* loss_out;
+      VG_TRY(det_targets(c, g, loss_sum, bg_out, loss_out, st));
+      VG_CUDA(det_reduce(0, nullptr, nullptr, nullptr, nullptr, nullptr, c->n_tiles,
+                         (const float*)c->det_bg.p, target ? (const double*)c->det_loss.p : nullptr,
+                         bg_out, loss_out, st));
+      VG_LAUNCHED(c, 1);
+    }
   }
   return VG_OK;
 }
@@ -892,7 +912,7 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
     vis = (uint8_t*)c->offset.p;
   }
   float scale = (float)(2.0 / ((double)c->cam.width * (double)c->cam.height));
-  const bool det = c->opt.deterministic != 0 && c->scene.n > 0 && c->pairs > 0;
+  const bool det = c->opt.deterministic != 0;
   float *dpart = nullptr, *dbg = nullptr;
   double* dloss = nullptr;
   if (det) VG_TRY(det_setup(c, dpart, dbg, dloss, st));
@@ -911,8 +931,8 @@ static int tomo_bwd_common(vg_context* c, const float* d_image, const float* ima
     vg_grads gn = *g;
     gn.d_background = nullptr;
     VG_TRY(det_targets(c, &gn, loss_sum, bg_out, loss_out, st));
-    VG_CUDA(det_reduce(c->scene.n, (const uint32_t*)c->det_cnt.p, (const uint32_t*)c->det_off.p,
-                       (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
+    VG_CUDA(det_reduce(c->pairs > 0 ? c->scene.n : 0, (const uint32_t*)c->det_cnt.p,
+                       (const uint32_t*)c->det_off.p, (const uint32_t*)c->det_slot.p, (const float*)c->det_part.p,
                        (float*)c->acc.p, c->n_tiles, dbg, target ? dloss : nullptr, nullptr,
                        loss_out, st));
     VG_LAUNCHED(c, 2);

@@ -36,11 +36,15 @@ struct BwdIO {
   float* det_part = nullptr;
   float* det_bg = nullptr;
   double* det_loss = nullptr;
-  // compact slots (render backward with a forward visibility mask): one slot per
-  // visible (entry, warp) pair, pair-major: slot of (entry p, warp w) =
-  // det_pbase[p] + popcount(det_vis4[p] & ((1 << w) - 1))
-  const uint32_t* det_pbase = nullptr;
-  const uint8_t* det_vis4 = nullptr;
+  // Gaussian-major slots (render backward with a forward visibility mask): the
+  // (entry, warp w) partial of Gaussian g in tile (tx, ty) goes to slot
+  // 4 (det_off[g] + (ty - y0) W + (tx - x0)) + w, with (x0, y0, W) from g's
+  // tile rectangle det_rect[g], and det_gvis4 at the same (Gaussian, tile)
+  // index gets the entry's four warp-visibility bits; slots of invisible
+  // pairs are never written nor read
+  const uint32_t* det_off = nullptr;
+  const ushort4* det_rect = nullptr;
+  uint8_t* det_gvis4 = nullptr;
 };
 
 // gm (nullable): per binned Gaussian M and M (mean - centre) in float64, for sort_by="gamma"
@@ -60,18 +64,16 @@ cudaError_t scan_u32(const uint32_t* in, uint32_t* out, void* scratch, uint32_t*
                      cudaStream_t st);
 size_t scan_u32_scratch_bytes(int64_t n);
 size_t det_part_bytes(int64_t pairs);
+// cnt[g] = tiles of g's rectangle, off = their exclusive scan; slot (nullable):
+// the pair-major map (g's k-th tile -> its list position)
 cudaError_t det_prepare(int64_t n, const ushort4* rect, const uint2* ranges, const uint32_t* vals,
                         int n_tiles, int ntx, uint32_t* cnt, uint32_t* off, uint32_t* slot,
                         void* scan_scratch, uint32_t* total, cudaStream_t st);
 cudaError_t det_reduce(int64_t n, const uint32_t* cnt, const uint32_t* off, const uint32_t* slot,
                        const float* part, float* acc, int n_tiles, const float* bg_part,
                        const double* loss_part, float* d_background, double* loss_sum,
-                       cudaStream_t st, const uint32_t* pbase = nullptr, const uint8_t* vis4 = nullptr);
-// compact pair-major slots from a visibility mask of 4 rows x vm_words words:
-// vis4[p] = the 4 warp bits of entry p, pbase[p] = slots before entry p (pbase[P] = total)
-cudaError_t det_pairs(const uint32_t* vm, int vm_words, int64_t pairs, uint8_t* vis4, uint32_t* cnt_tmp,
-                      uint32_t* pbase, void* scratch, cudaStream_t st);
-size_t det_pairs_scratch_bytes(int64_t pairs);
+                       cudaStream_t st, const uint8_t* gvis4 = nullptr,
+                       uint32_t* big_scratch = nullptr);  // gvis4: n + 1 uint32
 // deterministic VG_DEFER: out += (bg[3], loss); the sums are cleared
 void launch_det_flush(float* bg, double* loss, float* bg_out, double* loss_out, cudaStream_t st);
 // sort_by="gamma" re-sort of every tile list (vg_gamma.cu)
