@@ -24,14 +24,20 @@ __device__ __forceinline__ double centre(const Axes& a, int ax, int k) {
   return a.bmin[ax] + ((double)k + 0.5) * a.sp[ax];
 }
 
-// number of centres < v (side="left") or <= v (side="right")
+// numpy.searchsorted(axis_centres, v, side="left" | "right") for one key --
+// the plain binary search numpy runs, so it agrees with the reference on any
+// box: ascending (the usual case: the count of centres < v, resp. <= v), and
+// also degenerate (zero spacing: every centre at bbox_min) or reversed
+// (descending centres), which tomo.voxelize accepts unchecked
 __device__ __forceinline__ int count_below(const Axes& a, int ax, double v, bool inclusive) {
-  int k = (int)ceil((v - a.bmin[ax]) / a.sp[ax] - 0.5);
-  k = max(0, min(a.n[ax], k));
-  auto below = [&](int j) { const double c = centre(a, ax, j); return inclusive ? c <= v : c < v; };
-  while (k > 0 && !below(k - 1)) --k;
-  while (k < a.n[ax] && below(k)) ++k;
-  return k;
+  int lo = 0, hi = a.n[ax];
+  while (lo < hi) {
+    const int mid = lo + ((hi - lo) >> 1);
+    const double c = centre(a, ax, mid);
+    if (inclusive ? c <= v : c < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
 }
 
 __global__ void __launch_bounds__(256) k_voxelize(vg_scene s, Axes a, double* __restrict__ out) {
@@ -85,7 +91,6 @@ extern "C" int vg_voxelize(const vg_scene* s, const double* bbox_min, const doub
   voxel::Axes a;
   for (int k = 0; k < 3; ++k) {
     if (shape[k] <= 0) return set_error(VG_EINVAL, "vg_voxelize: resolution must be positive");
-    if (!(bbox_max[k] > bbox_min[k])) return set_error(VG_EINVAL, "vg_voxelize: empty bounding box");
     a.n[k] = shape[k];
     a.bmin[k] = bbox_min[k];
     a.sp[k] = (bbox_max[k] - bbox_min[k]) / (double)shape[k];

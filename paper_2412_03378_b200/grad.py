@@ -173,9 +173,12 @@ def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
 
 @dataclass
 class LossSpec:
-    """Photometric loss (grad.py:308-320).  This build implements 'l2' and
-    'l1' on the device; 'dssim'/'mixed' are outside the hot path."""
-    kind: str = "l2"
+    """Photometric loss (grad.py:308-320): 'l1', 'l2', 'dssim', or 'mixed'
+    ((1 - lam) L1 + lam D-SSIM), the reference's default.  The device fuses
+    L2 into the backward blend (vg_render_backward_l2); the other kinds are
+    formed by loss_and_grad on the rendered image (torch on its device, or
+    numpy) and enter through the explicit-gradient backward."""
+    kind: str = "mixed"
     lam: float = 0.2
 
     @classmethod
@@ -186,22 +189,45 @@ class LossSpec:
         return cls(kind=text.strip())
 
 
+_KINDS = ("l1", "l2", "dssim", "mixed")
+
+
+def loss_value(image, target, spec: LossSpec = None):
+    """grad.loss_value (grad.py:323-335)."""
+    return loss_and_grad(image, target, spec)[0]
+
+
 def loss_and_grad(image, target, spec: LossSpec = None):
-    """Loss value and dL/d(image) (grad.py:338-358) for 'l2' and 'l1'."""
-    spec = spec or LossSpec("l2")
-    if spec.kind not in ("l1", "l2"):
-        if spec.kind in ("dssim", "mixed"):
-            raise NotImplementedError(f"loss {spec.kind!r} is outside this build's hot path")
+    """Loss value and dL/d(image) (grad.py:338-358) for every loss kind; numpy
+    in -> float, numpy float64 gradient; torch in -> float, torch float64
+    gradient on the image's device.  D-SSIM = 1 - mean SSIM
+    (metrics.ssim_with_grad)."""
+    from . import metrics
+    spec = spec or LossSpec()
+    if spec.kind not in _KINDS:
         raise ValueError(f"unknown loss kind {spec.kind!r}")
     if _lib_is_torch(image):
         import torch
-        r = image - target.to(image)
+        x = image.to(torch.float64)
+        t = target.to(device=x.device, dtype=torch.float64) if _lib_is_torch(target) else \
+            torch.as_tensor(np.asarray(target, dtype=float), device=x.device)
+        r = x - t
         n = r.numel()
         if spec.kind == "l2":
             return float((r * r).mean()), 2.0 * r / n
-        return float(r.abs().mean()), torch.sign(r) / n
-    r = np.asarray(image, dtype=float) - np.asarray(target, dtype=float)
-    n = r.size
-    if spec.kind == "l2":
-        return float(np.mean(r * r)), 2.0 * r / n
-    return float(np.mean(np.abs(r))), np.sign(r) / n
+        l1, g1 = float(r.abs().mean()), torch.sign(r) / n
+    else:
+        x = np.asarray(image, dtype=float)
+        t = np.asarray(target, dtype=float)
+        r = x - t
+        n = r.size
+        if spec.kind == "l2":
+            return float(np.mean(r * r)), 2.0 * r / n
+        l1, g1 = float(np.mean(np.abs(r))), np.sign(r) / n
+    if spec.kind == "l1":
+        return l1, g1
+    sv, ds = metrics.ssim_with_grad(x, t)
+    sv = float(sv)
+    if spec.kind == "dssim":
+        return 1.0 - sv, -ds
+    return (1.0 - spec.lam) * l1 + spec.lam * (1.0 - sv), (1.0 - spec.lam) * g1 - spec.lam * ds

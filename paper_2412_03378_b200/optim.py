@@ -345,19 +345,24 @@ def _events(scene, scratch, n, accum, config, extent, iteration, lib, new, kept)
 
 
 def fit_image(targets, cameras, config: TrainConfig, mode="analytic", init_scene=None,
-              threads=None, background=(0, 0, 0), callback=None):
+              threads=None, background=(0, 0, 0), callback=None, deterministic=True):
     """optim.fit_image (optim.py:343-416) on the GPU, analytic mode: one
-    camera per iteration in the reference's seeded order, fused L2 loss +
-    backward, the fused Adam step, periodic densify/prune; the loss is read
-    back once per iteration (the reference's finite check) and the scene
-    restored from the last checkpoint on divergence.  Returns
-    (DeviceScene, FitReport); final_metrics holds the per-view mse/psnr."""
+    camera per iteration in the reference's seeded order, the loss and
+    backward (L2 fused into the backward blend; l1 / dssim / mixed formed by
+    grad.loss_and_grad on the rendered image on the device, then the
+    explicit-gradient backward), the fused Adam step, periodic
+    densify/prune; the loss is read back once per iteration (the reference's
+    finite check) and the scene restored from the last checkpoint on
+    divergence.  deterministic (default): fixed-order gradient sums, so a run
+    is bitwise reproducible like the reference's (its densify decisions
+    cannot flip on summation order).  Returns (DeviceScene, FitReport);
+    final_metrics holds the per-view mse/psnr."""
     import torch
     from .engine import Engine
+    from .grad import loss_and_grad
     if mode != "analytic":
         raise NotImplementedError("only the analytic mode is on the device")
-    if config.loss.kind != "l2":
-        raise NotImplementedError("the device fit loop fuses the L2 loss only")
+    fused = config.loss.kind == "l2"
     if not isinstance(targets, (list, tuple)):
         targets = [targets]
         cameras = [cameras] if not isinstance(cameras, (list, tuple)) else cameras
@@ -378,7 +383,7 @@ def fit_image(targets, cameras, config: TrainConfig, mode="analytic", init_scene
         order = np.concatenate([rng.permutation(len(cameras)) for _ in range(epochs)])[:config.iterations]
     else:
         order = np.zeros(config.iterations, dtype=int)
-    eng = Engine(dev.index)
+    eng = Engine(dev.index, deterministic=deterministic)
     grads = eng.new_grads(scene)
     loss = torch.zeros((), dtype=torch.float64, device=dev)
     checkpoint = _clone_scene(scene)
@@ -388,10 +393,15 @@ def fit_image(targets, cameras, config: TrainConfig, mode="analytic", init_scene
         H, W = int(cam.height), int(cam.width)
         eng.prepare(scene, cam)
         color, tfin, _ = eng.forward(counts=False)
-        loss.zero_()
-        eng.backward_l2(color, tfin, tgts[order[it]], grads, accumulate=False, loss=loss)
+        if fused:
+            loss.zero_()
+            eng.backward_l2(color, tfin, tgts[order[it]], grads, accumulate=False, loss=loss)
+        else:
+            value, d_img = loss_and_grad(color, tgts[order[it]], config.loss)
+            eng.backward(color, tfin, d_img.to(torch.float32).contiguous(), grads, accumulate=False)
         trainer.step(grads, it, accum=accum, check=False)
-        value = float(loss) / (H * W * 3)          # the one sync of the iteration
+        if fused:
+            value = float(loss) / (H * W * 3)      # the one sync of the iteration
         if not math.isfinite(value):
             report.diverged = True
             scene = checkpoint

@@ -127,13 +127,18 @@ def _tomo_init(config, bbox, rng):
 
 
 def reconstruct(projections, config, *, bbox=None, resolution=64, reference=None, threads=None,
-                init_scene=None, callback=None):
+                init_scene=None, callback=None, deterministic=True):
     """tomo.reconstruct (tomo.py:442-519) on the GPU: fit a mixture to
     cone-beam log-intensity projections with the device Trainer (fused Adam,
     GradAccum, densify/prune) -- one projection per iteration in the
     reference's seeded order, targets normalised by their joint maximum, the
     projector and adjoint on the device; returns (DeviceScene, DensityGrid,
-    report dict).  The device loop fuses the L2 loss only (like fit_image)."""
+    report dict).  L2 is fused into the adjoint; l1 / dssim / mixed (the
+    reference's default) are formed by grad.loss_and_grad on the normalised
+    projection on the device and pulled back through the explicit-gradient
+    adjoint.  deterministic (default): fixed-order gradient sums, so the run
+    is bitwise reproducible (densify / prune decisions cannot flip on
+    summation order)."""
     import math
 
     import torch
@@ -146,8 +151,7 @@ def reconstruct(projections, config, *, bbox=None, resolution=64, reference=None
     for p in projections:
         if np.any(np.asarray(p.image) < 0):
             raise ValueError("projections must be non-negative log-intensities")
-    if config.loss.kind != "l2":
-        raise NotImplementedError("the device reconstruction loop fuses the L2 loss only")
+    from .grad import loss_and_grad
     if bbox is None:
         bbox = (-np.ones(3), np.ones(3))
     bbox = (np.asarray(bbox[0], dtype=float), np.asarray(bbox[1], dtype=float))
@@ -165,7 +169,7 @@ def reconstruct(projections, config, *, bbox=None, resolution=64, reference=None
     n_views = len(projections)
     epochs = -(-config.iterations // n_views)
     order = np.concatenate([rng.permutation(n_views) for _ in range(epochs)])[:config.iterations]
-    eng = Engine(dev.index)
+    eng = Engine(dev.index, deterministic=deterministic)
     grads = eng.new_grads(scene)
     checkpoint = _clone_scene(scene)
     densify_stop = config.densify_stop_fraction * config.iterations
@@ -174,12 +178,16 @@ def reconstruct(projections, config, *, bbox=None, resolution=64, reference=None
         cam = cameras[v]
         eng.prepare(scene, cam, tomo=True)
         image = eng.tomo_forward()
-        # L2 of image / norm against the normalised target; its gradient is
-        # chained through the scale (tomo.py:486-494)
-        r = image / norm - targets[v]
-        n = r.numel()
-        value_t = (r.double() ** 2).sum() / n
-        d_img = (r * (2.0 / (n * norm))).contiguous()
+        # the loss of image / norm against the normalised target; its gradient
+        # is chained through the scale (tomo.py:486-494)
+        if config.loss.kind == "l2":
+            r = image / norm - targets[v]
+            n = r.numel()
+            value_t = (r.double() ** 2).sum() / n
+            d_img = (r * (2.0 / (n * norm))).contiguous()
+        else:
+            value_t, d = loss_and_grad(image / norm, targets[v], config.loss)
+            d_img = (d / norm).to(torch.float32).contiguous()
         eng.tomo_backward(d_img, grads, accumulate=False)
         trainer.step(grads, it, accum=accum, check=False)
         value = float(value_t)                       # the one host sync of the iteration

@@ -8,7 +8,8 @@ themselves.
 Inputs: six 24x24 cone-beam projections of the reference's blob phantom (the
 projections themselves are stored, so the test needs no phantom code), an
 L2 TrainConfig with 16 initial primitives and 24 iterations (no densify
-before iteration 24), seed 0.  Stored: the projections and cameras, the loss
+before iteration 24), seed 0; and the same run with loss="mixed" (the
+reference's default: 0.8 L1 + 0.2 D-SSIM), mixed_* keys.  Stored: the projections and cameras, the loss
 of every iteration, the final scene, its voxel grid at resolution 20, the
 psnr_3d / ssim_3d against the phantom grid, and a separate voxelize case
 (anisotropic rotated primitives, anisotropic resolution, box partly outside),
@@ -51,6 +52,14 @@ def main():
     out["grid"] = grid.values
     out["psnr_3d"] = np.array(rep["psnr_3d"])
     out["ssim_3d"] = np.array(rep["ssim_3d"])
+    # the same run with the reference's default loss, mixed (0.8 L1 + 0.2 D-SSIM)
+    cfg_m = TrainConfig(iterations=24, loss="mixed", n_init=16, seed=0)
+    scene_m, grid_m, rep_m = tomo.reconstruct(projs, cfg_m, resolution=20, reference=ref_grid)
+    out["mixed_losses"] = np.array(rep_m["losses"])
+    for k in ("means", "scales", "rotations", "thetas"):
+        out[f"mixed_final_{k}"] = getattr(scene_m, k)
+    out["mixed_grid"] = grid_m.values
+    out["mixed_psnr_3d"] = np.array(rep_m["psnr_3d"])
     # voxelize on its own
     rng = np.random.default_rng(5)
     n = 40
@@ -63,6 +72,13 @@ def main():
     vg = tomo.voxelize(vs, resolution=(18, 14, 22), bbox=(bmin, bmax))
     out.update(vox_means=vs.means, vox_scales=vs.scales, vox_rotations=vs.rotations,
                vox_thetas=vs.thetas, vox_bmin=bmin, vox_bmax=bmax, vox_values=vg.values)
+    # boxes tomo.voxelize accepts unchecked: a flat one (zero spacing on y) and a
+    # reversed one (bbox_max < bbox_min on x)
+    for tag, lo, hi in (("flat", [-1.0, 0.1, -1.2], [0.9, 0.1, 1.0]),
+                        ("reversed", [0.9, -0.8, -1.2], [-1.0, 1.1, 1.0])):
+        g = tomo.voxelize(vs, resolution=(9, 7, 11), bbox=(np.array(lo), np.array(hi)))
+        out[f"vox_{tag}_bmin"], out[f"vox_{tag}_bmax"] = np.array(lo), np.array(hi)
+        out[f"vox_{tag}_values"] = g.values
     np.savez_compressed(os.path.join(HERE, "recon.npz"), **out)
     # density grid I/O (tomo.save_density_grid): a 5x6x7 grid with negative and
     # awkward values and an asymmetric box -> io_grid.raw / io_grid.txt

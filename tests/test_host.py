@@ -81,3 +81,33 @@ def test_configs_deterministic_and_shaped():
     assert t.parallel and len(t.cameras) == 6
     o = configs.opaque(n=1000, size=32, n_views=2)
     assert np.allclose(o.scene.scales[:, 2], 1e-3)
+
+
+@pytest.mark.parametrize("name", ["rgb", "grey"])
+@pytest.mark.parametrize("kind", ["l1", "l2", "dssim", "mixed:0.2", "mixed:0.7"])
+def test_losses_match_reference_golden(name, kind):
+    """grad.loss_and_grad for every loss kind (grad.py:338-358, the SSIM
+    gradient of metrics.py:70-95) against the reference's own values
+    (tests/golden/make_golden_loss.py), on numpy and on torch (float64)."""
+    import os
+    import torch
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "loss.npz"))
+    a, b = g[f"{name}_a"], g[f"{name}_b"]
+    key = kind.replace(":", "_").replace(".", "")
+    spec = vg.LossSpec.parse(kind)
+    v, d = vg.loss_and_grad(a, b, spec)
+    assert v == pytest.approx(float(g[f"{name}_{key}_value"]), rel=1e-12, abs=1e-15)
+    np.testing.assert_allclose(d, g[f"{name}_{key}_grad"], rtol=1e-10, atol=1e-15)
+    vt, dt = vg.loss_and_grad(torch.from_numpy(a), torch.from_numpy(b), spec)
+    assert vt == pytest.approx(v, rel=1e-12, abs=1e-15)
+    np.testing.assert_allclose(dt.numpy(), d, rtol=1e-10, atol=1e-15)
+    assert vg.loss_value(a, b, spec) == v
+
+
+def test_loss_default_is_the_reference_default():
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "loss.npz"))
+    assert vg.LossSpec().kind == str(g["default_kind"]) == "mixed"
+    assert vg.LossSpec().lam == float(g["default_lam"])
+    from paper_2412_03378_b200.optim import TrainConfig
+    assert TrainConfig().loss.kind == "mixed"

@@ -103,10 +103,15 @@ def test_densify_and_prune_matches_reference():
     np.testing.assert_allclose(mom[:, :14], m_ref, rtol=1e-5, atol=1e-6 * np.abs(m_ref).max())
 
 
-def test_fit_image_tracks_the_oracle_loop():
+@pytest.mark.parametrize("loss", ["l2", "mixed"])
+def test_fit_image_tracks_the_oracle_loop(loss):
     """Five iterations of fit_image (two cameras, seeded order) against the
     same loop run with the CPU oracles: per-iteration losses and the final
-    scene agree."""
+    scene agree.  l2 is fused into the backward blend; mixed (the reference's
+    default loss) goes through grad.loss_and_grad on the device image and the
+    explicit-gradient backward (the oracle side uses the numpy loss pinned to
+    the reference's golden values, tests/test_host.py)."""
+    from paper_2412_03378_b200.grad import LossSpec, loss_and_grad
     from oracle import optim_oracle as OO
     from oracle import volgauss_oracle as O
     from paper_2412_03378_b200 import configs, optim
@@ -120,7 +125,7 @@ def test_fit_image_tracks_the_oracle_loop():
                               rotations=s.rotations.astype(np.float64), thetas=s.thetas.astype(np.float64),
                               colors=np.clip(s.colors.astype(np.float64), 0.02, 0.98),
                               background=np.zeros(3))
-    tc = optim.TrainConfig(iterations=5)
+    tc = optim.TrainConfig(iterations=5, loss=loss)
     gpu_scene, rep = optim.fit_image(targets, cams, tc, init_scene=scene64)
     # the oracle loop (optim.fit_image's body with the pinned CPU oracles)
     rng = np.random.Generator(np.random.Philox(key=tc.seed))
@@ -134,7 +139,7 @@ def test_fit_image_tracks_the_oracle_loop():
     for it in range(5):
         cam, tgt = cams[order[it]], targets[order[it]]
         out = O.render(sc, cam)
-        value, dimg = O.l2_loss_and_grad(out.color, tgt)
+        value, dimg = loss_and_grad(out.color, tgt, LossSpec.parse(loss))
         g = O.backward(sc, cam, dimg)
         tr.step(g, it)
         losses.append(value)

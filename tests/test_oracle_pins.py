@@ -201,6 +201,11 @@ def test_voxelize_oracle_pinned_to_reference():
     v = O.voxelize(d["vox_means"], d["vox_scales"], d["vox_rotations"], d["vox_thetas"],
                    d["vox_values"].shape, d["vox_bmin"], d["vox_bmax"])
     assert np.array_equal(v, d["vox_values"])
+    # boxes the reference accepts unchecked: flat (zero spacing) and reversed
+    for tag in ("flat", "reversed"):
+        v = O.voxelize(d["vox_means"], d["vox_scales"], d["vox_rotations"], d["vox_thetas"],
+                       d[f"vox_{tag}_values"].shape, d[f"vox_{tag}_bmin"], d[f"vox_{tag}_bmax"])
+        assert np.array_equal(v, d[f"vox_{tag}_values"]), tag
 
 
 def test_volume_metrics_match_reference():

@@ -877,6 +877,15 @@ def test_voxelize_matches_reference():
                        d["vox_bmin"], d["vox_bmax"])
     np.testing.assert_allclose(grid.values, ref32, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(grid.values, d["vox_values"], rtol=1e-5, atol=1e-6 * d["vox_values"].max())
+    # flat (zero spacing) and reversed boxes, which tomo.voxelize accepts
+    # unchecked: the device's index ranges are numpy's searchsorted on them
+    for tag in ("flat", "reversed"):
+        lo, hi = d[f"vox_{tag}_bmin"], d[f"vox_{tag}_bmax"]
+        ref_v = d[f"vox_{tag}_values"]
+        g2 = tomo.voxelize(scene, resolution=ref_v.shape, bbox=(lo, hi))
+        o2 = O.voxelize(scene.means, scene.scales, scene.rotations, scene.thetas, ref_v.shape, lo, hi)
+        np.testing.assert_allclose(g2.values, o2, rtol=1e-9, atol=1e-12, err_msg=tag)
+        np.testing.assert_allclose(g2.values, ref_v, rtol=1e-5, atol=1e-6 * ref_v.max(), err_msg=tag)
     empty = tomo.voxelize(SimpleNamespace(means=np.zeros((0, 3)), scales=np.zeros((0, 3)),
                                           rotations=np.zeros((0, 4)), thetas=np.zeros(0),
                                           colors=np.zeros((0, 3)), background=np.zeros(3)),
@@ -895,6 +904,8 @@ def test_reconstruct_follows_reference():
     ref = tomo.DensityGrid(d["ref_grid"], -np.ones(3), np.ones(3))
     cfg = TrainConfig(iterations=24, loss="l2", n_init=16, seed=0)
     scene, grid, rep = tomo.reconstruct(projs, cfg, resolution=20, reference=ref)
+    scene2, _, rep2 = tomo.reconstruct(projs, cfg, resolution=20, reference=ref)
+    assert rep2["losses"] == rep["losses"]          # deterministic adjoint (default)
     assert not rep["diverged"] and rep["final_count"] == 16 == scene.n
     # measured on B200: losses 1e-6 relative, primitives <= 1.5e-5, psnr 4e-6
     np.testing.assert_allclose(rep["losses"], d["losses"], rtol=1e-4)
@@ -906,6 +917,33 @@ def test_reconstruct_follows_reference():
     assert rep["ssim_3d"] == pytest.approx(float(d["ssim_3d"]), abs=1e-5)
     with pytest.raises(ValueError):
         tomo.reconstruct(projs[:1], cfg)
+
+
+def test_reconstruct_mixed_loss_follows_reference():
+    """tomo.reconstruct with the reference's default loss, mixed (0.8 L1 +
+    0.2 D-SSIM, grad.py:338-358): the loss is formed on the device image by
+    grad.loss_and_grad and pulled back through the explicit-gradient adjoint;
+    loss curve, final primitives and voxel grid against the reference's own
+    run (make_golden_recon.py), and two runs are bitwise identical
+    (deterministic adjoint, the default)."""
+    from paper_2412_03378_b200 import tomo
+    from paper_2412_03378_b200.optim import TrainConfig
+    d, projs = _recon_golden()
+    ref = tomo.DensityGrid(d["ref_grid"], -np.ones(3), np.ones(3))
+    cfg = TrainConfig(iterations=24, n_init=16, seed=0)
+    assert cfg.loss.kind == "mixed"
+    scene, grid, rep = tomo.reconstruct(projs, cfg, resolution=20, reference=ref)
+    assert not rep["diverged"]
+    np.testing.assert_allclose(rep["losses"], d["mixed_losses"], rtol=1e-4)
+    for k in ("means", "scales", "rotations", "thetas"):
+        np.testing.assert_allclose(getattr(scene, k).cpu().numpy(), d[f"mixed_final_{k}"], rtol=1e-4,
+                                   atol=1e-4, err_msg=k)
+    np.testing.assert_allclose(grid.values, d["mixed_grid"], rtol=1e-4, atol=1e-4 * d["mixed_grid"].max())
+    assert rep["psnr_3d"] == pytest.approx(float(d["mixed_psnr_3d"]), abs=1e-3)
+    scene2, _, rep2 = tomo.reconstruct(projs, cfg, resolution=20, reference=ref)
+    assert rep2["losses"] == rep["losses"]
+    for k in ("means", "scales", "rotations", "thetas"):
+        assert np.array_equal(getattr(scene2, k).cpu().numpy(), getattr(scene, k).cpu().numpy()), k
 
 
 def test_pipelined_step_is_stable_across_steps():
