@@ -74,6 +74,18 @@ class Scene:
     def __len__(self):
         return int(self.means.shape[0])
 
+    def gaussian(self, i):
+        """Primitive i as a camera.Gaussian3D (raster.py:85-89), host copies."""
+        from .camera import Gaussian3D
+
+        def host(a):
+            return a.detach().cpu().numpy().astype(np.float64) if _is_torch(a) else np.asarray(a, dtype=float)
+        op = self.splat_opacities
+        return Gaussian3D(mean=host(self.means[i]).copy(), scale=host(self.scales[i]).copy(),
+                          rotation=host(self.rotations[i]).copy(), theta=float(host(self.thetas[i])),
+                          color=host(self.colors[i]).copy(),
+                          splat_opacity=float(host(op[i])) if op is not None else 0.5)
+
     def copy(self):
         if _is_torch(self.means):
             return Scene(self.means.clone(), self.scales.clone(), self.rotations.clone(),

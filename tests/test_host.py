@@ -111,3 +111,25 @@ def test_loss_default_is_the_reference_default():
     assert vg.LossSpec().lam == float(g["default_lam"])
     from paper_2412_03378_b200.optim import TrainConfig
     assert TrainConfig().loss.kind == "mixed"
+
+
+def test_camera_helpers_and_scene_gaussian_match_reference():
+    """Camera.pixel_directions / view_to_pixel / ray_through_pixel, look_at and
+    Scene.gaussian (camera.py:50-99, raster.py:85-89) against the
+    reference's own outputs (tests/golden/make_golden_camera.py)."""
+    import os
+    from paper_2412_03378_b200.camera import look_at
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "camera.npz"))
+    cam = look_at([0.7, -1.1, -2.6], [0.1, 0.2, 0.0], up=(0.0, 1.0, 0.0), width=19, height=13,
+                  fov_x_deg=47.0)
+    np.testing.assert_array_equal(cam.rotation, g["R"])
+    np.testing.assert_array_equal(cam.translation, g["t"])
+    np.testing.assert_allclose(cam.pixel_directions(), g["dirs"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(cam.view_to_pixel(g["v"]), g["px"], rtol=1e-15, atol=1e-13)
+    ray = cam.ray_through_pixel(4, 11)
+    np.testing.assert_allclose(ray.origin, g["ray_o"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(ray.direction, g["ray_d"], rtol=0, atol=1e-15)
+    s = vg.Scene(g["s_means"], g["s_scales"], g["s_rot"], g["s_thetas"], g["s_colors"], g["s_opac"])
+    p = s.gaussian(2)
+    got = np.concatenate([p.mean, p.scale, p.rotation, [p.theta], p.color, [p.splat_opacity]])
+    np.testing.assert_array_equal(got, g["g"])
