@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tiles", type=int, default=0, help="tiles in the CPU sample (0 = auto)")
+    ap.add_argument("--no-facade", action="store_true",
+                    help="skip the drop-in facade leg (numpy render + backward of one view)")
     return ap.parse_args()
 
 
@@ -273,6 +275,59 @@ def run_gpu(args):
             "roofline": roof, "loss": loss_val,
         }
     return result
+
+
+def run_facade(args, cfg):
+    """The drop-in path a reference user calls (optim.py:379-386): numpy
+    scene in, prep = prepare(scene, cam); render(prep=prep); the L2 loss
+    gradient on the host (numpy float64, like the reference);
+    backward(prep=prep) -> float64 numpy SceneGrads.  One view of the
+    config per step with RGB colour (the reference Scene has no SH);
+    host<->device copies, float64<->float32 conversions and the per-call
+    context all inside the timed region (wall clock around synchronised
+    calls: the facade returns host arrays, so it synchronises anyway)."""
+    import torch
+    import paper_2412_03378_b200 as vgm
+    from paper_2412_03378_b200 import configs as C
+    s = cfg.scene
+    scene = vgm.Scene(s.means.astype(np.float64), s.scales.astype(np.float64),
+                      s.rotations.astype(np.float64), s.thetas.astype(np.float64),
+                      s.colors.astype(np.float64))
+    cam = cfg.cameras[0]
+    H, W = int(cam.height), int(cam.width)
+    target = cfg.target(0, (H, W, 3)).astype(np.float64)
+    stages = {"prepare": 0.0, "render": 0.0, "loss": 0.0, "backward": 0.0}
+
+    def once(acc):
+        t0 = time.perf_counter()
+        prep = vgm.prepare(scene, cam)
+        t1 = time.perf_counter()
+        out = vgm.render(scene, cam, prep=prep)
+        t2 = time.perf_counter()
+        _, d_img = vgm.loss_and_grad(out.color, target, vgm.LossSpec("l2"))
+        t3 = time.perf_counter()
+        g = vgm.backward(scene, cam, d_img, prep=prep, deterministic=False)
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+        if acc:
+            for k, a, b in (("prepare", t0, t1), ("render", t1, t2), ("loss", t2, t3), ("backward", t3, t4)):
+                stages[k] += b - a
+        return g
+    for _ in range(max(1, args.warmup)):
+        once(False)
+    n = max(1, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        g = once(True)
+    ms = (time.perf_counter() - t0) * 1e3 / n
+    del g
+    h2d = 14 * 8 * len(scene) + 3 * 8 * H * W
+    d2h = (3 + 1) * 8 * H * W + 4 * H * W + 16 * 8 * len(scene)
+    return {"value": round(H * W / (ms * 1e-3) / 1e6, 3), "unit": "Mpixels/s", "ms_per_view": round(ms, 3),
+            "stages_ms": {k: round(v * 1e3 / n, 3) for k, v in stages.items()},
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "prepare / render(prep=) / loss_and_grad (numpy) / backward(prep=, deterministic=False), "
+                   "float64 numpy in and out, one view of the config with RGB colour"}
 
 
 def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
@@ -602,6 +657,8 @@ def main():
     res = run_gpu(args)
     ws, rank, _ = dist_env()
     if rank == 0:
+        if not args.no_facade and ws == 1 and args.config != "tomography":
+            res["facade"] = run_facade(args, load_config(args.config, args.views))
         if not args.no_cpu and ws == 1:
             cfg = load_config(args.config, args.views)
             res["cpu_baseline"] = cpu_sample(cfg, args.cpu_tiles or 0, budget_s=15.0)

@@ -211,6 +211,35 @@ class Context:
 
 
 _tls = threading.local()
+_ctx_pool = {}          # device -> contexts released by collected Prep objects
+_ctx_pool_lock = threading.Lock()
+_CTX_POOL_MAX = 4
+
+
+def pooled_context(device):
+    """A context for a new Prep (raster.prepare without _ctx): one released
+    by a collected Prep if available -- its device buffers are already
+    sized, so a prepare -> render -> backward sequence per iteration (the
+    reference's optim.py:379-386 pattern) does not re-create and re-grow a
+    context every call -- else a new one.  Reuse is stream-ordered on the
+    caller's stream."""
+    with _ctx_pool_lock:
+        pool = _ctx_pool.get(int(device))
+        if pool:
+            return pool.pop()
+    return Context(device)
+
+
+def release_context(ctx):
+    """Return a Prep's context to the pool (called when the Prep is collected)."""
+    if ctx is None or not getattr(ctx, "_h", None) or not ctx._h.value:
+        return
+    with _ctx_pool_lock:
+        pool = _ctx_pool.setdefault(ctx.device, [])
+        if len(pool) < _CTX_POOL_MAX:
+            pool.append(ctx)
+            return
+    ctx.close()
 
 
 def scratch_context(device):

@@ -12,9 +12,9 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostio
 from .raster import (ALPHA_CLAMP, ALPHA_CUT, EARLY_STOP_T, TILE_SIZE, DeviceScene, _check_mode,
-                     _forward, _out, _stream, prepare)
+                     _forward, _stream, prepare)
 
 
 @dataclass
@@ -112,22 +112,37 @@ class GradBuffers:
     def to_scene_grads(self, mode, torch_out):
         n = self.n
         sg = SceneGrads(0, mode)
-        for name, _ in self.LAYOUT:
-            setattr(sg, name, _out(self.views[name], torch_out))
-        sg.d_background = _out(self.views["d_background"], torch_out)
-        vis = self.visible[:n]
-        sg.visible = vis.bool() if torch_out else vis.cpu().numpy().astype(bool)
+        if torch_out:
+            for name, _ in self.LAYOUT:
+                setattr(sg, name, self.views[name])
+            sg.d_background = self.views["d_background"]
+            sg.visible = self.visible[:n].bool()
+            if self.views["d_sh"] is not None:
+                sg.d_sh = self.views["d_sh"]
+            return sg
+        # one download of the whole flat buffer (float64 on the host), fields
+        # as views into it
+        flat = hostio.to_host(self.flat, np.float64)
+        off = 0
+        for name, w in self.LAYOUT:
+            setattr(sg, name, flat[off:off + n * w].reshape((n, w) if w > 1 else (n,)))
+            off += n * w
         if self.views["d_sh"] is not None:
-            sg.d_sh = _out(self.views["d_sh"], torch_out)
+            sg.d_sh = flat[off:off + n * 48].reshape(n, 16, 3)
+            off += n * 48
+        sg.d_background = flat[off:off + 3]
+        sg.visible = hostio.to_host(self.visible[:n], np.uint8).astype(bool)
         return sg
 
 
 def _finite_or_raise(*arrays):
+    """ValueError on a non-finite upstream gradient (grad.py:121-125); device
+    tensors are checked with one reduction on the device."""
     import torch
     for a in arrays:
         if a is None:
             continue
-        ok = bool(torch.isfinite(a).all()) if isinstance(a, torch.Tensor) else bool(np.all(np.isfinite(a)))
+        ok = hostio.all_finite(a) if isinstance(a, torch.Tensor) else bool(np.all(np.isfinite(a)))
         if not ok:
             raise ValueError("non-finite upstream pixel gradient")
 
@@ -136,7 +151,7 @@ def _dev_image(a, shape, dev):
     import torch
     if isinstance(a, torch.Tensor):
         return a.to(device=dev, dtype=torch.float32).reshape(shape).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(dev).reshape(shape)
+    return hostio.to_device(np.asarray(a), dev, shape)
 
 
 def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
@@ -149,17 +164,21 @@ def backward(scene, camera, d_color, mode="analytic", *, d_transmittance=None,
     reduces with fixed-order sums instead of float atomics: bitwise
     reproducible; False is the faster training-loop path."""
     _check_mode(mode, sort_by, tile_size)
-    _finite_or_raise(d_color, d_transmittance)
+    torch = _lib._require_cuda()
+    dev0 = prep.dscene.device if prep is not None else torch.device("cuda", torch.cuda.current_device())
+    H, W = int(camera.height), int(camera.width)
+    # the upstream gradient goes to the device first; its finiteness is then
+    # one reduction there (a host isfinite pass costs more than the upload)
+    dc = _dev_image(d_color, (H, W, 3), dev0)
+    dt = _dev_image(d_transmittance, (H, W), dev0) if d_transmittance is not None else None
+    _finite_or_raise(dc, dt)
     if prep is None:
         dscene = DeviceScene(scene)
         prep = prepare(dscene, camera, mode, tile_size, sort_by, alpha_cut,
                        _ctx=_lib.scratch_context(dscene.device.index))
     dscene = prep.dscene
     _, color, tfin, _ = _forward(prep, early_stop, alpha_cut, alpha_clamp)
-    H, W = int(camera.height), int(camera.width)
     dev = dscene.device
-    dc = _dev_image(d_color, (H, W, 3), dev)
-    dt = _dev_image(d_transmittance, (H, W), dev) if d_transmittance is not None else None
     bufs = GradBuffers(dscene.n, dev, with_sh=dscene.sh is not None)
     g = bufs.struct(accumulate=False)
     opt = _lib.make_options(TILE_SIZE, early_stop, alpha_cut, alpha_clamp, prep.alpha_cut,
@@ -217,13 +236,18 @@ def loss_and_grad(image, target, spec: LossSpec = None):
             return float((r * r).mean()), 2.0 * r / n
         l1, g1 = float(r.abs().mean()), torch.sign(r) / n
     else:
+        import torch
         x = np.asarray(image, dtype=float)
         t = np.asarray(target, dtype=float)
-        r = x - t
-        n = r.size
+        # elementwise work on torch CPU tensors sharing the numpy memory
+        # (multi-threaded: a 1080p RGB L2 gradient 40 -> a few ms)
+        r_t = torch.from_numpy(np.ascontiguousarray(x)) - torch.from_numpy(np.ascontiguousarray(t))
+        n = r_t.numel()
         if spec.kind == "l2":
-            return float(np.mean(r * r)), 2.0 * r / n
-        l1, g1 = float(np.mean(np.abs(r))), np.sign(r) / n
+            flat = r_t.reshape(-1)
+            value = float(torch.dot(flat, flat)) / n
+            return value, r_t.mul_(2.0 / n).numpy()
+        l1, g1 = float(r_t.abs().sum()) / n, torch.sign(r_t).div_(n).numpy()
     if spec.kind == "l1":
         return l1, g1
     sv, ds = metrics.ssim_with_grad(x, t)

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostio
 
 TILE_SIZE = 16            # raster.py:26
 ALPHA_CLAMP = 0.99        # raster.py:27
@@ -159,8 +159,8 @@ class DeviceScene:
             if _is_torch(a):
                 t = a.to(device=dev, dtype=torch.float32)
             else:
-                t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
-                t = t.to(dev, non_blocking=False)
+                # pinned float64 staging + a cast on the device (hostio)
+                t = hostio.to_device(np.asarray(a), dev, shape)
             return t.reshape(shape).contiguous()
 
         self.means = conv(scene.means, (n, 3))
@@ -212,6 +212,14 @@ class Prep:
         self.extent = extent
         self.fwd = None          # (flags, color, final_t, n_contrib) device tensors
         self._grid = None
+        self._pooled = False     # ctx came from _lib.pooled_context (returned on collection)
+
+    def __del__(self):
+        if getattr(self, "_pooled", False):
+            try:
+                _lib.release_context(self.ctx)
+            except Exception:
+                pass
 
     @property
     def n_tiles_x(self):
@@ -290,7 +298,7 @@ def prepare(scene, camera, mode="analytic", tile_size=TILE_SIZE, sort_by="depth"
     Returns a Prep that owns its own device context."""
     _check_mode(mode, sort_by, tile_size)
     dscene = scene if isinstance(scene, DeviceScene) else DeviceScene(scene)
-    ctx = _ctx if _ctx is not None else _lib.Context(dscene.device.index)
+    ctx = _ctx if _ctx is not None else _lib.pooled_context(dscene.device.index)
     bin_cut = alpha_cut if _bin_cut is None else _bin_cut
     opt = _options(tile_size, EARLY_STOP_T, alpha_cut, ALPHA_CLAMP, bin_cut, sort_by, mode)
     cam = _lib.make_camera(camera, _projection, _extent)
@@ -298,7 +306,9 @@ def prepare(scene, camera, mode="analytic", tile_size=TILE_SIZE, sort_by="depth"
     import ctypes
     _lib.check(_lib.load().vg_prepare(ctx.handle, ctypes.byref(s), ctypes.byref(cam),
                                       ctypes.byref(opt), _stream(dscene.device)), "vg_prepare")
-    return Prep(ctx, dscene, camera, mode, tile_size, alpha_cut, _kind, _projection, _extent)
+    prep = Prep(ctx, dscene, camera, mode, tile_size, alpha_cut, _kind, _projection, _extent)
+    prep._pooled = _ctx is None
+    return prep
 
 
 def bin_tiles(scene, camera, tile_size=TILE_SIZE, mode="analytic", sort_by="depth") -> TileGrid:
@@ -329,8 +339,7 @@ def _forward(prep, early_stop, alpha_cut, alpha_clamp):
 def _out(x, torch_in):
     if torch_in:
         return x
-    a = x.cpu().numpy()
-    return a.astype(np.float64) if a.dtype == np.float32 else a
+    return hostio.to_host(x, np.float64 if x.dtype.is_floating_point else np.int32)
 
 
 def render(scene, camera, mode="analytic", *, tile_size=TILE_SIZE, threads=None, sort_by="depth",

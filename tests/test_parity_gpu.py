@@ -145,7 +145,7 @@ def test_fused_l2_equals_explicit():
     color, tfin, _ = eng.forward()
     b1 = eng.new_grads(ds)
     loss = eng.backward_l2(color, tfin, tgt, b1)
-    ref_loss, dimg = vg().loss_and_grad(color.double().cpu().numpy(), d["target"])
+    ref_loss, dimg = vg().loss_and_grad(color.double().cpu().numpy(), d["target"], vg().LossSpec("l2"))
     assert float(loss) == pytest.approx(ref_loss, rel=1e-5)
     g2 = vg().backward(scene, cam, dimg)
     for f in GRAD_FIELDS:
