@@ -13,7 +13,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvolgauss_b200.so")
+# VG_LIB: an alternative build of the same library (the checking variant of
+# tools/debug_checks.py); the default is the in-tree release build
+LIB_PATH = os.environ.get("VG_LIB") or os.path.join(_HERE, "libvolgauss_b200.so")
 
 VG_OK, VG_EINVAL, VG_ECUDA, VG_ENOMEM = 0, 1, 2, 3
 VG_PINHOLE, VG_PARALLEL = 0, 1

@@ -43,17 +43,25 @@ def _newer(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False, ptxas_verbose=False):
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose=False, force=False, ptxas_verbose=False, debug=False):
+    """Compile and link the library.  debug=True builds the checking variant
+    (-DVG_DEBUG: index asserts that trap, warp-schedule jitter, guarded and
+    poisoned context buffers; tools/debug_checks.py) into
+    build/debug/libvolgauss_b200_debug.so, loaded with VG_LIB=<path>."""
+    build_dir, lib_path = BUILD, LIB
+    if debug:
+        build_dir = os.path.join(ROOT, "build", "debug")
+        lib_path = os.path.join(build_dir, "libvolgauss_b200_debug.so")
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(ROOT, "include", "volgauss_b200.h"))
     cc = nvcc()
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         if force or _newer(o, [s] + headers):
-            cmd = [cc] + ARCH + COMMON + EXTRA.get(src, []) + ["-c", s, "-o", o]
+            cmd = [cc] + ARCH + COMMON + EXTRA.get(src, []) + (["-DVG_DEBUG"] if debug else []) + ["-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((src, cmd))
@@ -71,16 +79,17 @@ def build(verbose=False, force=False, ptxas_verbose=False):
         for src, err in pool.map(run, jobs):
             if verbose and err.strip():
                 print(f"--- {src}\n{err}")
-    objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _newer(LIB, objs):
-        tmp = LIB + ".tmp"
+    objs = [os.path.join(build_dir, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _newer(lib_path, objs):
+        tmp = lib_path + ".tmp"
         cmd = [cc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv, ptxas_verbose="-v" in sys.argv))
+    print(build(verbose=True, force="--force" in sys.argv, ptxas_verbose="-v" in sys.argv,
+                debug="--debug" in sys.argv))

@@ -80,6 +80,12 @@
 
 namespace vg {
 
+// debug builds: a list entry must name a scene primitive
+__device__ __forceinline__ uint32_t chk_gid(const BlendParams& p, uint32_t gid) {
+  VG_ASSERT((int64_t)gid < p.dbg_n);
+  return gid;
+}
+
 struct __align__(16) SRec {
   float4 a;  // c1, c2, c3, cD2
   float4 b;  // P11, P21, P22, kap2
@@ -255,17 +261,20 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
   float fl0 = G.in0 ? p.cc : 1.f, fl1 = G.in1 ? p.cc : 1.f;
   int nc0 = 0, nc1 = 0, na0 = 0, na1 = 0;
   bool done = !(G.in0 || G.in1);
+  VG_ASSERT(r.x <= r.y && (int64_t)r.y <= p.dbg_pairs);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
+    VG_JITTER(p.dbg_jitter, base);
     if (__syncthreads_count(done) == NT) break;
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
       if (i < r.y)
-        smask[sidx] = (uint8_t)stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT, p.ecut, sdmax);
+        smask[sidx] = (uint8_t)stage(sm, sidx, rec, chk_gid(p, vals[i]), tx * TILE, ty * TILE, CUT, p.ecut, sdmax);
     }
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);
     const int jb = (int)(base - r.x) + 1;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
+      VG_JITTER(p.dbg_jitter, base + c + 1);
       const bool vb = (c + lane < nb) && ((smask[c + lane] >> warp) & 1);
       unsigned bits = __ballot_sync(FULL, vb);
       unsigned seen = 0;  // entries of this chunk with a visible pixel in this warp's block
@@ -311,11 +320,13 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
+        VG_ASSERT(k < nb);
         const SRec s = sm[k];
         const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
         if (bits) {
           const int kb = c + __ffs(bits) - 1;
           bits &= bits - 1;
+          VG_ASSERT(kb < nb);
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
           composite(k, s, e);
@@ -332,6 +343,7 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         const uint32_t g = base + c;
         uint32_t* row = vmask + (size_t)warp * vm_words + (g >> 5);
         const uint32_t sh = g & 31u;
+        VG_ASSERT((int)(g >> 5) + (sh ? 1 : 0) < vm_words);
         atomicOr(row, seen << sh);
         if (sh) atomicOr(row + 1, seen >> (32u - sh));
       }
@@ -530,6 +542,7 @@ __device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, cons
   // one shared-memory pass for both entries (all-zero sums are not stored)
   if (!(ra.flush || rb.flush)) return;
   const uint32_t ga = __float_as_uint(sa.c.w), gb = __float_as_uint(sb.c.w);
+  VG_ASSERT((int64_t)ga < p.dbg_n && (int64_t)gb < p.dbg_n);
   if (lane == 0 && ra.any_vis) io.visible[ga] = 1;
   if (lane == 0 && rb.any_vis) io.visible[gb] = 1;
   const F2 xs = smem_reduce13x2p(va, vb, lane, wb);
@@ -591,6 +604,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   // Gaussian-major slots: the staging put entry k's (Gaussian, tile) index in sm[k].d.w
   auto dslot = [&](uint32_t pos, const SRec& s, int k) -> size_t {
     if (!DET) return 0;
+    VG_ASSERT((int64_t)pos < p.dbg_pairs);
     if (io.det_gvis4) return (size_t)__float_as_uint(s.d.w) * (NT / 32) + warp;
     return (size_t)pos * (NT / 32) + warp;
   };
@@ -604,7 +618,9 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   }
 #endif
   const uint32_t* vrow = vmask ? vmask + (size_t)warp * vm_words : nullptr;
+  VG_ASSERT(r.x <= r.y && (int64_t)r.y <= p.dbg_pairs);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
+    VG_JITTER(p.dbg_jitter, base);
     if (__syncthreads_count(done) == NT) break;
 #if VG_BWD_PREF
 #pragma unroll
@@ -617,7 +633,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       const uint32_t i = base + sidx;
       if (i < r.y) {
-        const uint32_t m = stage(sm, sidx, rec, vals[i], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
+        const uint32_t m = stage(sm, sidx, rec, chk_gid(p, vals[i]), tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
 #endif
         if (!vmask) smask[sidx] = (uint8_t)m;
         if (DET && io.det_gvis4) {
@@ -627,6 +643,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           const ushort4 q = io.det_rect[gid];
           const uint32_t ps = io.det_off[gid] + (uint32_t)(ty - q.y) * (uint32_t)(q.z - q.x + 1) +
                               (uint32_t)(tx - q.x);
+          VG_ASSERT((int64_t)ps < p.dbg_pairs);
           sm[sidx].d.w = __uint_as_float(ps);
           uint32_t v = 0;
 #pragma unroll
@@ -648,6 +665,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
     // visibility word of the first chunk (lane l: entry base + l)
     uint32_t vwn = (vrow && lane < nb) ? __ldg(vrow + ((base + lane) >> 5)) : 0u;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
+      VG_JITTER(p.dbg_jitter, base + c + 1);
       unsigned bits;
       if (vmask) {
         // exact: the entries where the forward saw a visible pixel in this block
@@ -673,11 +691,13 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
+        VG_ASSERT(k < nb);
         const SRec s = sm[k];
         const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
         if (bits) {
           const int kb = c + __ffs(bits) - 1;
           bits &= bits - 1;
+          VG_ASSERT(kb < nb);
           const SRec sb = sm[kb];
           const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
 #if VG_BWD_PAIR

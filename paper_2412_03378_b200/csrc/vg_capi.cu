@@ -158,12 +158,41 @@ struct ProfScope {
   }
 };
 
+#ifdef VG_DEBUG
+// Debug builds: every context buffer is allocated with exactly the requested
+// size between two 4 KB guard bands, and the whole allocation is poisoned
+// with 0xA5 bytes (reads of never-written memory then give NaN-like garbage
+// that the parity checks see); vg_debug_guard_check finds writes past
+// either end.
+constexpr size_t VG_GUARD = 4096;
+static int buf_alloc(Buf& b, size_t bytes, cudaStream_t st) {
+  char* base = nullptr;
+  VG_CUDA(cudaMallocAsync((void**)&base, bytes + 2 * VG_GUARD, st));
+  VG_CUDA(cudaMemsetAsync(base, 0xA5, bytes + 2 * VG_GUARD, st));
+  b.p = base + VG_GUARD;
+  b.bytes = bytes;
+  return VG_OK;
+}
+static void* buf_base(const Buf& b) { return (char*)b.p - VG_GUARD; }
+#else
+static int buf_alloc(Buf& b, size_t bytes, cudaStream_t st) {
+  VG_CUDA(cudaMallocAsync(&b.p, bytes, st));
+  b.bytes = bytes;
+  return VG_OK;
+}
+static void* buf_base(const Buf& b) { return b.p; }
+#endif
+
 static int ensure(Buf& b, size_t bytes, cudaStream_t st, bool zero = false) {
+#ifdef VG_DEBUG
+  if (b.bytes == bytes && b.p) return VG_OK;  // exact sizes: the guards sit at the used end
+  const size_t want = bytes;
+#else
   if (b.bytes >= bytes && b.p) return VG_OK;
-  if (b.p) VG_CUDA(cudaFreeAsync(b.p, st));
-  size_t want = bytes + bytes / 4 + 256;
-  VG_CUDA(cudaMallocAsync(&b.p, want, st));
-  b.bytes = want;
+  const size_t want = bytes + bytes / 4 + 256;
+#endif
+  if (b.p) VG_CUDA(cudaFreeAsync(buf_base(b), st));
+  { const int _r = buf_alloc(b, want, st); if (_r != VG_OK) return _r; }
   if (zero) VG_CUDA(cudaMemsetAsync(b.p, 0, want, st));
   return VG_OK;
 }
@@ -212,17 +241,20 @@ int vg_create(vg_context** out, int32_t device) {
   return VG_OK;
 }
 
-void vg_destroy(vg_context* c) {
-  if (!c) return;
-  cudaSetDevice(c->device);
-  cudaDeviceSynchronize();
-  Buf* all[] = {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
+static std::vector<Buf*> all_bufs(vg_context* c) {
+  return {&c->rec,  &c->depth, &c->rect, &c->offset, &c->acc,
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
                 &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_gvis4, &c->det_big, &c->det_sums};
-  for (Buf* b : all)
-    if (b->p) cudaFree(b->p);
+}
+
+void vg_destroy(vg_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (Buf* b : all_bufs(c))
+    if (b->p) cudaFree(buf_base(*b));
   if (c->total_host) cudaFreeHost(c->total_host);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->count_ready) cudaEventDestroy(c->count_ready);
@@ -487,6 +519,11 @@ int vg_tile_lists(vg_context* c, int32_t* prims, int32_t* offsets, void* stream)
 
 static BlendParams blend_params(const vg_context* c) {
   BlendParams p;
+  p.dbg_n = c->scene.n;
+  p.dbg_pairs = c->pairs;
+#ifdef VG_DEBUG
+  if (const char* j = getenv("VG_DEBUG_JITTER")) p.dbg_jitter = (unsigned)atoi(j);
+#endif
   p.width = c->cam.width;
   p.height = c->cam.height;
   p.ntx = c->cam.ntx;
@@ -601,15 +638,18 @@ static int prep_grads(vg_context* c, vg_grads* g, cudaStream_t st) {
 // Grow a buffer to at least `bytes`, keeping its contents (stream ordered).
 static int grow_keep(Buf& b, size_t bytes, cudaStream_t st) {
   if (b.bytes >= bytes && b.p) return VG_OK;
-  size_t want = bytes * 2 + 256;
-  void* p = nullptr;
-  VG_CUDA(cudaMallocAsync(&p, want, st));
+#ifdef VG_DEBUG
+  const size_t want = bytes;
+#else
+  const size_t want = bytes * 2 + 256;
+#endif
+  Buf nb;
+  VG_TRY(buf_alloc(nb, want, st));
   if (b.p) {
-    VG_CUDA(cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, st));
-    VG_CUDA(cudaFreeAsync(b.p, st));
+    VG_CUDA(cudaMemcpyAsync(nb.p, b.p, b.bytes, cudaMemcpyDeviceToDevice, st));
+    VG_CUDA(cudaFreeAsync(buf_base(b), st));
   }
-  b.p = p;
-  b.bytes = want;
+  b = nb;
   return VG_OK;
 }
 
@@ -951,5 +991,35 @@ int vg_tomo_backward_l2(vg_context* c, const float* image, const float* target, 
   if (!c || !image || !target || !loss_sum) return fail(VG_EINVAL, "vg_tomo_backward_l2: NULL argument");
   return tomo_bwd_common(c, nullptr, image, target, loss_sum, g, stream);
 }
+
+#ifdef VG_DEBUG
+// Debug builds only (not in the public header): 0 if every guard band of the
+// context's buffers still holds its 0xA5 poison, else the number of damaged
+// buffers (first index in *first_bad, in all_bufs order).  Synchronises.
+int vg_debug_guard_check(vg_context* c, int32_t* first_bad) {
+  if (!c) return -1;
+  VG_CUDA(cudaDeviceSynchronize());
+  std::vector<unsigned char> h(VG_GUARD);
+  int bad = 0, idx = 0;
+  if (first_bad) *first_bad = -1;
+  for (Buf* b : all_bufs(c)) {
+    if (b->p) {
+      for (int side = 0; side < 2; ++side) {
+        const char* g = side ? (const char*)b->p + b->bytes : (const char*)b->p - VG_GUARD;
+        VG_CUDA(cudaMemcpy(h.data(), g, VG_GUARD, cudaMemcpyDeviceToHost));
+        bool ok = true;
+        for (unsigned char x : h) ok &= x == 0xA5;
+        if (!ok) {
+          if (first_bad && *first_bad < 0) *first_bad = idx;
+          ++bad;
+          break;
+        }
+      }
+    }
+    ++idx;
+  }
+  return bad;
+}
+#endif
 
 }  // extern "C"

@@ -18,9 +18,39 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "volgauss_b200.h"
+
+// Debug builds (-DVG_DEBUG, tools/debug_checks.py; compute-sanitizer is not
+// available on the measurement pool): VG_ASSERT traps on a violated index
+// bound, VG_JITTER sleeps a hashed number of nanoseconds so that warps
+// interleave differently from run to run (a shared-memory race then shows as
+// a result that differs between jitter seeds).  Both compile to nothing in
+// the release library.
+#ifdef VG_DEBUG
+#define VG_ASSERT(cond)                                                                  \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("VG_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#define VG_JITTER(seed, salt)                                                            \
+  do {                                                                                   \
+    if (seed) {                                                                          \
+      unsigned _h = (unsigned)(seed) * 2654435761u ^ (blockIdx.x * 97u + (threadIdx.x >> 5) * 131u + \
+                                                     (unsigned)(salt) * 7919u);            \
+      _h ^= _h >> 13; _h *= 0x5bd1e995u; _h ^= _h >> 15;                                 \
+      __nanosleep(_h & 2047u);                                                           \
+    }                                                                                    \
+  } while (0)
+#else
+#define VG_ASSERT(cond) do { } while (0)
+#define VG_JITTER(seed, salt) do { } while (0)
+#endif
 
 namespace vg {
 

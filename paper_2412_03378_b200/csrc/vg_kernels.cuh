@@ -19,6 +19,9 @@ struct BlendParams {
   float e2cut;     // -log1p(-alpha_cut) log2(e): entries with e log2(e) below it are cut
   float ecut;      // culling threshold on e: -log1p(-alpha_cut) * (1 - 1e-3)
   float bg[3];
+  // debug builds only (VG_ASSERT bounds, VG_JITTER seed)
+  int64_t dbg_n = 0, dbg_pairs = 0;
+  unsigned dbg_jitter = 0;
 };
 
 struct BwdIO {
