@@ -374,12 +374,18 @@ def run_e2e(args, cfg, eng, my_views, tshape, dev, ws, step, runner):
 # per unit of the blend kernels.  Render: per evaluated pair-pixel E (an entry
 # evaluated at a pixel: 64 per (entry, 8x8 warp block) pair the kernel walks)
 # plus extra FP32 per live pair-pixel L (sum of n_contrib).  Tomography: per
-# binned pair-pixel B (pairs x 256); the parallel-beam adjoint has no 8(d)
-# figure, the cone-beam one is used.
+# binned pair-pixel B (pairs x 256): cone-beam forward 16 + 2, adjoint 45 + 2;
+# parallel-beam forward 9 + 1.  The parallel-beam adjoint has no 8(d) figure:
+# the parallel-beam forward's (every binned pair-pixel's Gaussian evaluated
+# once) is used as its lower bound.
 COSTS = {"render_fwd": {"fp32_per_E": 21, "mufu_per_E": 3, "fp32_per_L": 5},
          "render_bwd": {"fp32_per_E": 24, "mufu_per_E": 4, "fp32_per_L": 46},
-         "tomo_fwd": {"fp32_per_E": 9, "mufu_per_E": 1, "fp32_per_L": 0},
+         "tomo_fwd": {"fp32_per_E": 16, "mufu_per_E": 2, "fp32_per_L": 0},
          "tomo_bwd": {"fp32_per_E": 45, "mufu_per_E": 2, "fp32_per_L": 0}}
+COSTS_PARALLEL = {"tomo_fwd": {"fp32_per_E": 9, "mufu_per_E": 1, "fp32_per_L": 0},
+                  "tomo_bwd": {"fp32_per_E": 9, "mufu_per_E": 1, "fp32_per_L": 0,
+                               "note": "no SURVEY 8(d) figure for the parallel-beam adjoint: the "
+                                       "parallel-beam forward's per-B cost used as a lower bound"}}
 
 
 def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, mufu_peak, cfg_name):
@@ -439,7 +445,7 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
         t = ms * 1e-3 / steps
         units = U["fwd" if k.endswith("fwd") else "bwd"]
         E = px_per_unit * units
-        c = COSTS[k]
+        c = (COSTS_PARALLEL if tomo and cfg.parallel else COSTS)[k]
         fp32 = c["fp32_per_E"] * E + c["fp32_per_L"] * (0.0 if tomo else L)
         mufu = c["mufu_per_E"] * E
         alg = {"kernel": k, "ms_per_step": ms / steps, "launches_per_step": cnt / steps,
@@ -447,6 +453,7 @@ def build_roofline(prof, steps, eng, ds, cams, my_views, tomo, cfg, fp32_peak, m
                        "evaluated pair-pixels E (64 x walked (entry, 8x8 block) pairs)",
                "E_per_step": E, "L_per_step": None if tomo else L,
                "fp32_per_E": c["fp32_per_E"], "fp32_per_L": c["fp32_per_L"], "mufu_per_E": c["mufu_per_E"],
+               "cost_note": c.get("note"),
                "fp32_instr_per_step": fp32, "mufu_ops_per_step": mufu,
                "p_fp32_per_s": fp32_peak, "p_mufu_per_s": mufu_peak, "sm_clock_mhz_probed": clock_mhz}
         if fp32_peak and mufu_peak:
