@@ -61,6 +61,12 @@
 // cost more than the hidden L2 latency, so off
 #define VG_BWD_PREF 0
 #endif
+#ifndef VG_BWD_SMPTR
+// backward: an entry's colour, D and id are re-read from shared memory where
+// they are used (replay, gradient terms, flush) instead of living in
+// registers from the alpha evaluation on (shorter live ranges)
+#define VG_BWD_SMPTR 0  // A/B (serial, 16 views of config 3): 17.98 -> 18.30 ms (96 regs), 19.44 ms (80 regs): off
+#endif
 #ifndef VG_TOMO_SKIP
 // projector: (entry, column) pairs whose peak in the column is below 2^-60 of
 // the Gaussian's peak (< 1e-18 relative; far below float32 resolution) are not
@@ -92,6 +98,16 @@ struct __align__(16) SRec {
   float4 c;  // n1, n2, D|beta, gid (bits)
   float4 d;  // r, g, b, 0
 };
+
+// Shared-memory loads the compiler may neither hoist nor merge with earlier
+// loads of the same record (a fresh read at the point of use).
+__device__ __forceinline__ float4 lds_fresh4(const float4* p) {
+  float4 v;
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
 
 // Tile-relative record of Gaussian gid for the tile at pixel origin (x0, y0).
 __device__ __forceinline__ SRec make_srec(const GRec& g, uint32_t gid, int x0, int y0) {
@@ -523,10 +539,24 @@ __device__ __forceinline__ void bwd_flush(const SRec& s, const Replay& r, float 
 }
 
 template <bool CUT, bool DET>
-__device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, const SRec& sb,
+__device__ __forceinline__ void bwd_entry2(const SRec& sa0, const Pair2& ea, const SRec& sb0,
                                            const Pair2& eb, bool in0, bool in1, F2 dcr, F2 dcg, F2 dcb,
                                            F2 tot, const BlendParams& p, F2& T, F2& P, int lane,
-                                           const BwdIO& io, size_t pa, size_t pb, float* wb) {
+                                           const BwdIO& io, size_t pa, size_t pb, float* wb,
+                                           const SRec* spa = nullptr, const SRec* spb = nullptr) {
+#if VG_BWD_SMPTR
+  // the fields used after the evaluation (c: D, id; d: colour), re-read here
+  SRec sa, sb;
+  sa.c = lds_fresh4(&spa->c);
+  sa.d = lds_fresh4(&spa->d);
+  sb.c = lds_fresh4(&spb->c);
+  sb.d = lds_fresh4(&spb->d);
+  (void)sa0;
+  (void)sb0;
+#else
+  const SRec& sa = sa0;
+  const SRec& sb = sb0;
+#endif
   const Replay ra = bwd_replay<CUT>(sa, ea, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   const Replay rb = bwd_replay<CUT>(sb, eb, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   float va[16], vb[16];
@@ -704,7 +734,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           const size_t ia = dslot(base + k, s, k);
           const size_t ib = dslot(base + kb, sb, kb);
           bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                               ia, ib, wb);
+                               ia, ib, wb, &sm[k], &sm[kb]);
 #else
           const size_t ia = dslot(base + k, s, k);
           bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
