@@ -274,6 +274,9 @@ def run_gpu(args):
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "kernels": kernels,
             "roofline": roof, "loss": loss_val,
         }
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     return result
 
 

@@ -133,3 +133,21 @@ def test_camera_helpers_and_scene_gaussian_match_reference():
     p = s.gaussian(2)
     got = np.concatenate([p.mean, p.scale, p.rotation, [p.theta], p.color, [p.splat_opacity]])
     np.testing.assert_array_equal(got, g["g"])
+
+
+def test_bench_multi_gpu_launch_guard():
+    """`bench.py --gpus N` outside torchrun launches N ranks itself; without N
+    visible GPUs it reports that as a JSON error line instead of silently
+    running one rank (bench.py main)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert "error" in line and "--gpus 2" in line["error"]
