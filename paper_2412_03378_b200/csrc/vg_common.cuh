@@ -112,11 +112,15 @@ __host__ __device__ inline void quat_rotmat(const float* qf, double* R, double* 
 }
 
 // Whitening W (view -> whitened local): row i = (R_c g_i)^T / s_i, g_i = column i of R_g.
-__host__ __device__ inline void whitening(const CamK& c, const double* R, const double* s, double* W) {
+// (Record-only quantities -- the blend record and the gradient frame, not the
+// bit-exact binning -- so the float64 divisions here and below are one
+// reciprocal each and multiplies: float64 division is a long Newton sequence.)
+__host__ __device__ __forceinline__ void whitening(const CamK& c, const double* R, const double* s, double* W) {
   for (int i = 0; i < 3; ++i) {
     double g0 = R[0 * 3 + i], g1 = R[1 * 3 + i], g2 = R[2 * 3 + i];
+    const double is = 1.0 / s[i];
     for (int j = 0; j < 3; ++j)
-      W[i * 3 + j] = (c.R[j * 3 + 0] * g0 + c.R[j * 3 + 1] * g1 + c.R[j * 3 + 2] * g2) / s[i];
+      W[i * 3 + j] = (c.R[j * 3 + 0] * g0 + c.R[j * 3 + 1] * g1 + c.R[j * 3 + 2] * g2) * is;
   }
 }
 
@@ -127,11 +131,11 @@ __host__ __device__ inline void matvec3(const double* W, const double* x, double
 }
 
 // Build e1,e2 from e3 and a vector g1 (not parallel to e3); returns plane coords.
-__host__ __device__ inline void plane_basis(const double* e3, const double* g1, double* e) {
+__host__ __device__ __forceinline__ void plane_basis(const double* e3, const double* g1, double* e) {
   double k = dot3(g1, e3);
   double p[3] = {g1[0] - k * e3[0], g1[1] - k * e3[1], g1[2] - k * e3[2]};
-  double pn = sqrt(dot3(p, p));
-  double e2[3] = {p[0] / pn, p[1] / pn, p[2] / pn};
+  const double ipn = 1.0 / sqrt(dot3(p, p));
+  double e2[3] = {p[0] * ipn, p[1] * ipn, p[2] * ipn};
   double e1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
                   e2[0] * e3[1] - e2[1] * e3[0]};
   for (int j = 0; j < 3; ++j) { e[j] = e1[j]; e[3 + j] = e2[j]; e[6 + j] = e3[j]; }
@@ -139,7 +143,7 @@ __host__ __device__ inline void plane_basis(const double* e3, const double* g1, 
 
 // Per-Gaussian frame for either ray model.  Returns false when the mean is
 // not in front of the near plane (pinhole) -- such Gaussians are never binned.
-__host__ __device__ inline bool make_frame(const CamK& c, const float* mu, const float* sc,
+__host__ __device__ __forceinline__ bool make_frame(const CamK& c, const float* mu, const float* sc,
                                            const float* q, Frame& f) {
   quat_rotmat(q, f.R, nullptr);
   for (int i = 0; i < 3; ++i) f.s[i] = fmax((double)sc[i], SCALE_FLOOR);
@@ -150,13 +154,16 @@ __host__ __device__ inline bool make_frame(const CamK& c, const float* mu, const
   if (c.projection == VG_PINHOLE) {
     double z = f.v[2];
     if (!(z > c.z_near)) return false;
-    double dmu[3] = {f.v[0] / z, f.v[1] / z, 1.0};
+    const double iz = 1.0 / z;
+    double dmu[3] = {f.v[0] * iz, f.v[1] * iz, 1.0};
     double m[3];
     matvec3(W, dmu, m);
     double mn = sqrt(dot3(m, m));
-    double e3[3] = {m[0] / mn, m[1] / mn, m[2] / mn};
-    double G0[3] = {W[0] / c.fx, W[3] / c.fx, W[6] / c.fx};
-    double G1[3] = {W[1] / c.fy, W[4] / c.fy, W[7] / c.fy};
+    const double imn = 1.0 / mn;
+    double e3[3] = {m[0] * imn, m[1] * imn, m[2] * imn};
+    const double ifx = 1.0 / c.fx, ify = 1.0 / c.fy;
+    double G0[3] = {W[0] * ifx, W[3] * ifx, W[6] * ifx};
+    double G1[3] = {W[1] * ify, W[4] * ify, W[7] * ify};
     plane_basis(e3, G1, f.e);
     f.P11 = dot3(f.e, G0);
     f.P21 = dot3(f.e + 3, G0);
@@ -219,6 +226,26 @@ __host__ __device__ inline void sh_basis(const double* d, double* b) {
   b[13] = -0.4570457994644658 * x * (4 * zz - xx - yy);
   b[14] = 1.445305721320277 * z * (xx - yy);
   b[15] = -0.5900435899266435 * x * (xx - 3 * yy);
+}
+
+// the same basis in float32 with explicit FMAs (preprocess colour evaluation)
+__device__ __forceinline__ void sh_basis_f(float x, float y, float z, float* b) {
+  const float xx = x * x, yy = y * y, zz = z * z;
+  const float c1 = 0.4886025119029199f;
+  b[0] = 1.f;
+  b[1] = -c1 * y; b[2] = c1 * z; b[3] = -c1 * x;
+  b[4] = 1.0925484305920792f * x * y;
+  b[5] = -1.0925484305920792f * y * z;
+  b[6] = 0.31539156525252005f * fmaf(2.f, zz, -xx - yy);
+  b[7] = -1.0925484305920792f * x * z;
+  b[8] = 0.5462742152960396f * (xx - yy);
+  b[9] = -0.5900435899266435f * y * fmaf(3.f, xx, -yy);
+  b[10] = 2.890611442640554f * x * y * z;
+  b[11] = -0.4570457994644658f * y * fmaf(4.f, zz, -xx - yy);
+  b[12] = 0.3731763325901154f * z * fmaf(2.f, zz, -3.f * xx - 3.f * yy);
+  b[13] = -0.4570457994644658f * x * fmaf(4.f, zz, -xx - yy);
+  b[14] = 1.445305721320277f * z * (xx - yy);
+  b[15] = -0.5900435899266435f * x * fmaf(-3.f, yy, xx);
 }
 
 // ---------------------------------------------------------------------------

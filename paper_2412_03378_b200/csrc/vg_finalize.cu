@@ -349,12 +349,14 @@ __global__ void __launch_bounds__(128) k_sh_pull(int64_t n, const float* __restr
     any = true;
     double d[3] = {m[0] - centers[3 * v], m[1] - centers[3 * v + 1], m[2] - centers[3 * v + 2]};
     const double dn = sqrt(dot3(d, d));
-    d[0] /= dn; d[1] /= dn; d[2] /= dn;
-    double b[16];
-    sh_basis(d, b);
+    const double idn = 1.0 / dn;
+    d[0] *= idn; d[1] *= idn; d[2] *= idn;
+    // the basis in float32, like the preprocess colour evaluation
+    float b[16];
+    sh_basis_f((float)d[0], (float)d[1], (float)d[2], b);
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
-      const float bl = (float)b[l];
+      const float bl = b[l];
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) acc[3 * l + ch] = fmaf(bl, dc[ch], acc[3 * l + ch]);
     }
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(128) k_sh_pull(int64_t n, const float* __restr
       sh_basis_vjp(x, y, z, g, gd);
       // through d = u / |u|: (I - d d^T) gd / |u|
       const float r = gd[0] * x + gd[1] * y + gd[2] * z;
-      const float inv = (float)(1.0 / dn);
+      const float inv = (float)idn;
       dm[0] += (gd[0] - r * x) * inv;
       dm[1] += (gd[1] - r * y) * inv;
       dm[2] += (gd[2] - r * z) * inv;

@@ -19,11 +19,14 @@ struct PrepOut {
   float* frame;        // e1, e2, e3 in whitened-local coordinates (12 floats)
 };
 
+#ifndef VG_PRE_NT
+#define VG_PRE_NT 64  // threads per CTA (A/B, 16 views of config 3: 256x3 CTAs 1.96 ms, 128x5 1.86, 64x10 1.84)
+#endif
 #ifndef VG_PRE_MINB
-#define VG_PRE_MINB 3  // <= 80 registers: 3 CTAs per SM (A/B: tools/ab_bench.sh, -8%)
+#define VG_PRE_MINB 10  // <= 96 registers (80 spilled ~350 bytes per thread)
 #endif
 
-__global__ void __launch_bounds__(256, VG_PRE_MINB) k_preprocess(int64_t n, const float* __restrict__ means,
+__global__ void __launch_bounds__(VG_PRE_NT, VG_PRE_MINB) k_preprocess(int64_t n, const float* __restrict__ means,
                                                     const float* __restrict__ scales,
                                                     const float* __restrict__ rots,
                                                     const float* __restrict__ thetas,
@@ -78,9 +81,11 @@ __global__ void __launch_bounds__(256, VG_PRE_MINB) k_preprocess(int64_t n, cons
     double det = cov[0] * cov[3] - cov[1] * cov[2];
     double lam = half_tr + sqrt(fmax(half_tr * half_tr - det, 0.0));
     lam_max = lam;
-    conic[0] = cov[3] / det;
-    conic[1] = -cov[1] / det;
-    conic[2] = cov[0] / det;
+    if (opac) {  // the splat record's conic (raster._inv2x2, raster.py:212-219)
+      conic[0] = cov[3] / det;
+      conic[1] = -cov[1] / det;
+      conic[2] = cov[0] / det;
+    }
     double smax = fmax(fmax(f.s[0], f.s[1]), f.s[2]);
     double amp = SQRT_2PI * kappa * smax;
     double cut = fmax(bin_cut, 1e-12);
@@ -164,23 +169,30 @@ __global__ void __launch_bounds__(256, VG_PRE_MINB) k_preprocess(int64_t n, cons
   g.pad0 = g.pad1 = g.pad2 = 0.f;
   double rgb[3] = {0.0, 0.0, 0.0};
   if (sh) {
+    // SH-3 colour (no reference counterpart): the direction in float64, the
+    // basis and the 48-term contraction in float32 with explicit FMAs (this
+    // file is built without FMA contraction for the binning's sake; float64
+    // without FMAs made the contraction ~300 float64 operations per Gaussian)
     double d[3] = {means[3 * i] - c.center[0], means[3 * i + 1] - c.center[1],
                    means[3 * i + 2] - c.center[2]};
-    double dn = sqrt(dot3(d, d));
-    d[0] /= dn; d[1] /= dn; d[2] /= dn;
-    double b[16];
-    sh_basis(d, b);
+    const double idn = 1.0 / sqrt(dot3(d, d));
+    float b[16];
+    sh_basis_f((float)(d[0] * idn), (float)(d[1] * idn), (float)(d[2] * idn), b);
     // 192 contiguous bytes per Gaussian: 12 x 16-byte loads (not 48 scalar ones)
+    // (each loaded value is folded in at once: no 48-float array to hold)
     const float4* q4 = reinterpret_cast<const float4*>(sh + 48 * i);
-    float q[48];
+    float rf[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
       const float4 v = __ldg(q4 + k);
-      q[4 * k] = v.x; q[4 * k + 1] = v.y; q[4 * k + 2] = v.z; q[4 * k + 3] = v.w;
-    }
+      const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int l = 0; l < 16; ++l)
-      for (int ch = 0; ch < 3; ++ch) rgb[ch] += b[l] * q[l * 3 + ch];
+      for (int e = 0; e < 4; ++e) {
+        const int idx = 4 * k + e;
+        rf[idx % 3] = fmaf(b[idx / 3], vv[e], rf[idx % 3]);
+      }
+    }
+    rgb[0] = rf[0]; rgb[1] = rf[1]; rgb[2] = rf[2];
   } else if (colors) {
     rgb[0] = colors[3 * i]; rgb[1] = colors[3 * i + 1]; rgb[2] = colors[3 * i + 2];
   }
@@ -199,8 +211,8 @@ void launch_preprocess(int64_t n, const vg_scene& s, const CamK& c, double bin_c
                        cudaStream_t st) {
   if (n <= 0) return;
   PrepOut o{rec, depth, rect, gm, frame};
-  int blocks = (int)((n + 255) / 256);
-  k_preprocess<<<blocks, 256, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
+  int blocks = (int)((n + VG_PRE_NT - 1) / VG_PRE_NT);
+  k_preprocess<<<blocks, VG_PRE_NT, 0, st>>>(n, s.means, s.scales, s.rotations, s.thetas, s.colors,
                                        s.sh, splat ? s.splat_opacities : nullptr, c, bin_cut, o);
 }
 
