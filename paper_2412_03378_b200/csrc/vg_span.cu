@@ -12,7 +12,7 @@
 //   step 2  spans of a row (depth order) -> tile entries: each span emits g
 //           into the lists of tiles (y, x0..x1); each list keeps depth order.
 //
-// Both steps are the same primitive.  The items are cut into chunks of 1024
+// Both steps are the same primitive.  The items are cut into chunks of CH (512)
 // (one CTA each); item i of a chunk covers the bucket interval [lo_i, hi_i]
 // (rows in step 1, tile columns in step 2).  A chunk's stable rank of item i
 // in bucket b is the number of earlier items of the chunk covering b, read
@@ -35,7 +35,10 @@ namespace vg {
 namespace span {
 
 constexpr unsigned FULLM = 0xffffffffu;
-constexpr int CH = 1024;         // items per chunk
+#ifndef VG_SPAN_CH
+#define VG_SPAN_CH 512  // A/B (16 views of config 3, serial, scan + place): 256: 2.42, 512: 2.21, 768: 2.22, 1024: 2.32 ms
+#endif
+constexpr int CH = VG_SPAN_CH;   // items per chunk
 constexpr int CT = 256;          // threads per chunk CTA
 constexpr int WPC = CH / 32;     // bitmap words per bucket
 constexpr int BMS = WPC + 1;     // padded bitmap row stride (conflict-free prefix pass)
