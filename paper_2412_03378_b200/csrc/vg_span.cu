@@ -24,7 +24,7 @@
 // pairs, i.e. to lexsort((prim, float32(depth), tile)).
 //
 // Step 2's chunks never straddle rows: every row's span list is padded to a
-// multiple of 1024 (the padding is never read: item validity comes from the
+// multiple of CH (the padding is never read: item validity comes from the
 // row's span count).  The host reads back the pair total and the number of
 // step-2 chunks once, to size the outputs (the pipeline's one host sync).
 #include <climits>
