@@ -39,7 +39,10 @@ constexpr unsigned FULLM = 0xffffffffu;
 #define VG_SPAN_CH 512  // A/B (16 views of config 3, serial, scan + place): 256: 2.42, 512: 2.21, 768: 2.22, 1024: 2.32 ms
 #endif
 constexpr int CH = VG_SPAN_CH;   // items per chunk
-constexpr int CT = 256;          // threads per chunk CTA
+#ifndef VG_SPAN_CT
+#define VG_SPAN_CT 256
+#endif
+constexpr int CT = VG_SPAN_CT;   // threads per chunk CTA
 constexpr int WPC = CH / 32;     // bitmap words per bucket
 constexpr int BMS = WPC + 1;     // padded bitmap row stride (conflict-free prefix pass)
 constexpr int SCAN_T = 1024;     // threads of the single-CTA kernels

@@ -1246,3 +1246,28 @@ def test_device_fd_check(loss):
     frac = sum(r.within(2e-2) for r in big) / len(big)
     print(f"[fd_check {loss}] {len(big)} non-negligible records, {frac:.3f} within 2e-2, worst {rep.worst()}")
     assert frac >= 0.95
+
+
+def test_hostio_round_trips():
+    """The facade's pinned staging (hostio): float64 numpy -> float32 device
+    equals numpy's float32 rounding; downloads are exact; non-contiguous and
+    empty inputs; back-to-back transfers through the same staging buffer do
+    not overwrite each other."""
+    import torch
+    from paper_2412_03378_b200 import hostio
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(7)
+    a = rng.normal(size=(300, 7))
+    t = hostio.to_device(a[:, ::2], dev, (300, 4))      # non-contiguous view
+    assert np.array_equal(t.cpu().numpy(), a[:, ::2].astype(np.float32))
+    outs = [hostio.to_device(np.full(1000, float(k)), dev, (1000,)) for k in range(5)]
+    for k, o in enumerate(outs):
+        assert bool((o == k).all())
+    g = torch.randn(1234, device=dev)
+    h = hostio.to_host(g)
+    assert h.dtype == np.float64 and np.array_equal(h, g.double().cpu().numpy())
+    i = torch.arange(77, dtype=torch.int32, device=dev)
+    assert np.array_equal(hostio.to_host(i, np.int32), np.arange(77))
+    assert hostio.to_device(np.zeros((0, 3)), dev, (0, 3)).shape == (0, 3)
+    assert hostio.to_host(torch.zeros((0, 3), device=dev)).shape == (0, 3)
+    assert hostio.all_finite(g) and not hostio.all_finite(g / 0.0)
