@@ -277,10 +277,12 @@ def test_full_size_medium_all_views():
 
 def test_full_size_opaque_view():
     """Config 4 (N=500k flattened disks, kappa 20-200, 1024x1024): early
-    termination on most pixels."""
+    termination on most pixels; three views (a side, top and oblique one)."""
     from paper_2412_03378_b200 import configs
     cfg = configs.opaque()
-    _full_size_check(_f64_scene(cfg.scene), cfg.cameras[3], seed=7)
+    scene = _f64_scene(cfg.scene)
+    for v, seed in ((3, 7), (11, 8), (26, 9)):
+        _full_size_check(scene, cfg.cameras[v], n_random=3, seed=seed, n_busy=2)
 
 
 def test_full_size_tomography_parallel_view():
