@@ -23,10 +23,17 @@ LIB = os.path.join(PKG, "libvolgauss_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-# per-file extra flags: preprocess rounds like numpy float64 (no FMA contraction)
-EXTRA = {"vg_preprocess.cu": ["-fmad=false"]}
-SOURCES = ["vg_preprocess.cu", "vg_radix.cu", "vg_span.cu", "vg_gamma.cu", "vg_blend.cu", "vg_splat.cu", "vg_finalize.cu",
-           "vg_capi.cu", "vg_probe.cu", "vg_optim.cu", "vg_det.cu", "vg_raymarch.cu", "vg_voxel.cu", "vg_comm.cu"]
+# translation units: (object, source, extra flags).  Preprocess rounds like
+# numpy float64 (no FMA contraction); vg_blend.cu is split in two units so
+# the forward kernel gets its own ptxas register-usage level (vg_blend.cu).
+UNITS = [("vg_preprocess", "vg_preprocess.cu", ["-fmad=false"]), ("vg_radix", "vg_radix.cu", []),
+         ("vg_span", "vg_span.cu", []), ("vg_gamma", "vg_gamma.cu", []),
+         ("vg_blend_fwd", "vg_blend.cu", ["-DVG_TU=1", "-Xptxas", "-regUsageLevel=6"]),
+         ("vg_blend", "vg_blend.cu", ["-DVG_TU=2"]), ("vg_splat", "vg_splat.cu", []),
+         ("vg_finalize", "vg_finalize.cu", []), ("vg_capi", "vg_capi.cu", []), ("vg_probe", "vg_probe.cu", []),
+         ("vg_optim", "vg_optim.cu", []), ("vg_det", "vg_det.cu", []), ("vg_raymarch", "vg_raymarch.cu", []),
+         ("vg_voxel", "vg_voxel.cu", []), ("vg_comm", "vg_comm.cu", [])]
+SOURCES = sorted({src for _, src, _ in UNITS})
 
 
 def nvcc():
@@ -57,11 +64,11 @@ def build(verbose=False, force=False, ptxas_verbose=False, debug=False):
     headers.append(os.path.join(ROOT, "include", "volgauss_b200.h"))
     cc = nvcc()
     jobs = []
-    for src in SOURCES:
+    for obj, src, extra in UNITS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(build_dir, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, obj + ".o")
         if force or _newer(o, [s] + headers):
-            cmd = [cc] + ARCH + COMMON + EXTRA.get(src, []) + (["-DVG_DEBUG"] if debug else []) + ["-c", s, "-o", o]
+            cmd = [cc] + ARCH + COMMON + extra + (["-DVG_DEBUG"] if debug else []) + ["-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((src, cmd))
@@ -79,7 +86,7 @@ def build(verbose=False, force=False, ptxas_verbose=False, debug=False):
         for src, err in pool.map(run, jobs):
             if verbose and err.strip():
                 print(f"--- {src}\n{err}")
-    objs = [os.path.join(build_dir, s.replace(".cu", ".o")) for s in SOURCES]
+    objs = [os.path.join(build_dir, obj + ".o") for obj, _, _ in UNITS]
     if force or jobs or _newer(lib_path, objs):
         tmp = lib_path + ".tmp"
         cmd = [cc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-ldl"]

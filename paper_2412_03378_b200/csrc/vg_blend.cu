@@ -34,6 +34,21 @@
 // red.global.add per warp and entry.
 #include "vg_blend.cuh"
 
+// The file is compiled twice (build.py): VG_TU=1 holds the forward kernel
+// (built with ptxas -regUsageLevel=6: forward -2.3 % on config 3, -4.3 % on
+// config 4; the same level makes the backward 0.8 % slower), VG_TU=2 the rest.
+// Without VG_TU everything is built (tools, A/B builds).
+#if !defined(VG_TU) || VG_TU == 1
+#define VG_TU_FWD 1
+#else
+#define VG_TU_FWD 0
+#endif
+#if !defined(VG_TU) || VG_TU == 2
+#define VG_TU_REST 1
+#else
+#define VG_TU_REST 0
+#endif
+
 // minimum resident CTAs per SM requested from ptxas (register budget); A/B knobs
 #ifndef VG_FWD_MINB
 #define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
@@ -239,6 +254,7 @@ __device__ __forceinline__ float pixel_lp(const BlendParams& p, int col, int row
   return 0.5f * lg2f(fmaf(X, X, fmaf(Y, Y, 1.f)));
 }
 
+#if VG_TU_FWD
 // ---------------------------------------------------------------------------
 // K5 forward blend (raster.render)
 
@@ -400,6 +416,9 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
   }
 }
 
+#endif  // VG_TU_FWD
+
+#if VG_TU_REST
 // ---------------------------------------------------------------------------
 // per-pair gradient terms (shared by the render and cone-beam backward):
 // fills v[0..9] with the two pixels' sum of h (rho rho^T + w^ w^T), h rho, h.
@@ -1119,9 +1138,12 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
   }
 }
 
+#endif  // VG_TU_REST
+
 // ---------------------------------------------------------------------------
 // launchers
 
+#if VG_TU_FWD
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
@@ -1144,7 +1166,9 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
   else VG_RF(false, false);
 #undef VG_RF
 }
+#endif  // VG_TU_FWD
 
+#if VG_TU_REST
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
                        const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
@@ -1203,8 +1227,10 @@ void launch_tomo_bwd(int n_tiles, int splits, int ray, int loss, const GRec* rec
 #undef VG_TB
 }
 
+#endif  // VG_TU_REST
 }  // namespace vg
 
+#if VG_TU_FWD
 namespace vg {
 // Debug statistics of one forward pass: {processed warp-entries, of which any
 // pixel had alpha > 0, list entries walked per warp}.  Not on the hot path.
@@ -1220,3 +1246,4 @@ int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, cons
   return (int)cudaGetLastError();
 }
 }  // namespace vg
+#endif  // VG_TU_FWD

@@ -11,7 +11,8 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 FILE=${FILE:-vg_blend.cu}
 objs=$(ls build/csrc/*.o)
 for f in $FILE; do
-  objs=$(echo "$objs" | grep -v "/${f%.cu}.o")
+  # every unit built from this source (vg_blend.cu -> vg_blend.o, vg_blend_fwd.o)
+  objs=$(echo "$objs" | grep -v "/${f%.cu}\(_[a-z]*\)\?\.o")
 done
 while [ $# -gt 0 ]; do
   name=$1; flags=$2; shift 2
