@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build library variants for tools/ab_bench.sh:
-#   [FILE="vg_blend.cu [vg_x.cu ...]"] tools/build_ab.sh name "-DVG_FWD_MINB=8 ..." [name2 "flags2" ...]
+#   [FILE="vg_blend.cu [vg_x.cu ...]"] [KEEP="build/csrc/x.o ..."] tools/build_ab.sh name "-DVG_FWD_MINB=8 ..." [name2 "flags2" ...]
 # Every file in FILE is recompiled with the variant's flags; the other objects
 # come from the regular build.
 set -e
@@ -24,5 +24,5 @@ while [ $# -gt 0 ]; do
       -Xptxas -v 2>&1 | grep -E "registers" | head -4 | sed "s/^/$name: /"
     vobjs="$vobjs $o"
   done
-  nvcc $ARCH -shared -cudart static -o build/ab/$name.so $objs $vobjs
+  nvcc $ARCH -shared -cudart static -o build/ab/$name.so $objs $vobjs $KEEP
 done
