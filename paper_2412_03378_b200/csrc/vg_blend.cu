@@ -69,19 +69,6 @@
 // 18.9 ms; packed pass 17.65 -> 17.28 ms)
 #define VG_BWD_PAIR 2
 #endif
-#ifndef VG_BWD_PREF
-// backward: load the next batch's list entries and the next chunk's
-// visibility words one step ahead.  A/B (serial, 16 views of config 3):
-// 17.98 -> 18.41 ms (+2.4 %; config 4 -0.8 %): the two extra live registers
-// cost more than the hidden L2 latency, so off
-#define VG_BWD_PREF 0
-#endif
-#ifndef VG_BWD_SMPTR
-// backward: an entry's colour, D and id are re-read from shared memory where
-// they are used (replay, gradient terms, flush) instead of living in
-// registers from the alpha evaluation on (shorter live ranges)
-#define VG_BWD_SMPTR 0  // A/B (serial, 16 views of config 3): 17.98 -> 18.30 ms (96 regs), 19.44 ms (80 regs): off
-#endif
 #ifndef VG_TOMO_SKIP
 // projector: (entry, column) pairs whose peak in the column is below 2^-60 of
 // the Gaussian's peak (< 1e-18 relative; far below float32 resolution) are not
@@ -113,16 +100,6 @@ struct __align__(16) SRec {
   float4 c;  // n1, n2, D|beta, gid (bits)
   float4 d;  // r, g, b, 0
 };
-
-// Shared-memory loads the compiler may neither hoist nor merge with earlier
-// loads of the same record (a fresh read at the point of use).
-__device__ __forceinline__ float4 lds_fresh4(const float4* p) {
-  float4 v;
-  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
 
 // Tile-relative record of Gaussian gid for the tile at pixel origin (x0, y0).
 __device__ __forceinline__ SRec make_srec(const GRec& g, uint32_t gid, int x0, int y0) {
@@ -558,24 +535,10 @@ __device__ __forceinline__ void bwd_flush(const SRec& s, const Replay& r, float 
 }
 
 template <bool CUT, bool DET>
-__device__ __forceinline__ void bwd_entry2(const SRec& sa0, const Pair2& ea, const SRec& sb0,
+__device__ __forceinline__ void bwd_entry2(const SRec& sa, const Pair2& ea, const SRec& sb,
                                            const Pair2& eb, bool in0, bool in1, F2 dcr, F2 dcg, F2 dcb,
                                            F2 tot, const BlendParams& p, F2& T, F2& P, int lane,
-                                           const BwdIO& io, size_t pa, size_t pb, float* wb,
-                                           const SRec* spa = nullptr, const SRec* spb = nullptr) {
-#if VG_BWD_SMPTR
-  // the fields used after the evaluation (c: D, id; d: colour), re-read here
-  SRec sa, sb;
-  sa.c = lds_fresh4(&spa->c);
-  sa.d = lds_fresh4(&spa->d);
-  sb.c = lds_fresh4(&spb->c);
-  sb.d = lds_fresh4(&spb->d);
-  (void)sa0;
-  (void)sb0;
-#else
-  const SRec& sa = sa0;
-  const SRec& sb = sb0;
-#endif
+                                           const BwdIO& io, size_t pa, size_t pb, float* wb) {
   const Replay ra = bwd_replay<CUT>(sa, ea, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   const Replay rb = bwd_replay<CUT>(sb, eb, in0, in1, dcr, dcg, dcb, tot, p, T, P);
   float va[16], vb[16];
@@ -657,33 +620,15 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
     if (io.det_gvis4) return (size_t)__float_as_uint(s.d.w) * (NT / 32) + warp;
     return (size_t)pos * (NT / 32) + warp;
   };
-#if VG_BWD_PREF
-  constexpr int PER = BATCH / NT;
-  uint32_t pv[PER];  // this thread's list entries of the next batch to stage
-#pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const uint32_t i = r.x + threadIdx.x + j * NT;
-    pv[j] = i < r.y ? vals[i] : 0u;
-  }
-#endif
   const uint32_t* vrow = vmask ? vmask + (size_t)warp * vm_words : nullptr;
   VG_ASSERT(r.x <= r.y && (int64_t)r.y <= p.dbg_pairs);
   for (uint32_t base = r.x; base < r.y; base += BATCH) {
     VG_JITTER(p.dbg_jitter, base);
     if (__syncthreads_count(done) == NT) break;
-#if VG_BWD_PREF
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int sidx = threadIdx.x + j * NT;
-      const uint32_t i = base + sidx;
-      if (i < r.y) {
-        const uint32_t m = stage(sm, sidx, rec, pv[j], tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
-#else
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       const uint32_t i = base + sidx;
       if (i < r.y) {
         const uint32_t m = stage(sm, sidx, rec, chk_gid(p, vals[i]), tx * TILE, ty * TILE, CUT && !vmask, p.ecut);
-#endif
         if (!vmask) smask[sidx] = (uint8_t)m;
         if (DET && io.det_gvis4) {
           // this entry's (Gaussian, tile) index within the Gaussian's tile
@@ -702,17 +647,8 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         }
       }
     }
-#if VG_BWD_PREF
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const uint32_t i = base + BATCH + threadIdx.x + j * NT;
-      pv[j] = i < r.y ? vals[i] : 0u;
-    }
-#endif
     __syncthreads();
     const int nb = min((uint32_t)BATCH, r.y - base);
-    // visibility word of the first chunk (lane l: entry base + l)
-    uint32_t vwn = (vrow && lane < nb) ? __ldg(vrow + ((base + lane) >> 5)) : 0u;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
       VG_JITTER(p.dbg_jitter, base + c + 1);
       unsigned bits;
@@ -723,12 +659,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
         // divergence bookkeeping: backward -6 % on config 3, -12 % on config 4
         // against extracting the 32 bits from the mask words per lane)
         const uint32_t g = base + c + lane;
-#if VG_BWD_PREF
-        const uint32_t vw = vwn;
-        if (c + 32 + lane < nb) vwn = __ldg(vrow + ((g + 32) >> 5));
-#else
         const uint32_t vw = __ldg(vrow + (g >> 5));
-#endif
         const bool vb = (c + lane < nb) && ((vw >> (g & 31u)) & 1u);
         bits = __ballot_sync(FULL, vb);
       } else {
@@ -753,7 +684,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           const size_t ia = dslot(base + k, s, k);
           const size_t ib = dslot(base + kb, sb, kb);
           bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                               ia, ib, wb, &sm[k], &sm[kb]);
+                               ia, ib, wb);
 #else
           const size_t ia = dslot(base + k, s, k);
           bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
