@@ -383,6 +383,18 @@ int vg_allreduce_grads(vg_context* ctx, void* nccl_comm, float* flat, int64_t co
 int vg_debug_forward_stats(vg_context* ctx, float* color, float* final_t, int32_t* n_contrib,
                            unsigned long long* out4, void* stream);
 
+/* Diagnostic (load balance, tools/walk_stats.py): while log != NULL, every
+ * forward / backward blend launch of this context writes, for CTA b < n,
+ * {start ns, end ns, (SM id << 32) | tile} (globaltimer) to the device buffer
+ * log[3 b .. 3 b + 2].  log = NULL turns it off. */
+int vg_debug_cta_log(vg_context* ctx, unsigned long long* log, int n);
+
+/* Diagnostic: the segmented backward's plan for the last forward of this
+ * context -- *segmented = 1 if its backward runs (tile, segment) work items
+ * (vg_kernels.cuh, SegIO), *items = their count (else 0, one CTA per tile).
+ * Synchronises the device. */
+int vg_debug_segments(vg_context* ctx, int64_t* items, int32_t* segmented);
+
 /* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and
  * MUFU ex2 ops/s over all SMs of `device`. */
 int vg_probe_peaks(int32_t device, double* fp32_per_s, double* mufu_per_s);

@@ -109,6 +109,8 @@ EXPORTS = {
                               C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vg_debug_forward_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
+    "vg_debug_cta_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "vg_debug_segments": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "vg_nccl_available": (C.c_int, []),
     "vg_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "vg_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32, C.c_int32]),

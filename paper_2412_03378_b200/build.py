@@ -51,15 +51,23 @@ def _newer(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False, ptxas_verbose=False, debug=False):
+def build(verbose=False, force=False, ptxas_verbose=False, debug=False, profile=False):
     """Compile and link the library.  debug=True builds the checking variant
     (-DVG_DEBUG: index asserts that trap, warp-schedule jitter, guarded and
     poisoned context buffers; tools/debug_checks.py) into
-    build/debug/libvolgauss_b200_debug.so, loaded with VG_LIB=<path>."""
+    build/debug/libvolgauss_b200_debug.so, loaded with VG_LIB=<path>;
+    profile=True the variant with the per-CTA launch log (-DVG_CTA_LOG=1,
+    vg_debug_cta_log; tools/walk_stats.py) into build/prof/."""
     build_dir, lib_path = BUILD, LIB
+    variant = []
     if debug:
         build_dir = os.path.join(ROOT, "build", "debug")
         lib_path = os.path.join(build_dir, "libvolgauss_b200_debug.so")
+        variant = ["-DVG_DEBUG"]
+    elif profile:
+        build_dir = os.path.join(ROOT, "build", "prof")
+        lib_path = os.path.join(build_dir, "libvolgauss_b200_prof.so")
+        variant = ["-DVG_CTA_LOG=1"]
     os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(ROOT, "include", "volgauss_b200.h"))
@@ -69,7 +77,7 @@ def build(verbose=False, force=False, ptxas_verbose=False, debug=False):
         s = os.path.join(CSRC, src)
         o = os.path.join(build_dir, obj + ".o")
         if force or _newer(o, [s] + headers):
-            cmd = [cc] + ARCH + COMMON + extra + (["-DVG_DEBUG"] if debug else []) + ["-c", s, "-o", o]
+            cmd = [cc] + ARCH + COMMON + extra + variant + ["-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((src, cmd))

@@ -56,12 +56,6 @@
 #ifndef VG_SEEN_REDUX
 #define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
 #endif
-#ifndef VG_BWD_MINB
-// 5: <= 96 registers.  With the cut decided on e (eval_pinhole2) the 80-register
-// budget of 6 CTAs spilled: config 3, 16 views, serial: 6 -> 19.26 ms,
-// 5 -> 18.01 ms, 4 -> 19.26 ms
-#define VG_BWD_MINB 5
-#endif
 #ifndef VG_BWD_PAIR
 // two visible entries per step: 1 = both replays, then both entries' gradient
 // terms, two reductions; 2 = the same with one shared-memory pass for both,
@@ -249,8 +243,10 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
                                                    float* __restrict__ final_t,
                                                    int* __restrict__ n_contrib,
                                                    int* __restrict__ n_act,
-                                                   uint32_t* __restrict__ vmask, int vm_words) {
+                                                   uint32_t* __restrict__ vmask, int vm_words,
+                                                   SegIO seg) {
   unsigned long long st_proc = 0, st_vis = 0, st_tot = 0;
+  cta_log_begin(p);
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   __shared__ float sdmax[4];
@@ -271,9 +267,18 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
   int nc0 = 0, nc1 = 0, na0 = 0, na1 = 0;
   bool done = !(G.in0 || G.in1);
   VG_ASSERT(r.x <= r.y && (int64_t)r.y <= p.dbg_pairs);
-  for (uint32_t base = r.x; base < r.y; base += BATCH) {
+  // after the loop, min(base, r.y) is the end of the last batch walked (the
+  // tile's depth)
+  uint32_t base = r.x;
+  for (; base < r.y; base += BATCH) {
     VG_JITTER(p.dbg_jitter, base);
     if (__syncthreads_count(done) == NT) break;
+    if (seg.on && base != r.x && ((base - r.x) & (VG_SEG - 1)) == 0) {
+      // a segment boundary: the state the backward's replay of the next segment starts from
+      float4* o = seg.state + ((size_t)(base / VG_SEG) * NT + threadIdx.x) * 2;
+      o[0] = make_float4(lo(T), hi(T), lo(Cr), hi(Cr));
+      o[1] = make_float4(lo(Cg), hi(Cg), lo(Cb), hi(Cb));
+    }
     for (int sidx = threadIdx.x; sidx < BATCH; sidx += NT) {
       uint32_t i = base + sidx;
       if (i < r.y)
@@ -364,6 +369,33 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
     atomicAdd(&g_vg_stats[0], st_proc);
     atomicAdd(&g_vg_stats[1], st_vis);
     atomicAdd(&g_vg_stats[2], st_tot);
+  }
+  if (VG_CTA_LOG) cta_log_end(p, tile);
+  if (seg.counts && threadIdx.x == 0) {
+    // this view's depth statistics (the next view's decision: seg_publish)
+    const uint32_t d = min(base, r.y) - r.x;
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(seg.counts + SEG_STATS);
+    atomicAdd(st, (unsigned long long)d);
+    atomicMax(st + 1, (unsigned long long)d);
+  }
+  if (seg.on && threadIdx.x == 0) {
+    // this tile's backward items (a tile that walked nothing still gets its
+    // item: the pixel terms)
+    const uint32_t d = min(base, r.y) - r.x;
+    const uint32_t t = order[blockIdx.x];
+    uint32_t ns = d > seg.thr ? (d + VG_SEG - 1) / VG_SEG : 1u;
+    if (ns > 1 && atomicAdd(seg.counts + SEG_BINS, ns - 1) + (ns - 1) > seg.budget) ns = 1;
+    if (ns == 1) {
+      const int b = seg_bin(d);
+      const uint32_t o = atomicAdd(seg.counts + b, 1u);
+      seg.items[(size_t)b * seg.cap + o] = make_uint2(t, SEG_WHOLE);
+    } else {
+      for (uint32_t k = 0; k < ns; ++k) {
+        const int b = seg_bin(min((uint32_t)VG_SEG, d - k * VG_SEG));
+        const uint32_t o = atomicAdd(seg.counts + b, 1u);
+        seg.items[(size_t)b * seg.cap + o] = make_uint2(t, k);
+      }
+    }
   }
   const int len = (int)(r.y - r.x);
   if (!STOP || lo(T) >= p.stop) na0 = len;
@@ -590,12 +622,38 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
                                                    const uint32_t* __restrict__ order,
                                                    BlendParams p, BwdIO io,
                                                    const uint32_t* __restrict__ vmask,
-                                                   int vm_words) {
+                                                   int vm_words, SegIO seg) {
+  cta_log_begin(p);
   __shared__ SRec sm[BATCH];
   __shared__ uint8_t smask[BATCH];
   __shared__ __align__(16) float sred[NT / 32][VG_BWD_PAIR == 2 ? (REDP_WORDS > RED_WORDS ? REDP_WORDS : RED_WORDS)
                                                : VG_SMEM_RED ? RED_WORDS : 4];
-  const int tile = order[blockIdx.x];
+  // segmented: item = (tile, segment k), entries [r.x + k VG_SEG, + VG_SEG)
+  int tile;
+  uint32_t ks = SEG_WHOLE;
+  if (!DET && seg.on) {
+    // CTA b -> the (b - items of the bins before)-th item of its bin; per
+    // warp: lane q holds bin q's count, a shuffle scan, a ballot
+    static_assert(SEG_BINS == 32, "one bin per lane");
+    const int ln = threadIdx.x & 31;
+    const uint32_t cq = __ldcg(seg.counts + ln);
+    uint32_t inc = cq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, o);
+      if (ln >= o) inc += y;
+    }
+    const unsigned past = __ballot_sync(FULL, inc <= blockIdx.x);  // bins wholly before b
+    const int bin = __popc(past);
+    if (bin == SEG_BINS) return;
+    const uint32_t before = __shfl_sync(FULL, inc - cq, bin);
+    uint2 it = make_uint2(0u, 0u);
+    if (ln == 0) it = __ldcg(seg.items + (size_t)bin * seg.cap + (blockIdx.x - before));
+    tile = (int)__shfl_sync(FULL, it.x, 0);
+    ks = __shfl_sync(FULL, it.y, 0);
+  } else {
+    tile = order[blockIdx.x];
+  }
   const int tx = tile % p.ntx, ty = tile / p.ntx;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* wb = sred[warp];
@@ -603,16 +661,29 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
   const float lx = (float)G.lxi;
   const F2 ly = f2((float)G.ly0, (float)(G.ly0 + 4));
   const F2 Lp = f2(pixel_lp(p, G.col, G.row0), pixel_lp(p, G.col, G.row1));
-  const uint2 r = ranges[tile];
+  uint2 r = ranges[tile];
   float dcv[2][3], totv[2];
-  bwd_prologue<LOSS, DET>(p, G, io, dcv, totv, tile);
+  // the per-pixel d_background / loss terms: once per tile (its first segment)
+  bwd_prologue<LOSS, DET>(p, G, io, dcv, totv, tile, (ks & ~SEG_WHOLE) == 0);
   const F2 dcr = f2(dcv[0][0], dcv[1][0]), dcg = f2(dcv[0][1], dcv[1][1]),
            dcb = f2(dcv[0][2], dcv[1][2]);
   const F2 tot = f2(totv[0], totv[1]);
   // the replay follows the forward exactly: same entries, same order, same
   // transmittance (so the same activity and the same early exits)
   F2 T = f2(G.in0 ? 1.f : 0.f, G.in1 ? 1.f : 0.f), P = f2s(0.f);
-  bool done = !(G.in0 || G.in1);
+  if (!DET && seg.on && !(ks & SEG_WHOLE)) {
+    const uint32_t s0 = r.x + ks * (uint32_t)VG_SEG;
+    r = make_uint2(s0, min(r.y, s0 + (uint32_t)VG_SEG));
+    if (ks) {
+      // the forward's transmittance at the boundary (bit-identical to the
+      // sequential replay) and the dot-weighted colour in front of it
+      const float4* o = seg.state + ((size_t)(s0 / VG_SEG) * NT + threadIdx.x) * 2;
+      const float4 a = o[0], b = o[1];
+      T = f2(a.x, a.y);
+      P = fma2(dcr, f2(a.z, a.w), fma2(dcg, f2(b.x, b.y), mul2(dcb, f2(b.z, b.w))));
+    }
+  }
+  bool done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);
   // Gaussian-major slots: the staging put entry k's (Gaussian, tile) index in sm[k].d.w
   auto dslot = [&](uint32_t pos, const SRec& s, int k) -> size_t {
     if (!DET) return 0;
@@ -699,6 +770,7 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
       done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);
     }
   }
+  if (VG_CTA_LOG) cta_log_end(p, tile);
 }
 
 // ---------------------------------------------------------------------------
@@ -1078,18 +1150,18 @@ __global__ void __launch_bounds__(NT) k_tomo_bwd(const GRec* __restrict__ rec,
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
-                       int vm_words, cudaStream_t st) {
+                       int vm_words, cudaStream_t st, const SegIO& seg) {
   // n_contrib == NULL: the training-step forward (no counts)
 #define VG_RF(S, C)                                                                             \
   do {                                                                                          \
     if (n_contrib)                                                                              \
       k_render_fwd<S, C, false, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color, \
                                                                final_t, n_contrib, n_act, vmask, \
-                                                               vm_words);                       \
+                                                               vm_words, seg);                  \
     else                                                                                        \
       k_render_fwd<S, C, false, false><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p,      \
                                                                 color, final_t, nullptr, nullptr, \
-                                                                vmask, vm_words);                \
+                                                                vmask, vm_words, seg);           \
   } while (0)
   if (stop && cut) VG_RF(true, true);
   else if (stop) VG_RF(true, false);
@@ -1102,10 +1174,13 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
 #if VG_TU_REST
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
-                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st) {
+                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st,
+                       const SegIO& seg) {
   const bool det = io.det_part != nullptr;
+  // segmented: seg.cap bounds the item count (surplus CTAs exit at once)
+  const int nb = seg.on ? (int)seg.cap : n_tiles;
 #define VG_RB(C, L, D) \
-  k_render_bwd<C, L, D><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words)
+  k_render_bwd<C, L, D><<<nb, NT, 0, st>>>(rec, vals, ranges, order, p, io, vmask, vm_words, seg)
   if (det) {
     if (cut) {
       if (loss) VG_RB(true, 1, true); else VG_RB(true, 0, true);
@@ -1171,7 +1246,8 @@ int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, cons
   unsigned long long z[4] = {0, 0, 0, 0};
   cudaMemcpyToSymbolAsync(g_vg_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
   k_render_fwd<true, true, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p, color,
-                                                        final_t, n_contrib, n_act, nullptr, 0);
+                                                        final_t, n_contrib, n_act, nullptr, 0,
+                                                        SegIO());
   cudaMemcpyFromSymbolAsync(out, g_vg_stats, sizeof(z), 0, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   return (int)cudaGetLastError();

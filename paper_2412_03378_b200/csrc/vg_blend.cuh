@@ -240,7 +240,8 @@ __device__ __forceinline__ void block_flush(float a0, float a1, float a2, double
 // L2), total = dc . color + dT T_final, n_act; d_background and loss sums.
 template <int LOSS, bool DET>
 __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo& G, const BwdIO& io,
-                                             float (&dcv)[2][3], float (&totv)[2], int tile) {
+                                             float (&dcv)[2][3], float (&totv)[2], int tile,
+                                             bool sums = true) {
   float Tfv[2] = {1.f, 1.f};
   double lossv = 0.0;
 #pragma unroll
@@ -268,6 +269,7 @@ __device__ __forceinline__ void bwd_prologue(const BlendParams& p, const LaneGeo
     }
     totv[q] = fmaf(dcv[q][0], cc0, fmaf(dcv[q][1], cc1, fmaf(dcv[q][2], cc2, dT * Tfv[q])));
   }
+  if (!sums) return;  // (CTA-uniform) a later segment of a segmented tile
   __syncthreads();
   if (DET)
     block_flush(dcv[0][0] * Tfv[0] + dcv[1][0] * Tfv[1], dcv[0][1] * Tfv[0] + dcv[1][1] * Tfv[1],

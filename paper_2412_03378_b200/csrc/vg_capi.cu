@@ -71,6 +71,14 @@ struct vg_context {
   double* defer_loss = nullptr;
   float* defer_bg = nullptr;
   Buf vmask;                         // forward -> backward visibility bits (4 rows of P bits)
+  Buf seg_state, seg_items;          // segmented backward (SegIO): boundary states, binned items
+  bool seg_valid = false;            // the last forward recorded depth statistics (atomic mode)
+  bool seg_on = false;               // ... and segmented its backward
+  bool seg_next = false;             // decision for the next view (from the last statistics read)
+  uint32_t seg_thr = 0;              // its split depth
+  unsigned long long* seg_host = nullptr;  // mapped pinned: the last finished forward's decision
+  unsigned long long* seg_host_dev = nullptr;
+  int sm_count = 0;
   int vm_words = 0;
   bool vmask_valid = false;
   unsigned long long* total_host = nullptr;  // {pairs, step-2 span chunks}
@@ -94,6 +102,8 @@ struct vg_context {
   struct Mark { int kind; cudaEvent_t a, b; };
   std::vector<Mark> marks;
   cudaEvent_t fence[2] = {nullptr, nullptr};   // launch fences (fence_mode)
+  unsigned long long* dbg_cta = nullptr;       // vg_debug_cta_log
+  int dbg_cta_n = 0;
 };
 
 static cudaEvent_t pool_event(vg_context* c) {
@@ -246,7 +256,8 @@ static std::vector<Buf*> all_bufs(vg_context* c) {
                 &c->vals0, &c->ranges, &c->n_act, &c->tord, &c->span1,
                 &c->span2, &c->dkey,  &c->perm,  &c->dsort_tmp, &c->frame, &c->lacc,
                 &c->cacc, &c->vmask, &c->dcol, &c->centers, &c->gm, &c->gscratch, &c->det_part, &c->det_cnt, &c->det_off, &c->det_slot,
-                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_gvis4, &c->det_big, &c->det_sums};
+                &c->det_bg, &c->det_loss, &c->det_scan, &c->tpart, &c->det_gvis4, &c->det_big, &c->det_sums,
+                &c->seg_state, &c->seg_items};
 }
 
 void vg_destroy(vg_context* c) {
@@ -256,6 +267,7 @@ void vg_destroy(vg_context* c) {
   for (Buf* b : all_bufs(c))
     if (b->p) cudaFree(buf_base(*b));
   if (c->total_host) cudaFreeHost(c->total_host);
+  if (c->seg_host) cudaFreeHost(c->seg_host);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->count_ready) cudaEventDestroy(c->count_ready);
   for (cudaEvent_t e : c->fence)
@@ -517,6 +529,54 @@ int vg_tile_lists(vg_context* c, int32_t* prims, int32_t* offsets, void* stream)
   return VG_OK;
 }
 
+// VG_SEG_BWD=0 turns the segmented backward off (one CTA per tile in list-length order)
+static bool seg_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("VG_SEG_BWD");
+    m = e ? atoi(e) != 0 : 1;
+  }
+  return m != 0;
+}
+
+// the segmented backward's buffers of the last forward (the bin counters
+// follow the visibility mask, 16-byte aligned, and are cleared with it)
+static SegIO seg_io(vg_context* c) {
+  SegIO s;
+  s.counts = (uint32_t*)((char*)c->vmask.p + ((sizeof(uint32_t) * 4 * (size_t)c->vm_words + 15) & ~(size_t)15));
+  s.decision = c->seg_host_dev;
+  s.slots = (uint32_t)(c->sm_count * VG_BWD_MINB);
+  s.on = c->seg_on;
+  if (!s.on) return s;
+  s.state = (float4*)c->seg_state.p;
+  s.items = (uint2*)c->seg_items.p;
+  s.budget = 2u * (uint32_t)(c->sm_count * VG_BWD_MINB);
+  s.n_tiles = (uint32_t)c->n_tiles;
+  s.cap = s.n_tiles + s.budget;
+  s.thr = c->seg_thr;
+  return s;
+}
+
+// This forward's segmentation: the decision the last finished forward on
+// this context left in mapped host memory (a stale one while the device runs
+// behind the host -- a heuristic either way).
+static int seg_decide(vg_context* c) {
+  if (!c->sm_count) {
+    VG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+    if (c->sm_count < 1) c->sm_count = 1;
+  }
+  if (!c->seg_host) {
+    if (cudaHostAlloc((void**)&c->seg_host, 64, cudaHostAllocMapped) != cudaSuccess)
+      return fail(VG_ENOMEM, "segmented backward: mapped pinned alloc failed");
+    *(volatile unsigned long long*)c->seg_host = 0ull;
+    VG_CUDA(cudaHostGetDevicePointer((void**)&c->seg_host_dev, c->seg_host, 0));
+  }
+  const unsigned long long d = *(volatile unsigned long long*)c->seg_host;
+  c->seg_next = (d & 1ull) != 0;
+  c->seg_thr = (uint32_t)(d >> 32);
+  return VG_OK;
+}
+
 static BlendParams blend_params(const vg_context* c) {
   BlendParams p;
   p.dbg_n = c->scene.n;
@@ -547,6 +607,8 @@ static BlendParams blend_params(const vg_context* c) {
   p.e2cut = (float)(-log1p(-c->opt.alpha_cut) * 1.4426950408889634);
   p.ecut = c->opt.alpha_cut > 0 ? (float)(-log1p(-c->opt.alpha_cut) * (1.0 - 1e-3)) : 0.f;
   for (int i = 0; i < 3; ++i) p.bg[i] = (float)c->scene.background[i];
+  p.dbg_cta = c->dbg_cta;
+  p.dbg_cta_n = c->dbg_cta_n;
   return p;
 }
 
@@ -562,12 +624,27 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   // walks exactly those
   const bool use_vm = c->opt.alpha_cut > 0 && c->pairs > 0 && c->opt.mode != VG_MODE_SPLAT;
   uint32_t* vm = nullptr;
+  SegIO seg;
+  c->seg_valid = use_vm && seg_enabled() && !c->opt.deterministic;
+  c->seg_on = false;
+  if (c->seg_valid) {
+    VG_TRY(seg_decide(c));
+    c->seg_on = c->seg_next;
+  }
   if (use_vm) {
     c->vm_words = (int)((c->pairs + 31) / 32) + 1;
-    const size_t bytes = sizeof(uint32_t) * 4 * (size_t)c->vm_words;
+    // the visibility rows, then the segmented backward's bin counters
+    const size_t bytes = ((sizeof(uint32_t) * 4 * (size_t)c->vm_words + 15) & ~(size_t)15) +
+                         SEG_COUNT_BYTES;
     VG_TRY(ensure(c->vmask, bytes, st));
     VG_CUDA(cudaMemsetAsync(c->vmask.p, 0, bytes, st));
     vm = (uint32_t*)c->vmask.p;
+    if (c->seg_on) {
+      VG_TRY(ensure(c->seg_state, seg_state_bytes(c->pairs), st));
+      VG_TRY(ensure(c->seg_items, sizeof(uint2) * SEG_BINS *
+                                      ((size_t)c->n_tiles + 2 * (size_t)c->sm_count * VG_BWD_MINB), st));
+    }
+    if (c->seg_valid) seg = seg_io(c);
   }
   c->vmask_valid = use_vm;
   {
@@ -580,7 +657,7 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
       launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                         (const uint32_t*)c->tord.p, p,
                         c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
-                        (int*)c->n_act.p, vm, c->vm_words, st);
+                        (int*)c->n_act.p, vm, c->vm_words, st, seg);
   }
   VG_LAUNCHED(c, 1);
   c->have_fwd = true;
@@ -597,6 +674,28 @@ int vg_debug_forward_stats(vg_context* c, float* color, float* final_t, int32_t*
                               (const uint32_t*)c->tord.p, p, color, final_t, n_contrib,
                               (int*)c->n_act.p, out4, (cudaStream_t)stream);
   return e ? fail(VG_ECUDA, "debug stats launch failed") : VG_OK;
+}
+
+// Diagnostic CTA log (volgauss_b200.h).
+int vg_debug_cta_log(vg_context* c, unsigned long long* log, int n) {
+  if (!c) return fail(VG_EINVAL, "vg_debug_cta_log: NULL context");
+  if (!VG_CTA_LOG && log) return fail(VG_EINVAL, "vg_debug_cta_log: needs the profiling build (-DVG_CTA_LOG=1)");
+  c->dbg_cta = log;
+  c->dbg_cta_n = log ? n : 0;
+  return VG_OK;
+}
+
+int vg_debug_segments(vg_context* c, int64_t* items, int32_t* segmented) {
+  if (!c || !items || !segmented) return fail(VG_EINVAL, "vg_debug_segments: NULL argument");
+  *items = 0;
+  *segmented = 0;
+  if (!c->have_fwd || !c->seg_on) return VG_OK;
+  uint32_t h[SEG_BINS];
+  VG_CUDA(cudaDeviceSynchronize());
+  VG_CUDA(cudaMemcpy(h, seg_io(c).counts, sizeof(h), cudaMemcpyDeviceToHost));
+  *segmented = 1;
+  for (int b = 0; b < SEG_BINS; ++b) *items += h[b];
+  return VG_OK;
 }
 
 int vg_n_active(vg_context* c, int32_t* out, void* stream) {
@@ -666,7 +765,9 @@ static int run_param_chain(vg_context* c, const vg_grads& g, cudaStream_t st) {
   return VG_OK;
 }
 
-static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
+// publish: the render backward of an atomic-mode view that recorded depth
+// statistics (the next view's segmentation decision, seg_publish)
+static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st, bool publish = false) {
   const int64_t n = c->scene.n;
   if (n <= 0) return VG_OK;
   float* dcol = nullptr;
@@ -681,9 +782,10 @@ static int finish_view(vg_context* c, vg_grads* g, cudaStream_t st) {
   }
   {
     ProfScope ps(c, VG_K_FINALIZE, st);
+    const SegIO seg = publish ? seg_io(c) : SegIO();
     launch_view_accumulate(n, c->scene, c->cam, (const float*)c->frame.p, (float*)c->acc.p,
                            (float*)c->lacc.p, (float*)c->cacc.p, dcol, center,
-                           c->opt.mode == VG_MODE_SPLAT, st);
+                           c->opt.mode == VG_MODE_SPLAT, st, publish ? &seg : nullptr);
   }
   VG_LAUNCHED(c, 1);
   if (g->accumulate != VG_DEFER) VG_TRY(run_param_chain(c, *g, st));
@@ -852,9 +954,15 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
         launch_splat_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                          (const uint32_t*)c->tord.p, p, target ? 1 : 0, io, st);
       else
+      {
+        // with the forward's visibility mask: (tile, segment) items, heaviest first
+        // (atomic mode: the segment plan, and the next view's decision; a
+        // deterministic backward after an atomic-mode forward: one CTA per tile)
+        const SegIO seg = vm && c->seg_valid && !det ? seg_io(c) : SegIO();
         launch_render_bwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                           (const uint32_t*)c->tord.p, p, c->opt.alpha_cut > 0, target ? 1 : 0, io,
-                          vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st);
+                          vm ? (const uint32_t*)c->vmask.p : nullptr, c->vm_words, st, seg);
+      }
     }
     VG_LAUNCHED(c, 1);
     if (det) {
@@ -868,7 +976,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                          loss_out, st, io.det_gvis4, (uint32_t*)c->det_big.p));
       VG_LAUNCHED(c, 2);
     }
-    VG_TRY(finish_view(c, g, st));
+    VG_TRY(finish_view(c, g, st, vm && c->seg_valid && !det));
   } else {
     // empty scene: d_background = sum of d_color (grad.py:126-128) -- the
     // blend kernel still runs over the (empty) tiles to form it.

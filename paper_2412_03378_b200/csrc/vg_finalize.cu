@@ -43,6 +43,9 @@ struct ViewAccIn {
   float* cacc;           // [3][n] RGB gradient accumulators (SoA: coalesced)
   float* dcol;           // SH scenes: this view's dL/dRGB slab [3][n]
   double* center;        // SH scenes: this view's camera centre (written by thread 0)
+  const uint32_t* seg_counts;          // segmented backward: publish the next view's decision
+  unsigned long long* seg_decision;
+  uint32_t seg_slots;
 };
 
 struct FinalIn {
@@ -55,6 +58,7 @@ struct FinalIn {
 
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (in.seg_decision && i == 0) seg_publish(in.seg_counts, in.seg_decision, in.seg_slots);
   if (i >= in.n) return;
   // all loads issued up front (one memory round trip instead of three)
   float4* a4 = reinterpret_cast<float4*>(in.acc + 16 * i);
@@ -515,9 +519,10 @@ __global__ void __launch_bounds__(128) k_finalize_params(FinalIn in, vg_grads g)
 
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,
-                            bool splat, cudaStream_t st) {
+                            bool splat, cudaStream_t st, const SegIO* seg) {
   if (n <= 0) return;
-  ViewAccIn in{n, s.means, s.scales, s.rotations, s.sh, frame, acc, lacc, cacc, dcol, center};
+  ViewAccIn in{n, s.means, s.scales, s.rotations, s.sh, frame, acc, lacc, cacc, dcol, center,
+               seg ? seg->counts : nullptr, seg ? seg->decision : nullptr, seg ? seg->slots : 1u};
   if (splat) {
     k_view_accumulate_splat<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, c);
     return;

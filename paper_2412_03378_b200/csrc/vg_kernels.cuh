@@ -22,7 +22,114 @@ struct BlendParams {
   // debug builds only (VG_ASSERT bounds, VG_JITTER seed)
   int64_t dbg_n = 0, dbg_pairs = 0;
   unsigned dbg_jitter = 0;
+  // diagnostic CTA log (any build; vg_debug_cta_log): CTA b < dbg_cta_n of a
+  // blend launch writes {start ns, end ns, (SM << 32) | tile} to dbg_cta[3 b]
+  unsigned long long* dbg_cta = nullptr;
+  int dbg_cta_n = 0;
 };
+
+// compiled in only with -DVG_CTA_LOG=1 (build(profile=True)): even unexecuted,
+// the log code changes the backward's register allocation (+3 % on config 3)
+#ifndef VG_CTA_LOG
+#define VG_CTA_LOG 0
+#endif
+// (the start time waits in the log itself: no register is held across the kernel)
+__device__ __forceinline__ void cta_log_begin(const BlendParams& p) {
+  if (VG_CTA_LOG && p.dbg_cta && threadIdx.x == 0 && (int)blockIdx.x < p.dbg_cta_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg_cta[3 * (size_t)blockIdx.x] = t;
+  }
+}
+__device__ __forceinline__ void cta_log_end(const BlendParams& p, int tile) {
+  if (!VG_CTA_LOG || !p.dbg_cta) return;
+  __syncthreads();
+  if (threadIdx.x == 0 && (int)blockIdx.x < p.dbg_cta_n) {
+    unsigned long long t;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    unsigned long long* o = p.dbg_cta + 3 * (size_t)blockIdx.x;
+    o[1] = t;
+    o[2] = ((unsigned long long)sm << 32) | (unsigned)tile;
+  }
+}
+
+#ifndef VG_BWD_MINB
+// backward blend CTAs per SM requested from ptxas.  5: <= 96 registers.  With
+// the cut decided on e (eval_pinhole2) the 80-register budget of 6 CTAs
+// spilled: config 3, 16 views, serial: 6 -> 19.26 ms, 5 -> 18.01 ms, 4 -> 19.26 ms
+#define VG_BWD_MINB 5
+#endif
+
+// Segmented backward (atomic mode).  Every forward that records the
+// visibility mask adds its tiles' walked depths (list entries) to a total and
+// a maximum; after the backward, the per-view accumulation pass turns them
+// into the next view's decision and stores it to mapped host memory
+// (seg_publish: one 8-byte store, no copy, no synchronisation, and no code in
+// the register-bound blend kernels).
+// When the previous view on the context had a tile deeper than the per-slot
+// share of its total work (max depth x backward CTA slots > total depth: its
+// backward ended on a few long tiles), the host turns segmentation on for the
+// next view (SegIO::on), and that forward also (a) stores, at every VG_SEG-entry
+// boundary of a tile's list that it reaches, each pixel's transmittance and
+// colour sums (state: two float4 per thread, at index boundary / VG_SEG --
+// unique, since boundaries of different tiles lie more than VG_SEG apart), and
+// (b) appends its tile's backward work items to SEG_BINS bins by work (half
+// an octave per bin, heaviest first): VG_SEG-entry segments for a tile deeper
+// than `thr` (half the per-slot share, within a budget of extra items), one
+// whole-tile item otherwise.  The backward then maps its CTA index over the
+// bins in order and runs every item as an independent CTA, a segment starting
+// its replay from the recorded state; otherwise it runs one CTA per tile in
+// list-length order.  No planning launch: the counters sit after the
+// visibility mask and are cleared with it.  Deterministic mode never
+// segments: a segment's replay seeds its running sum from the forward's
+// colour sums, which rounds differently from the unsegmented replay, and the
+// decision depends on the previous view.  (Config 4: backward -29 %, step
+// -3 %; config 3 never segments.)
+#ifndef VG_SEG
+#define VG_SEG 1024
+#endif
+static_assert((VG_SEG & (VG_SEG - 1)) == 0 && VG_SEG >= 256, "VG_SEG: a power of two >= BATCH");
+constexpr int SEG_BINS = 32;
+constexpr uint32_t SEG_WHOLE = 0x80000000u;  // item flag: the whole tile list
+struct SegIO {
+  float4* state = nullptr;       // forward writes, backward reads
+  uint32_t* counts = nullptr;    // [SEG_BINS] items per bin, extra-item budget used, pad,
+                                 // then 2 x uint64 {total depth, max depth} of this forward
+  uint2* items = nullptr;        // [SEG_BINS][cap] (tile, segment | SEG_WHOLE)
+  uint32_t cap = 0;              // items per bin: n_tiles + budget
+  uint32_t budget = 0;           // extra (split) items allowed
+  uint32_t thr = 0;              // split tiles deeper than this
+  uint32_t n_tiles = 0;
+  uint32_t slots = 1;            // backward CTA slots (SMs x resident CTAs)
+  int on = 0;                    // this view is segmented
+  unsigned long long* decision = nullptr;  // mapped host: (thr << 32) | on, for the next view
+};
+constexpr int SEG_THREADS = 128;    // threads of a blend CTA (NT in vg_blend.cuh)
+inline size_t seg_state_bytes(int64_t pairs) {
+  return sizeof(float4) * 2 * SEG_THREADS * (size_t)(pairs / VG_SEG + 1);
+}
+constexpr int SEG_STATS = SEG_BINS + 4;  // uint32 index of the uint64 stats
+constexpr size_t SEG_COUNT_BYTES = sizeof(uint32_t) * SEG_STATS + 2 * sizeof(unsigned long long);
+// the next view's decision from this view's (finished) forward statistics
+__device__ __forceinline__ void seg_publish(const uint32_t* counts, unsigned long long* decision,
+                                            uint32_t slots) {
+  const unsigned long long* st = reinterpret_cast<const unsigned long long*>(counts + SEG_STATS);
+  const unsigned long long total = __ldcg(st), mx = __ldcg(st + 1);
+  const unsigned long long on = total > 0 && mx * slots > total;
+  const unsigned long long thr = min(0xffffffffull, max(2ull * VG_SEG, total / (2ull * slots)));
+  *(volatile unsigned long long*)decision = (thr << 32) | on;
+}
+// half-octave bins: 0 = 2^14 entries or more, ..., SEG_BINS - 1 = none
+__device__ __forceinline__ int seg_bin(uint32_t w) {
+  if (w == 0) return SEG_BINS - 1;
+  const int e = 31 - __clz(w);                                  // floor(log2 w)
+  if (e >= 15) return 0;
+  const int upper = e ? (int)((w >> (e - 1)) & 1u) : 0;         // w >= 1.5 * 2^e
+  const int b = 2 * (14 - e) + 1 - upper;
+  return b < 0 ? 0 : (b > SEG_BINS - 2 ? SEG_BINS - 2 : b);
+}
 
 struct BwdIO {
   const float* color;
@@ -88,13 +195,14 @@ void launch_gamma_sort(int n_tiles, const uint2* ranges, uint32_t* vals, const d
 void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
-                       int vm_words, cudaStream_t st);
+                       int vm_words, cudaStream_t st, const SegIO& seg = SegIO());
 int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                         const uint32_t* order, const BlendParams& p, float* color, float* final_t,
                         int* n_contrib, int* n_act, unsigned long long* out, cudaStream_t st);
 void launch_render_bwd(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                        const uint32_t* order, const BlendParams& p, bool cut, int loss,
-                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st);
+                       const BwdIO& io, const uint32_t* vmask, int vm_words, cudaStream_t st,
+                       const SegIO& seg = SegIO());
 // Tomography splits each tile's pair list over `splits` CTAs (small detectors
 // with long lists would otherwise leave most SMs idle): the forward writes
 // per-split partial images into `part` (splits * H * W floats, unused when
@@ -110,9 +218,10 @@ void launch_tomo_bwd(int n_tiles, int splits, int ray, int loss, const GRec* rec
                      float* acc, uint8_t* visible, float* det_part, double* det_loss,
                      cudaStream_t st);
 // SH scenes: dcol / center receive this view's dL/dRGB slab [3][n] and camera centre
+// seg (nullable): publish the segmentation decision (seg_publish) from block 0
 void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const float* frame,
                             float* acc, float* lacc, float* cacc, float* dcol, double* center,
-                            bool splat, cudaStream_t st);
+                            bool splat, cudaStream_t st, const SegIO* seg = nullptr);
 // returns the number of kernels launched; SH scenes fold the sh_views slabs of dcol
 void launch_merge_acc(int64_t n, float* dst, float* src, cudaStream_t st);
 int launch_finalize_params(int64_t n, const vg_scene& s, float* lacc, float* cacc,

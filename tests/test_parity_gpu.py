@@ -1273,3 +1273,109 @@ def test_hostio_round_trips():
     assert hostio.to_device(np.zeros((0, 3)), dev, (0, 3)).shape == (0, 3)
     assert hostio.to_host(torch.zeros((0, 3), device=dev)).shape == (0, 3)
     assert hostio.all_finite(g) and not hostio.all_finite(g / 0.0)
+
+
+def _deep_scene(n=5000, seed=11):
+    """Thin, overlapping Gaussians: ~5000-entry tile lists walked to depths of
+    1500-5000 before the early stop, i.e. several VG_SEG (1024) segments per
+    tile for the segmented backward."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(seed)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    return SimpleNamespace(means=rng.normal(0, 0.25, (n, 3)), scales=rng.uniform(0.25, 0.5, (n, 3)),
+                           rotations=q, thetas=rng.uniform(0.002, 0.006, n),
+                           colors=rng.uniform(0, 1, (n, 3)), background=np.array([0.2, 0.1, 0.3]))
+
+
+_SEG_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import test_parity_gpu as T
+g = T._deep_engine_backward(np.load(sys.argv[2])["dc"], passes=1)[0]
+np.savez(sys.argv[3], **g)
+"""
+
+
+def _segments(ctx):
+    import ctypes
+    import paper_2412_03378_b200._lib as L
+    n, flag = ctypes.c_int64(), ctypes.c_int32()
+    L.check(L.load().vg_debug_segments(ctx.handle, ctypes.byref(n), ctypes.byref(flag)),
+            "vg_debug_segments")
+    return int(flag.value), int(n.value)
+
+
+def _deep_engine_backward(dc, passes=2, deterministic=False):
+    """Forward + explicit-gradient backward of the deep scene, `passes` times
+    on one atomic-mode engine context; per pass the gradient fields and the
+    context's segment plan (segmented flag, item count)."""
+    import torch
+    from paper_2412_03378_b200.engine import Engine
+    s = _deep_scene()
+    cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=36, fov_x_deg=40.0)
+    eng = Engine(deterministic=deterministic)
+    ds = eng.upload(s)
+    eng.prepare(ds, cam)
+    dct = torch.from_numpy(np.ascontiguousarray(dc, dtype=np.float32)).cuda()
+    out = []
+    for _ in range(passes):
+        color, tfin, _ = eng.forward(counts=False)
+        grads = eng.new_grads(ds)
+        eng.backward(color, tfin, dct, grads)
+        torch.cuda.synchronize()
+        sg = grads.to_scene_grads("analytic", False)
+        out.append(({f: np.array(getattr(sg, f), dtype=np.float64) for f in GRAD_FIELDS + ["d_background"]},
+                    _segments(eng.ctx)))
+    return [g for g, _ in out] if passes == 1 else out
+
+
+def test_segmented_backward_deep_tiles(tmp_path):
+    """Tiles walked past several VG_SEG boundaries.  The first atomic-mode
+    forward on a context only records depth statistics; the next view's
+    backward then splits this scene's deep tiles into (tile, segment) items
+    that run as independent CTAs from the forward's boundary states.  Both
+    passes against the oracle (parity contract); the segmented pass equal to
+    the unsegmented one within float32 rounding, and to the backward of a
+    library with segmentation off (VG_SEG_BWD=0, child process); the
+    deterministic backward never segments (bitwise reproducible)."""
+    import subprocess
+    import sys
+    s = _deep_scene()
+    cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=36, fov_x_deg=40.0)
+    dc = np.random.default_rng(5).uniform(-1, 1, (36, 40, 3))
+    flags = dict(early_stop=O.EARLY_STOP_T, alpha_cut=O.ALPHA_CUT)
+    dprep = vg().prepare(s, cam)
+    out = vg().render(s, cam, prep=dprep)
+    na = dprep.n_active()
+    assert na.max() > 4 * 1024, "the scene must span several segments"
+    prep = O.prepare(s, cam)
+    knife = device_knife_mask(prep, s, flags, out.n_contrib, na)
+    knife_cap(int(knife.sum()), knife.size, "deep backward")
+    dck = dc * ~knife[..., None]
+    ref = O.backward(s, cam, dck, prep=prep)
+    (g1, p1), (g2, p2) = _deep_engine_backward(dck)
+    assert p1 == (0, 0), "no statistics before the first forward"
+    assert p2[0] == 1 and p2[1] > 2 * 9, p2
+    for f in GRAD_FIELDS + ["d_background"]:
+        check_field(g1[f], getattr(ref, f), f"deep unsegmented {f}")
+        check_field(g2[f], getattr(ref, f), f"deep segmented {f}")
+        np.testing.assert_allclose(g2[f], g1[f], rtol=1e-4, atol=1e-5 * max(1.0, float(np.abs(g1[f]).max())),
+                                   err_msg=f)
+    # a library with segmentation off, same upstream gradient
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    np.savez(str(tmp_path / "dc.npz"), dc=dck)
+    env = dict(os.environ, VG_SEG_BWD="0")
+    r = subprocess.run([sys.executable, "-c", _SEG_CHILD, root, str(tmp_path / "dc.npz"),
+                        str(tmp_path / "unseg.npz")], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    unseg = np.load(str(tmp_path / "unseg.npz"))
+    for f in GRAD_FIELDS + ["d_background"]:
+        np.testing.assert_allclose(g2[f], unseg[f], rtol=1e-4,
+                                   atol=1e-5 * max(1.0, float(np.abs(unseg[f]).max())), err_msg=f)
+    # deterministic mode: never segmented, bitwise reproducible
+    (d1, q1), (d2, q2) = _deep_engine_backward(dck, deterministic=True)
+    assert q1 == q2 == (0, 0)
+    for f in GRAD_FIELDS + ["d_background"]:
+        assert np.array_equal(d1[f], d2[f]), f
+        check_field(d1[f], getattr(ref, f), f"deep det {f}")
