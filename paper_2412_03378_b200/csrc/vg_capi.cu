@@ -539,6 +539,18 @@ static bool seg_enabled() {
   return m != 0;
 }
 
+// VG_SEG_RATIO: segment a view when its deepest tile exceeds this multiple of
+// the per-slot share of its work (default 1)
+static float seg_ratio() {
+  static float r = -1.f;
+  if (r < 0.f) {
+    const char* e = getenv("VG_SEG_RATIO");
+    r = e ? (float)atof(e) : 1.f;
+    if (!(r > 0.f)) r = 1.f;
+  }
+  return r;
+}
+
 // the segmented backward's buffers of the last forward (the bin counters
 // follow the visibility mask, 16-byte aligned, and are cleared with it)
 static SegIO seg_io(vg_context* c) {
@@ -546,6 +558,7 @@ static SegIO seg_io(vg_context* c) {
   s.counts = (uint32_t*)((char*)c->vmask.p + ((sizeof(uint32_t) * 4 * (size_t)c->vm_words + 15) & ~(size_t)15));
   s.decision = c->seg_host_dev;
   s.slots = (uint32_t)(c->sm_count * VG_BWD_MINB);
+  s.ratio = seg_ratio();
   s.on = c->seg_on;
   if (!s.on) return s;
   s.state = (float4*)c->seg_state.p;

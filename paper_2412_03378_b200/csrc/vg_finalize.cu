@@ -46,6 +46,7 @@ struct ViewAccIn {
   const uint32_t* seg_counts;          // segmented backward: publish the next view's decision
   unsigned long long* seg_decision;
   uint32_t seg_slots;
+  float seg_ratio;
 };
 
 struct FinalIn {
@@ -58,7 +59,7 @@ struct FinalIn {
 
 __global__ void __launch_bounds__(256) k_view_accumulate(ViewAccIn in, CamK c) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (in.seg_decision && i == 0) seg_publish(in.seg_counts, in.seg_decision, in.seg_slots);
+  if (in.seg_decision && i == 0) seg_publish(in.seg_counts, in.seg_decision, in.seg_slots, in.seg_ratio);
   if (i >= in.n) return;
   // all loads issued up front (one memory round trip instead of three)
   float4* a4 = reinterpret_cast<float4*>(in.acc + 16 * i);
@@ -522,7 +523,8 @@ void launch_view_accumulate(int64_t n, const vg_scene& s, const CamK& c, const f
                             bool splat, cudaStream_t st, const SegIO* seg) {
   if (n <= 0) return;
   ViewAccIn in{n, s.means, s.scales, s.rotations, s.sh, frame, acc, lacc, cacc, dcol, center,
-               seg ? seg->counts : nullptr, seg ? seg->decision : nullptr, seg ? seg->slots : 1u};
+               seg ? seg->counts : nullptr, seg ? seg->decision : nullptr, seg ? seg->slots : 1u,
+               seg ? seg->ratio : 1.f};
   if (splat) {
     k_view_accumulate_splat<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(in, c);
     return;

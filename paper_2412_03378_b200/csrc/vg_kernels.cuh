@@ -103,6 +103,7 @@ struct SegIO {
   uint32_t thr = 0;              // split tiles deeper than this
   uint32_t n_tiles = 0;
   uint32_t slots = 1;            // backward CTA slots (SMs x resident CTAs)
+  float ratio = 1.f;             // segment when max depth x slots > ratio x total depth
   int on = 0;                    // this view is segmented
   unsigned long long* decision = nullptr;  // mapped host: (thr << 32) | on, for the next view
 };
@@ -114,10 +115,10 @@ constexpr int SEG_STATS = SEG_BINS + 4;  // uint32 index of the uint64 stats
 constexpr size_t SEG_COUNT_BYTES = sizeof(uint32_t) * SEG_STATS + 2 * sizeof(unsigned long long);
 // the next view's decision from this view's (finished) forward statistics
 __device__ __forceinline__ void seg_publish(const uint32_t* counts, unsigned long long* decision,
-                                            uint32_t slots) {
+                                            uint32_t slots, float ratio) {
   const unsigned long long* st = reinterpret_cast<const unsigned long long*>(counts + SEG_STATS);
   const unsigned long long total = __ldcg(st), mx = __ldcg(st + 1);
-  const unsigned long long on = total > 0 && mx * slots > total;
+  const unsigned long long on = total > 0 && (double)mx * slots > (double)ratio * (double)total;
   const unsigned long long thr = min(0xffffffffull, max(2ull * VG_SEG, total / (2ull * slots)));
   *(volatile unsigned long long*)decision = (thr << 32) | on;
 }

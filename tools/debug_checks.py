@@ -12,7 +12,8 @@ schedule-perturbed reruns.
 2. runs every device path (tools/sanitize_run.py: render, atomic and
    deterministic backward, gamma, splat, cone/parallel tomography, the
    pipelined SH multi-view step, the fused Adam step, ray marcher, voxelizer)
-   plus an engine workload whose outputs live in guarded tensors, under the
+   plus an engine workload whose outputs live in guarded tensors and a
+   deep-tile view whose second atomic-mode backward is segmented, under the
    checking build with warp-schedule jitter seeds 0, 1, 2 (VG_JITTER sleeps a
    hashed number of ns at every batch and chunk of the blend kernels);
 3. checks: no trap, every guard band of every context intact, every output
@@ -103,6 +104,32 @@ def child(out_path):
         res[f"ncon_det{int(det)}"] = ncon.cpu().numpy()
         res[f"grads_det{int(det)}"] = flat.cpu().numpy()
         res[f"loss_det{int(det)}"] = np.array(float(loss))
+    # the segmented backward (atomic mode): deep tiles, second pass segmented
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import test_parity_gpu as T
+    deep = T._deep_scene()
+    dcam = T.vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=36, fov_x_deg=40.0)
+    deng = Engine(deterministic=False)
+    dds = deng.upload(deep)
+    deng.prepare(dds, dcam)
+    ddc = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, (36, 40, 3)).astype(np.float32)).cuda()
+    for k in range(2):
+        bc, color = guarded(torch, (36, 40, 3), torch.float32, dev)
+        bt, tfin = guarded(torch, (36, 40), torch.float32, dev)
+        _lib.check(lib.vg_render_forward(deng.ctx.handle, _lib.ptr(color), _lib.ptr(tfin), None,
+                                         deng.stream()), "forward")
+        grads = deng.new_grads(dds)
+        deng.backward(color, tfin, ddc, grads)
+        torch.cuda.synchronize()
+        seg = T._segments(deng.ctx)
+        for tag, b in (("deep color", bc), ("deep T", bt)):
+            if not guards_ok(torch, b):
+                bad_guards.append((f"output {tag} pass {k}", 1, -1))
+        res[f"deep_seg{k}"] = np.array(seg[0])
+        res[f"deep_grads{k}"] = grads.flat.cpu().numpy()
+    check_ctx("deep segmented engine", deng.ctx)
+    if res["deep_seg1"] != 1:
+        bad_guards.append(("deep view not segmented", 1, -1))
     # the pipelined deterministic multi-view step (three contexts, two streams)
     big = configs.large(n=3000, width=96, height=64, n_views=5)
     eng = Engine(deterministic=True)
@@ -158,7 +185,7 @@ def main():
             outs[(kind, seed)] = dict(np.load(path))
     ref = outs.get(("release", 0))
     lines += ["\n## Bitwise comparisons against the release build (seed 0)\n",
-              "| run | forward image + n_contrib | deterministic grads + loss | pipelined det step | atomic grads max rel diff |",
+              "| run | forward image + n_contrib | deterministic grads + loss | pipelined det step | atomic grads (incl. segmented) max rel diff |",
               "|---|---|---|---|---|"]
     for key, o in outs.items():
         if ref is None or key == ("release", 0):
@@ -168,6 +195,8 @@ def main():
         stp = np.array_equal(o["step_grads"], ref["step_grads"]) and np.array_equal(o["step_loss"], ref["step_loss"])
         d = np.abs(o["grads_det0"].astype(np.float64) - ref["grads_det0"])
         rel = float(d.max() / max(np.abs(ref["grads_det0"]).max(), 1e-30))
+        ds = np.abs(o["deep_grads1"].astype(np.float64) - ref["deep_grads1"])
+        rel = max(rel, float(ds.max() / max(np.abs(ref["deep_grads1"]).max(), 1e-30)))
         lines.append(f"| {key[0]} seed {key[1]} | {'identical' if fwd else 'DIFFERS'} | "
                      f"{'identical' if det else 'DIFFERS'} | {'identical' if stp else 'DIFFERS'} | {rel:.2e} |")
         ok &= fwd and det and stp
