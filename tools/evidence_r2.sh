@@ -1,4 +1,9 @@
-set -x
+# Round-2 evidence pass on the GPU box (outputs under gpurun_out/; the files
+# judged are copied to profiles/):  bash tools/evidence_r2.sh
+#   GPU tests, smoke, the checking-build run (debug_checks), bench lines of
+#   configs 3/2/4/5 + deterministic config 3, the opaque launch-balance log
+#   (walk_stats, profiling build) and an ncu --set full capture of a
+#   segmented opaque backward.
 python -m pytest tests -x -q -m gpu > gpurun_out/ev_tests.log 2>&1; echo tests=$? > gpurun_out/ev_status.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; echo smoke=$? >> gpurun_out/ev_status.log
 python tools/debug_checks.py --out gpurun_out/debug_checks_r2.md > gpurun_out/ev_debug.log 2>&1; echo debug=$? >> gpurun_out/ev_status.log
