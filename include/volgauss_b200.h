@@ -383,16 +383,19 @@ int vg_allreduce_grads(vg_context* ctx, void* nccl_comm, float* flat, int64_t co
 int vg_debug_forward_stats(vg_context* ctx, float* color, float* final_t, int32_t* n_contrib,
                            unsigned long long* out4, void* stream);
 
-/* Diagnostic (load balance, tools/walk_stats.py): while log != NULL, every
- * forward / backward blend launch of this context writes, for CTA b < n,
- * {start ns, end ns, (SM id << 32) | tile} (globaltimer) to the device buffer
- * log[3 b .. 3 b + 2].  log = NULL turns it off. */
+/* Diagnostic (load balance, tools/walk_stats.py; profiling build only,
+ * -DVG_CTA_LOG=1, else VG_EINVAL): while log != NULL, every forward /
+ * backward blend launch of this context writes, for CTA b < n, {start ns,
+ * end ns, (SM id << 32) | tile} (globaltimer) and, for the forward, each
+ * warp's chunk-walk and staging cycles to the device buffer log[16 b ..
+ * 16 b + 10].  log = NULL turns it off. */
 int vg_debug_cta_log(vg_context* ctx, unsigned long long* log, int n);
 
-/* Diagnostic: the segmented backward's plan for the last forward of this
- * context -- *segmented = 1 if its backward runs (tile, segment) work items
- * (vg_kernels.cuh, SegIO), *items = their count (else 0, one CTA per tile).
- * Synchronises the device. */
+/* Diagnostic: the load-balance plan of the last forward of this context --
+ * *segmented bit 0: its backward runs (tile, segment) work items
+ * (vg_kernels.cuh, SegIO), *items = their count (else 0, one CTA per tile);
+ * bit 1: its deepest tiles ran through the deep-tile forward.  Synchronises
+ * the device. */
 int vg_debug_segments(vg_context* ctx, int64_t* items, int32_t* segmented);
 
 /* Roofline denominators measured at the live clock: FP32 FFMA lane-ops/s and

@@ -53,6 +53,11 @@
 #ifndef VG_FWD_MINB
 #define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
 #endif
+#ifndef VG_DEEP_ILP
+// deep-tile forward: entries evaluated ahead (4 and 8 measured the same; the
+// deepest config-4 tile alone on an SM: 521 -> 391 us)
+#define VG_DEEP_ILP 4
+#endif
 #ifndef VG_SEEN_REDUX
 #define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
 #endif
@@ -234,8 +239,11 @@ __device__ unsigned long long g_vg_stats[4];  // debug: processed / visible warp
 // COUNTS: also produce n_contrib and n_active (the render API and the
 // roofline statistics); the training step's forward skips them -- the
 // backward re-derives activity from its own transmittance replay.
-template <bool STOP, bool CUT, bool STATS = false, bool COUNTS = true>
-__global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __restrict__ rec,
+// DEEP: the latency-bound variant for the few very deep tiles of a tail-bound
+// view (run beside the regular launch): VG_DEEP_ILP visible entries' alpha
+// factors evaluated ahead of their (sequential) compositing, at low occupancy
+template <bool STOP, bool CUT, bool STATS = false, bool COUNTS = true, bool DEEP = false>
+__global__ void __launch_bounds__(NT, DEEP ? 2 : VG_FWD_MINB) k_render_fwd(const GRec* __restrict__ rec,
                                                    const uint32_t* __restrict__ vals,
                                                    const uint2* __restrict__ ranges,
                                                    const uint32_t* __restrict__ order,
@@ -270,9 +278,15 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
   // after the loop, min(base, r.y) is the end of the last batch walked (the
   // tile's depth)
   uint32_t base = r.x;
+#if VG_CTA_LOG
+  unsigned long long w_walk = 0, w_stage = 0;  // this warp's cycles: chunk walk, staging + its barrier
+#endif
   for (; base < r.y; base += BATCH) {
     VG_JITTER(p.dbg_jitter, base);
     if (__syncthreads_count(done) == NT) break;
+#if VG_CTA_LOG
+    const unsigned long long c0 = clock64();
+#endif
     if (seg.on && base != r.x && ((base - r.x) & (VG_SEG - 1)) == 0) {
       // a segment boundary: the state the backward's replay of the next segment starts from
       float4* o = seg.state + ((size_t)(base / VG_SEG) * NT + threadIdx.x) * 2;
@@ -285,6 +299,10 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         smask[sidx] = (uint8_t)stage(sm, sidx, rec, chk_gid(p, vals[i]), tx * TILE, ty * TILE, CUT, p.ecut, sdmax);
     }
     __syncthreads();
+#if VG_CTA_LOG
+    const unsigned long long c1 = clock64();
+    w_stage += c1 - c0;
+#endif
     const int nb = min((uint32_t)BATCH, r.y - base);
     const int jb = (int)(base - r.x) + 1;
     for (int c = 0; c < nb && !__all_sync(FULL, done); c += 32) {
@@ -293,7 +311,7 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
       unsigned bits = __ballot_sync(FULL, vb);
       unsigned seen = 0;  // entries of this chunk with a visible pixel in this warp's block
       // composite one evaluated entry (front to back; T carries the order)
-      auto composite = [&](int k, const SRec& s, const Pair2& e) {
+      auto composite_ex = [&](int k, const float4& d, F2 ex) {
         if (STOP) {
           // active iff the transmittance in front is >= stop (raster.py:384-385);
           // n_act = 1 + index of the last active processed entry
@@ -307,16 +325,16 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
         }
         // cut entries carry the factor 1 (eval_pinhole2), inactive ones the
         // floor 1: either way om = 1, no contribution, no count
-        const float om0 = fmaxf(lo(e.ex), fl0), om1 = fmaxf(hi(e.ex), fl1);
+        const float om0 = fmaxf(lo(ex), fl0), om1 = fmaxf(hi(ex), fl1);
         if (COUNTS) {
           nc0 += om0 < 1.f;
           nc1 += om1 < 1.f;
         }
         const F2 om = f2(om0, om1);
         const F2 w = mul2(sub2(f2s(1.f), om), T);
-        Cr = fma2(w, f2s(s.d.x), Cr);
-        Cg = fma2(w, f2s(s.d.y), Cg);
-        Cb = fma2(w, f2s(s.d.z), Cb);
+        Cr = fma2(w, f2s(d.x), Cr);
+        Cg = fma2(w, f2s(d.y), Cg);
+        Cb = fma2(w, f2s(d.z), Cb);
         T = mul2(T, om);
 #if VG_SEEN_REDUX
         // per-lane bits, OR-reduced over the warp once per chunk
@@ -329,6 +347,29 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
           st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
         }
       };
+      auto composite = [&](int k, const SRec& s, const Pair2& e) { composite_ex(k, s.d, e.ex); };
+      if constexpr (DEEP) {
+        // up to VG_DEEP_ILP visible entries evaluated, then composited in order
+        // (branch-free: missing entries repeat the last one, so the
+        // evaluations are straight-line code the scheduler interleaves)
+        while (bits) {
+          int kk[VG_DEEP_ILP];
+          F2 xe[VG_DEEP_ILP];
+          int m = 0;
+#pragma unroll
+          for (int j = 0; j < VG_DEEP_ILP; ++j) {
+            const bool v = bits != 0u;
+            kk[j] = v ? c + __ffs(bits) - 1 : kk[j > 0 ? j - 1 : 0];
+            m = v ? j + 1 : m;
+            bits &= bits - 1u;
+          }
+#pragma unroll
+          for (int j = 0; j < VG_DEEP_ILP; ++j) xe[j] = eval_pinhole2<CUT>(sm[kk[j]], lx, ly, Lp, p.e2cut).ex;
+#pragma unroll
+          for (int j = 0; j < VG_DEEP_ILP; ++j)
+            if (j < m) composite_ex(kk[j], sm[kk[j]].d, xe[j]);
+        }
+      } else
       // two visible entries per iteration: their (independent) alpha
       // evaluations overlap before the short compositing chain
       while (bits) {
@@ -364,7 +405,16 @@ __global__ void __launch_bounds__(NT, VG_FWD_MINB) k_render_fwd(const GRec* __re
       if (STATS) st_tot += min(32, nb - c);
       if (STOP) done = !(lo(T) >= p.stop) && !(hi(T) >= p.stop);
     }
+#if VG_CTA_LOG
+    w_walk += clock64() - c1;
+#endif
   }
+#if VG_CTA_LOG
+  if (p.dbg_cta && lane == 0 && (int)blockIdx.x < p.dbg_cta_n) {
+    p.dbg_cta[VG_CTA_LOG_STRIDE * (size_t)blockIdx.x + 3 + warp] = w_walk;
+    p.dbg_cta[VG_CTA_LOG_STRIDE * (size_t)blockIdx.x + 7 + warp] = w_stage;
+  }
+#endif
   if (STATS && lane == 0) {
     atomicAdd(&g_vg_stats[0], st_proc);
     atomicAdd(&g_vg_stats[1], st_vis);
@@ -1151,6 +1201,10 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
                        int vm_words, cudaStream_t st, const SegIO& seg) {
+#if VG_CTA_LOG
+  // profiling build: VG_FWD_GRID=k launches only the k heaviest tiles (load-balance experiments)
+  if (const char* g = getenv("VG_FWD_GRID")) n_tiles = min(n_tiles, atoi(g));
+#endif
   // n_contrib == NULL: the training-step forward (no counts)
 #define VG_RF(S, C)                                                                             \
   do {                                                                                          \
@@ -1168,6 +1222,21 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
   else if (cut) VG_RF(false, true);
   else VG_RF(false, false);
 #undef VG_RF
+}
+
+void launch_render_fwd_deep(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                            const uint32_t* order, const BlendParams& p, bool stop, bool cut,
+                            float* color, float* final_t, uint32_t* vmask, int vm_words,
+                            cudaStream_t st, const SegIO& seg) {
+#define VG_RFD(S, C)                                                                              \
+  k_render_fwd<S, C, false, false, true><<<n_tiles, NT, 0, st>>>(rec, vals, ranges, order, p,     \
+                                                                  color, final_t, nullptr, nullptr, \
+                                                                  vmask, vm_words, seg)
+  if (stop && cut) VG_RFD(true, true);
+  else if (stop) VG_RFD(true, false);
+  else if (cut) VG_RFD(false, true);
+  else VG_RFD(false, false);
+#undef VG_RFD
 }
 #endif  // VG_TU_FWD
 

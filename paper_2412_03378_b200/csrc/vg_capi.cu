@@ -3,6 +3,7 @@
 // sort -> K4 ranges -> K5/K6/K8 tile kernels -> K7 finalize.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -78,6 +79,9 @@ struct vg_context {
   uint32_t seg_thr = 0;              // its split depth
   unsigned long long* seg_host = nullptr;  // mapped pinned: the last finished forward's decision
   unsigned long long* seg_host_dev = nullptr;
+  cudaStream_t side = nullptr;       // deep-tile forward beside the regular launch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int last_deep = 0;                 // tiles the last forward ran through the deep variant
   int sm_count = 0;
   int vm_words = 0;
   bool vmask_valid = false;
@@ -268,6 +272,9 @@ void vg_destroy(vg_context* c) {
     if (b->p) cudaFree(buf_base(*b));
   if (c->total_host) cudaFreeHost(c->total_host);
   if (c->seg_host) cudaFreeHost(c->seg_host);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   if (c->count_ready) cudaEventDestroy(c->count_ready);
   for (cudaEvent_t e : c->fence)
@@ -573,6 +580,28 @@ static SegIO seg_io(vg_context* c) {
 // This forward's segmentation: the decision the last finished forward on
 // this context left in mapped host memory (a stale one while the device runs
 // behind the host -- a heuristic either way).
+// VG_DEEP_TILES: tiles the deep-tile forward takes (default: 4 per SM -- config 4
+// step 32.6 ms without, 148: 32.4, 296: 31.8, 444-592: 31.3, 888: 31.6, all: 32.2; 0: off)
+static int deep_tiles(const vg_context* c) {
+  static int k = -2;
+  if (k == -2) {
+    const char* e = getenv("VG_DEEP_TILES");
+    k = e ? std::max(0, atoi(e)) : -1;
+  }
+  return k < 0 ? 4 * c->sm_count : k;
+}
+
+// the context's side stream (highest priority) and fork / join events
+static int side_stream(vg_context* c) {
+  if (c->side) return VG_OK;
+  int lo = 0, hi = 0;
+  VG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  VG_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  VG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  VG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  return VG_OK;
+}
+
 static int seg_decide(vg_context* c) {
   if (!c->sm_count) {
     VG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
@@ -638,11 +667,15 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
   const bool use_vm = c->opt.alpha_cut > 0 && c->pairs > 0 && c->opt.mode != VG_MODE_SPLAT;
   uint32_t* vm = nullptr;
   SegIO seg;
-  c->seg_valid = use_vm && seg_enabled() && !c->opt.deterministic;
+  // depth statistics in both modes; a tail-bound view (the previous view's
+  // decision) gets the deep-tile forward, and in atomic mode the segmented backward
+  c->seg_valid = use_vm && seg_enabled();
   c->seg_on = false;
+  bool tail = false;
   if (c->seg_valid) {
     VG_TRY(seg_decide(c));
-    c->seg_on = c->seg_next;
+    tail = c->seg_next;
+    c->seg_on = tail && !c->opt.deterministic;
   }
   if (use_vm) {
     c->vm_words = (int)((c->pairs + 31) / 32) + 1;
@@ -666,11 +699,36 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
       launch_splat_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                        (const uint32_t*)c->tord.p, p, color, final_t, n_contrib,
                        n_contrib ? (int*)c->n_act.p : nullptr, st);
-    else
-      launch_render_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
-                        (const uint32_t*)c->tord.p, p,
-                        c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
-                        (int*)c->n_act.p, vm, c->vm_words, st, seg);
+    else {
+      // the training forward of a tail-bound view: the deepest (longest-list)
+      // tiles through the latency-bound variant on a side stream, beside the
+      // regular launch over the others
+      const int deep = tail && !n_contrib ? std::min(c->n_tiles, deep_tiles(c)) : 0;
+      if (deep > 0) {
+        VG_TRY(side_stream(c));
+        VG_CUDA(cudaEventRecord(c->ev_fork, st));
+        VG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        BlendParams pd = p;
+        if (pd.dbg_cta) {  // profiling log: the deep CTAs after the regular ones
+          pd.dbg_cta += (size_t)VG_CTA_LOG_STRIDE * (size_t)(c->n_tiles - deep);
+          pd.dbg_cta_n = std::max(0, pd.dbg_cta_n - (c->n_tiles - deep));
+        }
+        launch_render_fwd_deep(deep, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                               (const uint32_t*)c->tord.p, pd, c->opt.early_stop > 0,
+                               c->opt.alpha_cut > 0, color, final_t, vm, c->vm_words, c->side, seg);
+        VG_LAUNCHED(c, 1);
+      }
+      if (c->n_tiles > deep)
+        launch_render_fwd(c->n_tiles - deep, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
+                          (const uint32_t*)c->tord.p + deep, p,
+                          c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
+                          (int*)c->n_act.p, vm, c->vm_words, st, seg);
+      if (deep > 0) {
+        VG_CUDA(cudaEventRecord(c->ev_join, c->side));
+        VG_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+      }
+      c->last_deep = deep;
+    }
   }
   VG_LAUNCHED(c, 1);
   c->have_fwd = true;
@@ -702,11 +760,13 @@ int vg_debug_segments(vg_context* c, int64_t* items, int32_t* segmented) {
   if (!c || !items || !segmented) return fail(VG_EINVAL, "vg_debug_segments: NULL argument");
   *items = 0;
   *segmented = 0;
-  if (!c->have_fwd || !c->seg_on) return VG_OK;
+  if (!c->have_fwd) return VG_OK;
+  *segmented = c->last_deep > 0 ? 2 : 0;
+  if (!c->seg_on) return VG_OK;
   uint32_t h[SEG_BINS];
   VG_CUDA(cudaDeviceSynchronize());
   VG_CUDA(cudaMemcpy(h, seg_io(c).counts, sizeof(h), cudaMemcpyDeviceToHost));
-  *segmented = 1;
+  *segmented |= 1;
   for (int b = 0; b < SEG_BINS; ++b) *items += h[b];
   return VG_OK;
 }
@@ -989,7 +1049,7 @@ static int render_bwd_common(vg_context* c, const float* color, const float* fin
                          loss_out, st, io.det_gvis4, (uint32_t*)c->det_big.p));
       VG_LAUNCHED(c, 2);
     }
-    VG_TRY(finish_view(c, g, st, vm && c->seg_valid && !det));
+    VG_TRY(finish_view(c, g, st, vm && c->seg_valid));
   } else {
     // empty scene: d_background = sum of d_color (grad.py:126-128) -- the
     // blend kernel still runs over the (empty) tiles to form it.

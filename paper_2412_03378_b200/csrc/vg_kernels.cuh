@@ -22,8 +22,9 @@ struct BlendParams {
   // debug builds only (VG_ASSERT bounds, VG_JITTER seed)
   int64_t dbg_n = 0, dbg_pairs = 0;
   unsigned dbg_jitter = 0;
-  // diagnostic CTA log (any build; vg_debug_cta_log): CTA b < dbg_cta_n of a
-  // blend launch writes {start ns, end ns, (SM << 32) | tile} to dbg_cta[3 b]
+  // diagnostic CTA log (profiling build; vg_debug_cta_log): CTA b < dbg_cta_n
+  // of a blend launch writes {start ns, end ns, (SM << 32) | tile, forward:
+  // per-warp walk cycles [4], per-warp staging cycles [4]} to dbg_cta[16 b]
   unsigned long long* dbg_cta = nullptr;
   int dbg_cta_n = 0;
 };
@@ -33,12 +34,13 @@ struct BlendParams {
 #ifndef VG_CTA_LOG
 #define VG_CTA_LOG 0
 #endif
+constexpr int VG_CTA_LOG_STRIDE = 16;  // uint64 per CTA in the log
 // (the start time waits in the log itself: no register is held across the kernel)
 __device__ __forceinline__ void cta_log_begin(const BlendParams& p) {
   if (VG_CTA_LOG && p.dbg_cta && threadIdx.x == 0 && (int)blockIdx.x < p.dbg_cta_n) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.dbg_cta[3 * (size_t)blockIdx.x] = t;
+    p.dbg_cta[VG_CTA_LOG_STRIDE * (size_t)blockIdx.x] = t;
   }
 }
 __device__ __forceinline__ void cta_log_end(const BlendParams& p, int tile) {
@@ -49,7 +51,7 @@ __device__ __forceinline__ void cta_log_end(const BlendParams& p, int tile) {
     unsigned sm;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    unsigned long long* o = p.dbg_cta + 3 * (size_t)blockIdx.x;
+    unsigned long long* o = p.dbg_cta + VG_CTA_LOG_STRIDE * (size_t)blockIdx.x;
     o[1] = t;
     o[2] = ((unsigned long long)sm << 32) | (unsigned)tile;
   }
@@ -197,6 +199,12 @@ void launch_render_fwd(int n_tiles, const GRec* rec, const uint32_t* vals, const
                        const uint32_t* order, const BlendParams& p, bool stop, bool cut,
                        float* color, float* final_t, int* n_contrib, int* n_act, uint32_t* vmask,
                        int vm_words, cudaStream_t st, const SegIO& seg = SegIO());
+// the latency-bound variant for the deepest tiles of a tail-bound view (the
+// training forward; run beside launch_render_fwd on the remaining tiles)
+void launch_render_fwd_deep(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
+                            const uint32_t* order, const BlendParams& p, bool stop, bool cut,
+                            float* color, float* final_t, uint32_t* vmask, int vm_words,
+                            cudaStream_t st, const SegIO& seg);
 int debug_forward_stats(int n_tiles, const GRec* rec, const uint32_t* vals, const uint2* ranges,
                         const uint32_t* order, const BlendParams& p, float* color, float* final_t,
                         int* n_contrib, int* n_act, unsigned long long* out, cudaStream_t st);

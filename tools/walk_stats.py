@@ -24,8 +24,12 @@ sys.path.insert(0, ROOT)
 BATCH = 256
 
 
+STRIDE = 16  # uint64 per CTA (VG_CTA_LOG_STRIDE)
+
+
 def cta_stats(log, nt, d_tile):
-    ct = log.cpu().numpy().reshape(nt, 3)
+    full = log.cpu().numpy().reshape(nt, STRIDE)
+    ct = full[:, :3]
     t0 = ct[:, 0].min()
     st, en = (ct[:, 0] - t0) / 1e3, (ct[:, 1] - t0) / 1e3  # us
     sm = ct[:, 2] >> 32
@@ -34,7 +38,7 @@ def cta_stats(log, nt, d_tile):
     span = en.max()
     sm_end = np.array([en[sm == k].max() if (sm == k).any() else 0 for k in range(148)])
     order = np.argsort(-dur)
-    return {
+    out = {
         "span_us": round(float(span), 1),
         "sum_cta_us": round(float(dur.sum()), 1),
         "mean_resident": round(float(dur.sum() / span / 148), 2),
@@ -45,6 +49,14 @@ def cta_stats(log, nt, d_tile):
         "last_cta_start_us": round(float(st.max()), 1),
         "corr_dur_depth": round(float(np.corrcoef(dur, d_tile[tile])[0, 1]), 3),
     }
+    walk, stage = full[:, 3:7].astype(np.float64), full[:, 7:11].astype(np.float64)
+    if walk.any():
+        # forward: per-warp cycles walking chunks / staging (incl. its barrier), longest CTAs
+        out["longest_warp_cycles(walk[4],stage[4])"] = [
+            (int(tile[i]), [int(x) for x in walk[i]], [int(x) for x in stage[i]]) for i in order[:3]]
+        tot = walk.sum(1) + 1e-9
+        out["walk_max_over_mean"] = round(float(np.mean(walk.max(1) / (tot / 4))), 3)
+    return out
 
 
 def main():
@@ -77,9 +89,9 @@ def main():
         staged = np.minimum(np.ceil(d_tile / BATCH) * BATCH, d_tile + BATCH)  # upper bound
         proc, vis, tot = eng.forward_stats()
         nt = th * tw
-        log = torch.zeros(3 * nt, dtype=torch.int64, device="cuda")
+        log = torch.zeros(STRIDE * nt, dtype=torch.int64, device="cuda")
         _lib.check(eng.lib.vg_debug_cta_log(eng.ctx.handle, _lib.ptr(log), nt), "vg_debug_cta_log")
-        color, tfin, _ = eng.forward()
+        color, tfin, _ = eng.forward(counts=False)  # the training forward (deep tiles when tail-bound)
         torch.cuda.synchronize()
         cta = {"fwd": cta_stats(log, nt, d_tile)}
         log.zero_()
