@@ -1,8 +1,15 @@
+"""Load-balance probe of the forward blend on one view (profiling build,
+-DVG_CTA_LOG=1): per-CTA span / residency and per-warp walk / staging cycles
+of a training forward.  VG_FWD_GRID=k (profiling build) launches only the k
+longest-list tiles, e.g. k = 148 runs the heaviest tiles alone, one per SM.
+
+    LIBP=build/prof/libvolgauss_b200_prof.so VG_FWD_GRID=148 CFG=opaque python tools/deep_probe.py
+"""
 import os, sys, json
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tools')
 import numpy as np
 from paper_2412_03378_b200 import _lib as L
-L.LIB_PATH = os.environ["LIBP"]
+L.LIB_PATH = os.environ.get("LIBP") or __import__("paper_2412_03378_b200.build", fromlist=["build"]).build(profile=True)
 import torch
 from paper_2412_03378_b200 import configs
 from paper_2412_03378_b200.engine import Engine
