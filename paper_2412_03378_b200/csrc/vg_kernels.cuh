@@ -87,8 +87,10 @@ __device__ __forceinline__ void cta_log_end(const BlendParams& p, int tile) {
 // visibility mask and are cleared with it.  Deterministic mode never
 // segments: a segment's replay seeds its running sum from the forward's
 // colour sums, which rounds differently from the unsegmented replay, and the
-// decision depends on the previous view.  (Config 4: backward -29 %, step
-// -3 %; config 3 never segments.)
+// decision depends on the previous view.  The same decision sends a
+// tail-bound view's longest-list tiles through the deep-tile forward (both
+// modes: its results are bit-identical).  (Config 4: backward -29 %, step
+// 33.6 -> 31.3 ms with both; config 3 never segments.)
 #ifndef VG_SEG
 #define VG_SEG 1024
 #endif

@@ -128,7 +128,7 @@ def child(out_path):
         res[f"deep_seg{k}"] = np.array(seg[0])
         res[f"deep_grads{k}"] = grads.flat.cpu().numpy()
     check_ctx("deep segmented engine", deng.ctx)
-    if res["deep_seg1"] != 1:
+    if not (int(res["deep_seg1"]) & 1):  # bit 0: segmented backward
         bad_guards.append(("deep view not segmented", 1, -1))
     # the pipelined deterministic multi-view step (three contexts, two streams)
     big = configs.large(n=3000, width=96, height=64, n_views=5)
