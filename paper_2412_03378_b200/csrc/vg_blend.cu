@@ -58,12 +58,6 @@
 // deepest config-4 tile alone on an SM: 521 -> 391 us)
 #define VG_DEEP_ILP 4
 #endif
-#ifndef VG_BWD_BF
-#define VG_BWD_BF 0  // A/B: branch-free pair evaluation in the backward
-#endif
-#ifndef VG_FWD_BF
-#define VG_FWD_BF 0  // A/B: branch-free pair evaluation in the regular forward
-#endif
 #ifndef VG_SEEN_REDUX
 #define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
 #endif
@@ -353,60 +347,45 @@ __global__ void __launch_bounds__(NT, DEEP ? 2 : VG_FWD_MINB) k_render_fwd(const
           st_vis += __any_sync(FULL, om0 < 1.f || om1 < 1.f) ? 1 : 0;
         }
       };
-      auto composite = [&](int k, const SRec& s, const Pair2& e) { composite_ex(k, s.d, e.ex); };
       if constexpr (DEEP) {
         // up to VG_DEEP_ILP visible entries evaluated, then composited in order
+        constexpr int ILP = VG_DEEP_ILP;
         // (branch-free: missing entries repeat the last one, so the
         // evaluations are straight-line code the scheduler interleaves)
         while (bits) {
-          int kk[VG_DEEP_ILP];
-          F2 xe[VG_DEEP_ILP];
+          int kk[ILP];
+          F2 xe[ILP];
           int m = 0;
 #pragma unroll
-          for (int j = 0; j < VG_DEEP_ILP; ++j) {
+          for (int j = 0; j < ILP; ++j) {
             const bool v = bits != 0u;
             kk[j] = v ? c + __ffs(bits) - 1 : kk[j > 0 ? j - 1 : 0];
             m = v ? j + 1 : m;
             bits &= bits - 1u;
           }
 #pragma unroll
-          for (int j = 0; j < VG_DEEP_ILP; ++j) xe[j] = eval_pinhole2<CUT>(sm[kk[j]], lx, ly, Lp, p.e2cut).ex;
+          for (int j = 0; j < ILP; ++j) xe[j] = eval_pinhole2<CUT>(sm[kk[j]], lx, ly, Lp, p.e2cut).ex;
 #pragma unroll
-          for (int j = 0; j < VG_DEEP_ILP; ++j)
+          for (int j = 0; j < ILP; ++j)
             if (j < m) composite_ex(kk[j], sm[kk[j]].d, xe[j]);
         }
-      } else if (VG_FWD_BF) {
-        // (branch-free pair: the second evaluation repeats the first when missing)
+      } else {
+        // two visible entries per iteration, evaluated branch-free (the second
+        // repeats the first when the chunk has no second entry) so that both
+        // evaluations are straight-line code the scheduler interleaves before
+        // the short compositing chain (forward -5.7 % on config 3 against
+        // evaluating the second entry under its own branch)
         while (bits) {
           const int k = c + __ffs(bits) - 1;
           bits &= bits - 1;
           const bool two = bits != 0u;
           const int kb = two ? c + __ffs(bits) - 1 : k;
           bits &= bits - 1;
+          VG_ASSERT(k < nb && kb < nb);
           const F2 ea = eval_pinhole2<CUT>(sm[k], lx, ly, Lp, p.e2cut).ex;
           const F2 eb = eval_pinhole2<CUT>(sm[kb], lx, ly, Lp, p.e2cut).ex;
           composite_ex(k, sm[k].d, ea);
           if (two) composite_ex(kb, sm[kb].d, eb);
-        }
-      } else
-      // two visible entries per iteration: their (independent) alpha
-      // evaluations overlap before the short compositing chain
-      while (bits) {
-        const int k = c + __ffs(bits) - 1;
-        bits &= bits - 1;
-        VG_ASSERT(k < nb);
-        const SRec s = sm[k];
-        const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
-        if (bits) {
-          const int kb = c + __ffs(bits) - 1;
-          bits &= bits - 1;
-          VG_ASSERT(kb < nb);
-          const SRec sb = sm[kb];
-          const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
-          composite(k, s, e);
-          composite(kb, sb, eb);
-        } else {
-          composite(k, s, e);
         }
       }
 #if VG_SEEN_REDUX
@@ -808,29 +787,6 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
       }
       // two visible entries per iteration: both alpha evaluations are
       // issued before the replay chain of the first
-#if VG_BWD_BF
-      // (branch-free: the second evaluation repeats the first when the chunk
-      // has no second entry, so both are straight-line code)
-      while (bits) {
-        const int k = c + __ffs(bits) - 1;
-        bits &= bits - 1;
-        const bool two = bits != 0u;
-        const int kb = two ? c + __ffs(bits) - 1 : k;
-        bits &= bits - 1;
-        const SRec s = sm[k];
-        const SRec sb = sm[kb];
-        const Pair2 e = eval_pinhole2<CUT>(s, lx, ly, Lp, p.e2cut);
-        const Pair2 eb = eval_pinhole2<CUT>(sb, lx, ly, Lp, p.e2cut);
-        const size_t ia = dslot(base + k, s, k);
-        if (two) {
-          const size_t ib = dslot(base + kb, sb, kb);
-          bwd_entry2<CUT, DET>(s, e, sb, eb, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io,
-                               ia, ib, wb);
-        } else {
-          bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
-        }
-      }
-#else
       while (bits) {
         const int k = c + __ffs(bits) - 1;
         bits &= bits - 1;
@@ -859,7 +815,6 @@ __global__ void __launch_bounds__(NT, VG_BWD_MINB) k_render_bwd(const GRec* __re
           bwd_entry<CUT, DET>(s, e, G.in0, G.in1, dcr, dcg, dcb, tot, p, T, P, lane, io, ia, wb);
         }
       }
-#endif
       done = !(G.in0 && lo(T) >= p.stop) && !(G.in1 && hi(T) >= p.stop);
     }
   }
