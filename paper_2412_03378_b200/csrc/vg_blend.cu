@@ -58,9 +58,6 @@
 // deepest config-4 tile alone on an SM: 521 -> 391 us)
 #define VG_DEEP_ILP 4
 #endif
-#ifndef VG_BWD_FASTCHAIN
-#define VG_BWD_FASTCHAIN 0  // A/B: shorter transmittance dependency chain in the backward replay
-#endif
 #ifndef VG_SEEN_REDUX
 #define VG_SEEN_REDUX 1  // forward: per-lane visibility bits, one warp OR per chunk
 #endif
@@ -588,24 +585,12 @@ __device__ __forceinline__ Replay bwd_replay(const SRec& s, const Pair2& e, bool
                                              F2 dcg, F2 dcb, F2 tot, const BlendParams& p, F2& T,
                                              F2& P) {
   const bool act0 = in0 && lo(T) >= p.stop, act1 = in1 && hi(T) >= p.stop;
-#if VG_BWD_FASTCHAIN
-  // the same values with a shorter dependency on T: an inactive entry's
-  // factor is exactly 1 (ex <= 1), so T' = active ? T max(ex, 1 - clamp) : T
-  const F2 mx = f2(fmaxf(lo(e.ex), p.cc), fmaxf(hi(e.ex), p.cc));
-  const F2 Tm = mul2(T, mx);
-  const float om0 = act0 ? lo(mx) : 1.f, om1 = act1 ? hi(mx) : 1.f;
-  const F2 om = f2(om0, om1);
-  Replay r;
-  r.contrib = mul2(sub2(f2s(1.f), om), T);
-  const F2 Tn = f2(act0 ? lo(Tm) : lo(T), act1 ? hi(Tm) : hi(T));
-#else
   const float om0 = fmaxf(lo(e.ex), act0 ? p.cc : 1.f);
   const float om1 = fmaxf(hi(e.ex), act1 ? p.cc : 1.f);
   const F2 om = f2(om0, om1);
   Replay r;
   r.contrib = mul2(sub2(f2s(1.f), om), T);
   const F2 Tn = mul2(T, om);
-#endif
   const F2 dot = fma2(dcr, f2s(s.d.x), fma2(dcg, f2s(s.d.y), mul2(dcb, f2s(s.d.z))));
   P = fma2(dot, r.contrib, P);
   T = Tn;
