@@ -1381,3 +1381,54 @@ def test_segmented_backward_deep_tiles(tmp_path):
     for f in GRAD_FIELDS + ["d_background"]:
         assert np.array_equal(d1[f], d2[f]), f
         check_field(d1[f], getattr(ref, f), f"deep det {f}")
+
+
+_TAIL_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import test_parity_gpu as T
+flat, loss, _ = T._tail_step()
+np.savez(sys.argv[2], flat=flat, loss=np.array(loss))
+"""
+
+
+def _tail_step(steps=2):
+    """Two multi-view steps (three rotating contexts, two blend streams,
+    atomic mode) of a small opaque scene; every context's later views are
+    tail-bound (a 256 x 256 view has far fewer tiles than backward CTA slots).
+    Returns the last step's flat gradient buffer, its loss and the per-context
+    load-balance plans of the last views."""
+    import torch
+    from paper_2412_03378_b200 import configs
+    from paper_2412_03378_b200.engine import Engine
+    from paper_2412_03378_b200.multiview import ViewShardedStep
+    cfg = configs.opaque(n=60000, size=256, n_views=6)
+    eng = Engine(deterministic=False)
+    ds = eng.upload(cfg.scene)
+    targets = {v: torch.from_numpy(cfg.target(v, (256, 256, 3))).cuda() for v in range(6)}
+    step = ViewShardedStep(eng, ds, cfg.cameras, targets)
+    for _ in range(steps):
+        loss = float(step())
+    torch.cuda.synchronize()
+    plans = [_segments(e.ctx) for e in step.engines]
+    return step.grads.flat.cpu().numpy().astype(np.float64), loss, plans
+
+
+def test_tail_bound_multiview_step_matches_unsegmented(tmp_path):
+    """The production multi-view step with the load-balance paths engaged
+    (deep-tile forward beside the regular launch on each context's side
+    stream, segmented backward) equals the same step with them off
+    (VG_SEG_BWD=0, child process) within float32 rounding."""
+    import subprocess
+    import sys
+    flat, loss, plans = _tail_step()
+    assert all(p[0] == 3 for p in plans), plans
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp_path / "off.npz")
+    env = dict(os.environ, VG_SEG_BWD="0")
+    r = subprocess.run([sys.executable, "-c", _TAIL_CHILD, root, path], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    off = np.load(path)
+    assert abs(loss - float(off["loss"])) <= 1e-6 * abs(float(off["loss"])), (loss, float(off["loss"]))
+    np.testing.assert_allclose(flat, off["flat"], rtol=1e-4, atol=1e-5 * float(np.abs(off["flat"]).max()))
