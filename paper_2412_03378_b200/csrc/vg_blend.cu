@@ -51,7 +51,10 @@
 
 // minimum resident CTAs per SM requested from ptxas (register budget); A/B knobs
 #ifndef VG_FWD_MINB
-#define VG_FWD_MINB 10  // <= 48 registers: 10 CTAs per SM (A/B: tools/ab_bench.sh)
+// 8: <= 64 registers.  With the branch-free entry pairs, 8 CTAs / 63 registers
+// beat 10 / 48 (config 3 step 121.5 -> 120.3 ms, config 2 3.86 -> 3.77 ms);
+// 6, 7, 9 and 12 were slower
+#define VG_FWD_MINB 8
 #endif
 #ifndef VG_DEEP_ILP
 // deep-tile forward: entries evaluated ahead (4 and 8 measured the same; the
