@@ -580,15 +580,16 @@ static SegIO seg_io(vg_context* c) {
 // This forward's segmentation: the decision the last finished forward on
 // this context left in mapped host memory (a stale one while the device runs
 // behind the host -- a heuristic either way).
-// VG_DEEP_TILES: tiles the deep-tile forward takes (default: 4 per SM -- config 4
-// step 32.6 ms without, 148: 32.4, 296: 31.8, 444-592: 31.3, 888: 31.6, all: 32.2; 0: off)
+// VG_DEEP_TILES: tiles the deep-tile forward takes (default: 2 per SM; 0: off).
+// Config 4 step with the 63-register regular forward: 148: 30.9 ms, 222-370:
+// 30.6, 444: 30.8, 592: 31.0, 888: 31.7 (with the 48-register one 4 per SM was best)
 static int deep_tiles(const vg_context* c) {
   static int k = -2;
   if (k == -2) {
     const char* e = getenv("VG_DEEP_TILES");
     k = e ? std::max(0, atoi(e)) : -1;
   }
-  return k < 0 ? 4 * c->sm_count : k;
+  return k < 0 ? 2 * c->sm_count : k;
 }
 
 // the context's side stream (highest priority) and fork / join events
