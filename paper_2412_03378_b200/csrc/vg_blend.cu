@@ -304,8 +304,9 @@ __global__ void __launch_bounds__(NT, DEEP ? 2 : VG_FWD_MINB) k_render_fwd(const
     }
     if constexpr (DEEP) {
       // both of this thread's entries: list values, then both records, in
-      // flight together (a missing entry re-reads the batch's first; the
-      // regular kernel would spill at its 48 registers: forward +13 %)
+      // flight together (a missing entry re-reads the batch's first; in the
+      // regular kernel the two records spill: forward +13 % at 48 and at 63
+      // registers)
       static_assert(BATCH == 2 * NT, "two staged entries per thread");
       const uint32_t i0 = base + threadIdx.x, i1 = i0 + NT;
       const bool v0 = i0 < r.y, v1 = i1 < r.y;
