@@ -694,13 +694,15 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
     if (c->seg_valid) seg = seg_io(c);
   }
   c->vmask_valid = use_vm;
+  c->last_deep = 0;
   {
     ProfScope ps(c, VG_K_RENDER_FWD, st);
-    if (c->opt.mode == VG_MODE_SPLAT)
+    if (c->opt.mode == VG_MODE_SPLAT) {
       launch_splat_fwd(c->n_tiles, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                        (const uint32_t*)c->tord.p, p, color, final_t, n_contrib,
                        n_contrib ? (int*)c->n_act.p : nullptr, st);
-    else {
+      VG_LAUNCHED(c, 1);
+    } else {
       // the training forward of a tail-bound view: the deepest (longest-list)
       // tiles through the latency-bound variant on a side stream, beside the
       // regular launch over the others
@@ -719,11 +721,13 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
                                c->opt.alpha_cut > 0, color, final_t, vm, c->vm_words, c->side, seg);
         VG_LAUNCHED(c, 1);
       }
-      if (c->n_tiles > deep)
+      if (c->n_tiles > deep) {
         launch_render_fwd(c->n_tiles - deep, (const GRec*)c->rec.p, c->vals, (const uint2*)c->ranges.p,
                           (const uint32_t*)c->tord.p + deep, p,
                           c->opt.early_stop > 0, c->opt.alpha_cut > 0, color, final_t, n_contrib,
                           (int*)c->n_act.p, vm, c->vm_words, st, seg);
+        VG_LAUNCHED(c, 1);
+      }
       if (deep > 0) {
         VG_CUDA(cudaEventRecord(c->ev_join, c->side));
         VG_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
@@ -731,7 +735,6 @@ int vg_render_forward(vg_context* c, float* color, float* final_t, int32_t* n_co
       c->last_deep = deep;
     }
   }
-  VG_LAUNCHED(c, 1);
   c->have_fwd = true;
   c->have_counts = n_contrib != nullptr;
   return VG_OK;
