@@ -1306,7 +1306,7 @@ def _segments(ctx):
     return int(flag.value), int(n.value)
 
 
-def _deep_engine_backward(dc, passes=2, deterministic=False):
+def _deep_engine_backward(dc, passes=2, deterministic=False, sort_by="depth"):
     """Forward + explicit-gradient backward of the deep scene, `passes` times
     on one atomic-mode engine context; per pass the gradient fields and the
     context's segment plan (segmented flag, item count)."""
@@ -1314,7 +1314,7 @@ def _deep_engine_backward(dc, passes=2, deterministic=False):
     from paper_2412_03378_b200.engine import Engine
     s = _deep_scene()
     cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=36, fov_x_deg=40.0)
-    eng = Engine(deterministic=deterministic)
+    eng = Engine(deterministic=deterministic, sort_by=sort_by)
     ds = eng.upload(s)
     eng.prepare(ds, cam)
     dct = torch.from_numpy(np.ascontiguousarray(dc, dtype=np.float32)).cuda()
@@ -1432,3 +1432,26 @@ def test_tail_bound_multiview_step_matches_unsegmented(tmp_path):
     off = np.load(path)
     assert abs(loss - float(off["loss"])) <= 1e-6 * abs(float(off["loss"])), (loss, float(off["loss"]))
     np.testing.assert_allclose(flat, off["flat"], rtol=1e-4, atol=1e-5 * float(np.abs(off["flat"]).max()))
+
+
+def test_segmented_backward_deep_tiles_gamma_order():
+    """The load-balance paths on sort_by='gamma' lists (the same blend
+    kernels over per-tile gamma-sorted lists): both engine passes -- the
+    second with the deep-tile forward and the segmented backward -- against
+    the oracle composited in gamma order."""
+    s = _deep_scene()
+    cam = vg().look_at([0, 0, -3.0], [0, 0, 0], width=40, height=36, fov_x_deg=40.0)
+    dc = np.random.default_rng(6).uniform(-1, 1, (36, 40, 3))
+    flags = dict(early_stop=O.EARLY_STOP_T, alpha_cut=O.ALPHA_CUT)
+    dprep = vg().prepare(s, cam, sort_by="gamma")
+    out = vg().render(s, cam, sort_by="gamma", prep=dprep)
+    gprep = O.prepare(s, cam, sort_by="gamma")
+    knife = device_knife_mask(gprep, s, flags, out.n_contrib, dprep.n_active())
+    knife_cap(int(knife.sum()), knife.size, "deep gamma backward")
+    dck = dc * ~knife[..., None]
+    ref = O.backward(s, cam, dck, prep=gprep)
+    (g1, p1), (g2, p2) = _deep_engine_backward(dck, sort_by="gamma")
+    assert p1 == (0, 0) and p2[0] == 3, (p1, p2)
+    for f in GRAD_FIELDS + ["d_background"]:
+        check_field(g1[f], getattr(ref, f), f"deep gamma unsegmented {f}")
+        check_field(g2[f], getattr(ref, f), f"deep gamma segmented {f}")
