@@ -253,6 +253,14 @@ def _full_size_check(scene, cam, n_random=5, seed=5, n_busy=3):
     rg = O.backward(scene, cam, dc, prep=oprep, tiles=tiles)
     for f in GRAD_FIELDS:
         check_field(getattr(g, f), getattr(rg, f), f)
+    # the atomic-mode backward on the same context: the earlier forwards left
+    # depth statistics, so a tail-bound view now runs the deep-tile forward
+    # and the segmented backward
+    ga = vg().backward(scene, cam, dc, prep=prep, deterministic=False)
+    plan = _segments(prep.ctx)
+    for f in GRAD_FIELDS:
+        check_field(getattr(ga, f), getattr(rg, f), f"atomic {f}")
+    return plan
 
 
 def test_full_size_large_view_tiles_and_sampled_pixels():
@@ -281,8 +289,12 @@ def test_full_size_opaque_view():
     from paper_2412_03378_b200 import configs
     cfg = configs.opaque()
     scene = _f64_scene(cfg.scene)
-    for v, seed in ((3, 7), (11, 8), (26, 9)):
-        _full_size_check(scene, cfg.cameras[v], n_random=3, seed=seed, n_busy=2)
+    plans = [_full_size_check(scene, cfg.cameras[v], n_random=3, seed=seed, n_busy=2)
+             for v, seed in ((3, 7), (11, 8), (26, 9))]
+    # the segmented backward ran at full size on the tail-bound views (the
+    # drop-in backward's forward counts n_contrib, so it never takes the
+    # deep-tile variant -- that is the engine's training forward)
+    assert sum(p[0] & 1 for p in plans) >= 2, plans
 
 
 def test_full_size_tomography_parallel_view():
